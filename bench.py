@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""Benchmark: XNOR-conv forward on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C3|C2k3|C2k5|C2k7|C1] [--variant popc|b1mma] [--no-cpu]
+
+One STEP = one pass of the hot path over one batch: K1 sign+bit-pack+|x|-mean,
+K2 K map, K3+K4 XNOR-popcount conv with the alpha*K epilogue, for every
+(image, filter) pair of the layer.  Weight packing is outside the timed region
+(the reference's set_weights is untimed too, bench.py:234-237).
+
+Workload at N=1: BASELINE config 3 (the roofline headline): 3x3, C=O=256,
+56x56, batch 256 per GPU (weak scaling under torchrun: every rank runs its own
+256-image shard, no collective on the data path).  Inputs are 822 MB > L2
+(126 MB), so no explicit L2 flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the reference's own
+CPU implementation (oracle/_ref: xnorconv._kernels_cy.xnor_reconstruct, built
+from the reference .pyx) on the host cores, same metric and config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (N per GPU, C, H, W, O, k)
+    "C1": (1, 64, 32, 32, 64, 3),
+    "C2k3": (64, 128, 64, 64, 128, 3),
+    "C2k5": (64, 128, 64, 64, 128, 5),
+    "C2k7": (64, 128, 64, 64, 128, 7),
+    "C3": (256, 256, 56, 56, 256, 3),
+}
+CONFIG_TEXT = {
+    "C1": "single XNOR conv layer 3x3, C_in=C_out=64, 32x32, batch 1",
+    "C2k3": "XNOR conv 3x3, C=128, 64x64, batch 64", "C2k5": "XNOR conv 5x5, C=128, 64x64, batch 64",
+    "C2k7": "XNOR conv 7x7, C=128, 64x64, batch 64",
+    "C3": "ResNet-stage binary conv 3x3, C=256, 56x56, batch 256 (BASELINE config 3)",
+}
+METRIC = "XNOR-conv Gbinop/s and images/sec at 1/2/4/8 B200 vs host-CPU reference"
+POPC_LANES_PER_CLK_SM = 15.95  # measured, profiles/int_peaks_r1.json
+
+
+def binops(N, C, H, W, O, k):
+    pad = (k - 1) // 2
+    oh, ow = H + 2 * pad - k + 1, W + 2 * pad - k + 1
+    return 2.0 * N * O * oh * ow * C * k * k  # 1 bit-MAC = 2 binops
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                     "--format=csv,noheader,nounits", "-lms", "100"],
+                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        while not self._stop.is_set():
+            line = proc.stdout.readline()
+            if not line:
+                break
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+        proc.terminate()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=2)
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        busy = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        mask = 0
+        for s in busy:
+            mask |= s[2]
+        return {"sm_mhz": statistics.median(s[0] for s in busy), "sm_max_mhz": max(s[1] for s in busy),
+                "reasons": [v for k, v in self.REASONS.items() if mask & k and k != 0x1],
+                "samples": len(busy)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(value: float, ws: int, device) -> float:
+    if ws == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ CPU reference
+def _ref_native_build():
+    """Rebuild the reference kernels with the reference's -march=native on this host
+    (setup.py:10) from the C that cython generated in the build container."""
+    stamp = os.path.join(ROOT, "oracle", "_ref", ".native_host")
+    host = platform.node()
+    if os.path.exists(stamp) and open(stamp).read().strip() == host:
+        return "native"
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "_kernels_cy.c")):
+        return "prebuilt"
+    try:
+        subprocess.run([os.path.join(ROOT, "oracle", "build_ref.sh"), "--cc-only"], check=True,
+                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=300,
+                       env=dict(os.environ, PYTHON=sys.executable))
+        with open(stamp, "w") as fh:
+            fh.write(host)
+        return "native"
+    except Exception:
+        return "prebuilt"
+
+
+class RefRunner:
+    """The reference's fused ConvWorkspace.run (pipeline.py:142-150 ->
+    _kernels_cy.pyx:242 xnor_reconstruct) over (image, filter) pairs, filters
+    prebuilt and inputs padded outside the timing (the reference protocol,
+    bench.py:5-7,234-237)."""
+
+    def __init__(self, cfg, seed=0):
+        import numpy as np
+        from oracle import oracle as O
+        self.march = _ref_native_build()
+        self.O = O
+        self.R = O.RefKernels()
+        N, C, H, W, Oc, k = cfg
+        self.cfg = cfg
+        self.k = k
+        self.pad = (k - 1) // 2
+        rng = np.random.default_rng((seed, 3))
+        n_img = min(N, 8)
+        self.x = rng.uniform(-1, 1, (n_img, C, H, W)).astype(np.float32)
+        w = rng.uniform(-1, 1, (Oc, C, k, k)).astype(np.float32)
+        self.filters = [O.build_filter(w[o]) for o in range(Oc)]
+        self.ws = [self.R.workspace(self.x[i], self.pad, k, k) for i in range(n_img)]
+        self.threads = os.cpu_count() or 1
+
+    def pair_rate(self, budget_s: float, threads=None):
+        """Time (image, filter) pairs for ~budget_s seconds; returns (s_per_pair, pairs)."""
+        threads = threads or self.threads
+        padded, out = self.ws[0]
+        self.R.run(padded, out, self.filters[0], self.k, self.k, threads)  # warm the OpenMP team
+        pairs, t0 = 0, time.perf_counter()
+        while True:
+            padded, out = self.ws[(pairs // len(self.filters)) % len(self.ws)]
+            self.R.run(padded, out, self.filters[pairs % len(self.filters)], self.k, self.k, threads)
+            pairs += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s and pairs >= 4:
+                return el / pairs, pairs
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, cfg_name):
+    import numpy as np
+    import torch
+    from paper_2007_14178_b200 import XnorConv2d, ops
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    N, C, H, W, Oc, k = CONFIGS[cfg_name]
+    pad = (k - 1) // 2
+    # synthetic data, seeded per rank: rank r holds images [r*N, (r+1)*N) of the global batch
+    g = torch.Generator(device="cpu").manual_seed(1000 + rank)
+    x_host = (torch.rand((N, C, H, W), generator=g) * 2 - 1).pin_memory()
+    w_host = torch.rand((Oc, C, k, k), generator=torch.Generator().manual_seed(7)) * 2 - 1
+    x = x_host.to(dev)
+    layer = XnorConv2d(w_host.to(dev), pad=pad, variant=args.variant)
+    filt = layer.filters
+    oh, ow = ops.out_dims(H, W, k, k, pad)
+    y = torch.empty((N, Oc, oh, ow), dtype=torch.float32, device=dev)
+    bits = torch.empty((N, H, W, ops.words(C)), dtype=torch.int32, device=dev)
+    A = torch.empty((N, H, W), dtype=torch.float32, device=dev)
+    K = torch.empty((N, oh, ow), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    from paper_2007_14178_b200._lib import check, lib
+    L = lib()
+    sptr = stream.cuda_stream
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        check(L.xnc_pack_input(x.data_ptr(), N, C, H, W, bits.data_ptr(), A.data_ptr(), sptr), "pack")
+        if ev is not None:
+            ev[1].record(stream)
+        check(L.xnc_scale_map(A.data_ptr(), N, H, W, k, k, pad, K.data_ptr(), sptr), "scale")
+        if ev is not None:
+            ev[2].record(stream)
+        check(L.xnc_xnor_conv_variant(ops.VARIANTS[args.variant], bits.data_ptr(), filt.wbits.data_ptr(),
+                                      K.data_ptr(), filt.alpha.data_ptr(), N, C, H, W, Oc, k, k, pad,
+                                      y.data_ptr(), None, sptr), "conv")
+        if ev is not None:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        # keep the sampler alive over a short tail so very short runs still get samples
+        if t_start.elapsed_time(t_end) < 500:
+            for _ in range(max(1, int(500 / max(t_start.elapsed_time(t_end) / args.steps, 0.05)))):
+                step()
+            torch.cuda.synchronize(dev)
+    if ws > 1:
+        torch.distributed.barrier()
+    ms_total = t_start.elapsed_time(t_end)
+    ms_total = max_over_ranks(ms_total, ws, dev)
+    ms_step = ms_total / args.steps
+    per_kernel = {
+        "pack_input": statistics.mean(e[0].elapsed_time(e[1]) for e in evs),
+        "scale_map": statistics.mean(e[1].elapsed_time(e[2]) for e in evs),
+        "xnor_conv": statistics.mean(e[2].elapsed_time(e[3]) for e in evs),
+    }
+    bops_rank = binops(N, C, H, W, Oc, k)
+    value = bops_rank * ws / (ms_step * 1e-3) / 1e9
+    imgs = N * ws / (ms_step * 1e-3)
+
+    # ---- e2e: the public API call with host buffers (pinned x in, y out), copies timed
+    y_host = torch.empty((N, Oc, oh, ow), dtype=torch.float32).pin_memory()
+    e2e_steps = max(2, min(args.steps, 5))
+
+    def e2e_step():
+        xd = x_host.to(dev, non_blocking=True)
+        yd = layer.forward(xd, out=y)
+        y_host.copy_(yd, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        torch.distributed.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps, ws, dev)
+    e2e = {"value": bops_rank * ws / (e2e_ms * 1e-3) / 1e9, "unit": "Gbinop/s",
+           "h2d_bytes_per_step": x_host.numel() * 4, "d2h_bytes_per_step": y_host.numel() * 4,
+           "ms_per_step": e2e_ms, "api": "XnorConv2d.forward (paper_2007_14178_b200.layer)"}
+
+    # ---- k-sweep (BASELINE config 2): GPU throughput per kernel size, same protocol
+    ksweep = None
+    if not args.no_ksweep and cfg_name == "C3":
+        ksweep = {}
+        for kname in ("C2k3", "C2k5", "C2k7"):
+            Nk, Ck, Hk, Wk, Ok, kk = CONFIGS[kname]
+            xk = (torch.rand((Nk, Ck, Hk, Wk), generator=g) * 2 - 1).to(dev)
+            lk = XnorConv2d((torch.rand((Ok, Ck, kk, kk), generator=g) * 2 - 1).to(dev), variant=args.variant)
+            yk = lk.forward(xk)
+            for _ in range(3):
+                lk.forward(xk, out=yk)
+            torch.cuda.synchronize(dev)
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            a_ev.record(stream)
+            for _ in range(reps):
+                lk.forward(xk, out=yk)
+            b_ev.record(stream)
+            torch.cuda.synchronize(dev)
+            ms_k = a_ev.elapsed_time(b_ev) / reps
+            ksweep[kname] = {"k": kk, "ms_per_layer": ms_k,
+                             "gpu_Gbinop_s": binops(Nk, Ck, Hk, Wk, Ok, kk) / (ms_k * 1e-3) / 1e9}
+            del xk, yk, lk
+
+    result = None
+    if rank == 0:
+        peaks, peaks_src = read_peaks()
+        f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        props = torch.cuda.get_device_properties(dev)
+        sms = props.multi_processor_count
+        peak_tbinops = 2 * POPC_LANES_PER_CLK_SM * 32 * sms * f_max / 1e12
+        conv_ms = per_kernel["xnor_conv"]
+        achieved = bops_rank / (conv_ms * 1e-3) / 1e12
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", f"ncu_{cfg_name}_conv_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        pack_bytes = 4.0 * N * C * H * W + 4.0 * N * H * W * ops.words(C) + 4.0 * N * H * W
+        result = {
+            "metric": METRIC, "value": value, "unit": "Gbinop/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32 (1-bit signs, int32 popcount accumulators) + f32 K/alpha",
+            "data": "synthetic U(-1,1) float32 activations and weights, seeded",
+            "config": {"workload": CONFIG_TEXT[cfg_name], "name": cfg_name, "batch_per_gpu": N,
+                       "global_batch": N * ws, "C_in": C, "C_out": Oc, "H": H, "W": W, "k": k, "pad": pad,
+                       "parallelism": f"batch-sharded x{ws}, per-rank weight replicas, no collective",
+                       "variant": args.variant,
+                       "l2": "inputs 4*N*C*H*W bytes > 126 MB L2; no flush needed"},
+            "images_per_s": imgs,
+            "kernel_ms": per_kernel,
+            "gpu_launches": 3 * args.steps,
+            "roofline": {"bound": "popc", "kernel": "xnor_conv (K3+K4)", "achieved": achieved,
+                         "peak": peak_tbinops, "unit": "Tbinop/s", "frac": achieved / peak_tbinops,
+                         "traffic": traffic,
+                         "peak_basis": f"{POPC_LANES_PER_CLK_SM} POPC lanes/clk/SM (measured microbench) x 32 "
+                                       f"bit-MACs x 2 binops x {sms} SMs x {f_max / 1e6:.0f} MHz "
+                                       f"(sm_max_mhz, {peaks_src})"},
+            "pack_roofline": {"bound": "hbm", "achieved": pack_bytes / (per_kernel["pack_input"] * 1e-3) / 1e9,
+                              "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
+                              "frac": pack_bytes / (per_kernel["pack_input"] * 1e-3) / 1e9 /
+                                      float(peaks.get("hbm_gbs", 6650.0))},
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "ksweep": ksweep,
+            "gpu": props.name,
+        }
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return result
+
+
+def cpu_baseline_fields(cfg_name, budget_s, ksweep=None):
+    cfg = CONFIGS[cfg_name]
+    rr = RefRunner(cfg)
+    N, C, H, W, Oc, k = cfg
+    s_pair, pairs = rr.pair_rate(budget_s)
+    bops_pair = binops(1, C, H, W, 1, k)
+    out = {"value": bops_pair / s_pair / 1e9, "unit": "Gbinop/s", "cores": rr.threads, "kind": "reference",
+           "sample": f"{pairs} (image, filter) pairs of {cfg_name} through the reference's fused "
+                     f"xnor_reconstruct (oracle/_ref, -march={rr.march}), threads={rr.threads}",
+           "ms_per_pair": s_pair * 1e3}
+    if ksweep:
+        for kname, row in ksweep.items():
+            rk = RefRunner(CONFIGS[kname])
+            sp, pr = rk.pair_rate(max(2.0, budget_s / 4))
+            _, Ck, Hk, Wk, _, kk = CONFIGS[kname]
+            row["cpu_Gbinop_s"] = binops(1, Ck, Hk, Wk, 1, kk) / sp / 1e9
+            row["cpu_threads"] = rk.threads
+            row["cpu_note"] = ("reference fused path, threads>1: output nondeterministic (reference "
+                               "race, SURVEY.md section 0 item 6)" if CONFIGS[kname][5] != 3 else
+                               "reference fused path")
+            row["speedup_vs_cpu"] = row["gpu_Gbinop_s"] / row["cpu_Gbinop_s"]
+    return out
+
+
+def run_reference(args, cfg_name):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    rr = RefRunner(CONFIGS[cfg_name])
+    N, C, H, W, Oc, k = CONFIGS[cfg_name]
+    bops_pair = binops(1, C, H, W, 1, k)
+    per_step_budget = max(0.5, min(10.0, 60.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        rr.pair_rate(per_step_budget / 4)
+    rates = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s_pair, pairs = rr.pair_rate(per_step_budget)
+        rates.append(bops_pair / s_pair / 1e9)
+    el = time.perf_counter() - t0
+    value = statistics.mean(rates)
+    return {"metric": METRIC, "value": value, "unit": "Gbinop/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 tile words + f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": CONFIG_TEXT[cfg_name], "name": cfg_name, "C_in": C, "C_out": Oc,
+                       "H": H, "W": W, "k": k, "batch_per_gpu": N},
+            "cpu_baseline": {"value": value, "unit": "Gbinop/s", "cores": rr.threads, "kind": "reference",
+                             "sample": f"each step ~{per_step_budget:.1f}s of (image, filter) pairs of "
+                                       f"{cfg_name} through xnor_reconstruct (oracle/_ref, -march={rr.march})"},
+            "e2e": {"value": value, "unit": "Gbinop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C3")
+    ap.add_argument("--variant", choices=["popc", "b1mma"], default="popc")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-ksweep", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU reference work")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        res = run_reference(args, args.config)
+    else:
+        res = run_ours(args, args.config)
+        ws, rank, _ = dist_env()
+        if res is not None and rank == 0 and ws == 1 and not args.no_cpu:
+            try:
+                res["cpu_baseline"] = cpu_baseline_fields(args.config, args.cpu_budget, res.get("ksweep"))
+                res["speedup_vs_cpu_reference"] = res["value"] / res["cpu_baseline"]["value"]
+            except Exception as exc:  # report, never fake
+                res["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

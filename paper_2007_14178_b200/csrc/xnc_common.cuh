@@ -1,0 +1,47 @@
+// Shared helpers for the sm_100a XNOR-conv kernels (libxnorb200.so).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/xnorb200.h"
+
+namespace xnc {
+
+constexpr int kMaxK = 8;  // reference: kernel must fit an 8x8 (64-bit) tile, pack.py:45-53
+
+__host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ inline long cdivl(long a, long b) { return (a + b - 1) / b; }
+__host__ __device__ inline int round_up(int a, int b) { return cdiv(a, b) * b; }
+
+// Word j of the +1 padding pixel: every valid channel bit set, tail bits 0
+// (padding binarizes to sign(0) = +1, reference.py:87; tail channels must be
+// 0 in both operands so they never count as disagreements).
+__host__ __device__ inline uint32_t pad_word(int j, int C) {
+  int rem = C - 32 * j;
+  return rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+}
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? XNC_OK : XNC_ECUDA_BASE + (int)e;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace xnc
+
+// Kernel launchers implemented in the per-kernel translation units.
+namespace xnc {
+int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
+                      cudaStream_t s);
+int launch_pack_weights(const float* w, int O, int C, int kh, int kw, uint32_t* wbits,
+                        float* alpha, double* alpha64, cudaStream_t s);
+int launch_scale_map(const float* A, int N, int H, int W, int kh, int kw, int pad, float* K,
+                     cudaStream_t s);
+int launch_conv_popc(const uint32_t* bits, const uint32_t* wbits, const float* K,
+                     const float* alpha, int N, int C, int H, int W, int O, int kh, int kw,
+                     int pad, float* y, int32_t* acc, cudaStream_t s);
+int launch_conv_b1mma(const uint32_t* bits, const uint32_t* wbits, const float* K,
+                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw,
+                      int pad, float* y, int32_t* acc, cudaStream_t s);
+}  // namespace xnc

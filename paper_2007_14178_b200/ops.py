@@ -1,0 +1,141 @@
+"""Device-tensor operators over libxnorb200.so (torch is plumbing: memory and
+streams; all arithmetic runs in the sm_100a kernels).
+
+Every function takes CUDA tensors, allocates its outputs with torch on the
+same device, and enqueues on torch's current stream.  Shapes follow the
+layouts documented in include/xnorb200.h.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import check, lib
+
+ABI_VERSION = 1
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _need_cuda(t: torch.Tensor, name: str, dtype: torch.dtype) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the B200 path has no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def out_dims(h: int, w: int, kh: int, kw: int, pad: int) -> tuple[int, int]:
+    """(H', W') of a stride-1 conv with zero padding `pad` (pipeline.py:62-66)."""
+    return h + 2 * pad - kh + 1, w + 2 * pad - kw + 1
+
+
+def words(c: int) -> int:
+    return (c + 31) // 32
+
+
+def pack_input(x: torch.Tensor, want_A: bool = True):
+    """K1: x f32 [N,C,H,W] -> (bits i32 [N,H,W,Cw] (u32 payload), A f32 [N,H,W])."""
+    _need_cuda(x, "x", torch.float32)
+    N, C, H, W = x.shape
+    bits = torch.empty((N, H, W, words(C)), dtype=torch.int32, device=x.device)
+    A = torch.empty((N, H, W), dtype=torch.float32, device=x.device) if want_A else None
+    check(lib().xnc_pack_input(x.data_ptr(), N, C, H, W, bits.data_ptr(), _ptr(A), _stream(x.device)),
+          "xnc_pack_input")
+    return bits, A
+
+
+@dataclass
+class PackedFilters:
+    """Binarized filter bank on the device (build_filter for every filter)."""
+
+    wbits: torch.Tensor    # i32 [Cw, kh, kw, O]
+    alpha: torch.Tensor    # f32 [O]
+    alpha64: torch.Tensor  # f64 [O] (BinaryFilter.scale)
+    O: int
+    C: int
+    kh: int
+    kw: int
+
+
+def pack_weights(w: torch.Tensor) -> PackedFilters:
+    """w f32 [O,C,kh,kw] -> PackedFilters (engine.py:102-120, binarize.py:65-75)."""
+    _need_cuda(w, "w", torch.float32)
+    O, C, kh, kw = w.shape
+    wbits = torch.empty((words(C), kh, kw, O), dtype=torch.int32, device=w.device)
+    alpha = torch.empty(O, dtype=torch.float32, device=w.device)
+    alpha64 = torch.empty(O, dtype=torch.float64, device=w.device)
+    check(lib().xnc_pack_weights(w.data_ptr(), O, C, kh, kw, wbits.data_ptr(), alpha.data_ptr(),
+                                 alpha64.data_ptr(), _stream(w.device)), "xnc_pack_weights")
+    return PackedFilters(wbits, alpha, alpha64, O, C, kh, kw)
+
+
+def scale_map(A: torch.Tensor, kh: int, kw: int, pad: int) -> torch.Tensor:
+    """K2: A f32 [N,H,W] -> K f32 [N,H',W'] (float32 reconstruct order)."""
+    _need_cuda(A, "A", torch.float32)
+    N, H, W = A.shape
+    oh, ow = out_dims(H, W, kh, kw, pad)
+    K = torch.empty((N, oh, ow), dtype=torch.float32, device=A.device)
+    check(lib().xnc_scale_map(A.data_ptr(), N, H, W, kh, kw, pad, K.data_ptr(), _stream(A.device)),
+          "xnc_scale_map")
+    return K
+
+
+VARIANTS = {"popc": 0, "b1mma": 1}
+
+
+def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, pad: int,
+              C: int | None = None, want_y: bool = True, want_acc: bool = False,
+              variant: str = "popc", y: torch.Tensor | None = None,
+              acc: torch.Tensor | None = None):
+    """K3+K4: (y f32 [N,O,H',W'] or None, acc i32 [N,O,H',W'] or None)."""
+    _need_cuda(bits, "bits", torch.int32)
+    N, H, W, Cw = bits.shape
+    C = filt.C if C is None else C
+    if words(C) != Cw or filt.C != C:
+        raise ValueError(f"bits hold {Cw} words per pixel; filters have {filt.C} channels")
+    oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    dev = bits.device
+    if want_y and y is None:
+        y = torch.empty((N, filt.O, oh, ow), dtype=torch.float32, device=dev)
+    if want_acc and acc is None:
+        acc = torch.empty((N, filt.O, oh, ow), dtype=torch.int32, device=dev)
+    if not want_y:
+        y = None
+    if want_y:
+        if K is None:
+            raise ValueError("K map required for the float output")
+        _need_cuda(K, "K", torch.float32)
+    check(lib().xnc_xnor_conv_variant(VARIANTS[variant], bits.data_ptr(), filt.wbits.data_ptr(),
+                                      _ptr(K), filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh,
+                                      filt.kw, pad, _ptr(y), _ptr(acc), _stream(dev)),
+          "xnc_xnor_conv")
+    return y, acc
+
+
+def layer_workspace_bytes(N: int, C: int, H: int, W: int, kh: int, kw: int, pad: int) -> int:
+    return int(lib().xnc_layer_workspace_bytes(N, C, H, W, kh, kw, pad))
+
+
+def layer_forward(x: torch.Tensor, filt: PackedFilters, pad: int, workspace: torch.Tensor,
+                  y: torch.Tensor | None = None, acc: torch.Tensor | None = None):
+    """K1 -> K2 -> K3+K4 in one C-ABI call (xnc_layer_forward)."""
+    _need_cuda(x, "x", torch.float32)
+    N, C, H, W = x.shape
+    if C != filt.C:
+        raise ValueError(f"{C} input channels vs {filt.C} filter channels")
+    oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    if y is None:
+        y = torch.empty((N, filt.O, oh, ow), dtype=torch.float32, device=x.device)
+    check(lib().xnc_layer_forward(x.data_ptr(), filt.wbits.data_ptr(), filt.alpha.data_ptr(), N, C,
+                                  H, W, filt.O, filt.kh, filt.kw, pad, workspace.data_ptr(), _ptr(y),
+                                  _ptr(acc), _stream(x.device)), "xnc_layer_forward")
+    return y

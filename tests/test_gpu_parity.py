@@ -1,0 +1,164 @@
+"""GPU parity: the sm_100a path (libxnorb200.so via the C-ABI) against the
+reference's own outputs (golden vectors) and the CPU oracle.
+
+Bar (BASELINE.json north star): packed bits and integer accumulators
+bit-exact; float outputs within 1e-5 relative (max-norm, the reference's own
+metric, verify.py:123-124) -- and in fact asserted BIT-EXACT here, because the
+kernels reproduce the reference's float32 operation order.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5  # north star float tolerance (max-norm relative)
+
+
+def _dev():
+    return torch.device("cuda:0")
+
+
+def _layer(x, w, pad, variant="popc"):
+    from paper_2007_14178_b200 import XnorConv2d
+    layer = XnorConv2d(torch.from_numpy(w).to(_dev()), pad=pad, variant=variant)
+    y, acc = layer.forward(torch.from_numpy(x).to(_dev()), want_acc=True)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), acc.cpu().numpy(), layer
+
+
+def _assert_float_parity(got, want):
+    denom = max(float(np.abs(want).max()), 1e-30)
+    assert float(np.abs(got.astype(np.float64) - want).max()) / denom <= REL_TOL
+    assert np.array_equal(got.view(np.uint32), want.astype(np.float32).view(np.uint32))
+
+
+@pytest.mark.parametrize("case", golden_io.layer_cases(), ids=lambda c: c["name"])
+def test_layer_matches_reference_golden(case):
+    y, acc, layer = _layer(case["x"], case["w"], case["pad"])
+    assert np.array_equal(acc, case["ints"])
+    _assert_float_parity(y, case["out"])
+    assert np.array_equal(layer.alpha64.cpu().numpy(), case["alpha"])
+
+
+def _unpack_bits(bits, C):
+    """[N,H,W,Cw] words -> [N,C,H,W] +-1 (bit c%32 of word c//32)."""
+    b = bits.view(np.uint32)
+    N, H, W, Cw = b.shape
+    c = np.arange(C)
+    vals = (b[..., c // 32] >> (c % 32).astype(np.uint32)) & 1
+    return np.where(vals.transpose(0, 3, 1, 2) == 1, 1, -1).astype(np.int8)
+
+
+@pytest.mark.parametrize("C", [1, 3, 31, 32, 33, 64, 96, 257])
+@pytest.mark.parametrize("HW", [(5, 7), (8, 8), (13, 11)])
+def test_pack_input_bits_and_absmean(C, HW):
+    from paper_2007_14178_b200 import ops
+    rng = np.random.default_rng([C, *HW])
+    H, W = HW
+    x = O.f32_exact(rng, (2, C, H, W))
+    x[0, 0, 0, :] = 0.0
+    x[0, -1, -1, :] = -0.0
+    bits, A = ops.pack_input(torch.from_numpy(x).to(_dev()))
+    bits = bits.cpu().numpy()
+    assert np.array_equal(_unpack_bits(bits, C), O.signs(x))
+    tail = C % 32
+    if tail:
+        assert ((bits[..., -1].view(np.uint32) >> tail) == 0).all()  # tail bits are 0
+    for n in range(2):
+        A_ref, _ = O.scale_map_f32(x[n], 3, 3, 1)
+        assert np.array_equal(A[n].cpu().numpy().view(np.uint32), A_ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("k,pad", [((1, 1), 0), ((3, 3), 1), ((3, 3), 0), ((5, 5), 2), ((7, 7), 3),
+                                   ((3, 5), 2), ((8, 8), 3), ((2, 2), 1)])
+def test_scale_map_bit_exact(k, pad):
+    from paper_2007_14178_b200 import ops
+    rng = np.random.default_rng([k[0], k[1], pad])
+    x = O.f32_exact(rng, (3, 6, 37, 41))
+    _, A = ops.pack_input(torch.from_numpy(x).to(_dev()))
+    K = ops.scale_map(A, k[0], k[1], pad).cpu().numpy()
+    for n in range(3):
+        _, K_ref = O.scale_map_f32(x[n], k[0], k[1], pad)
+        assert np.array_equal(K[n].view(np.uint32), K_ref.view(np.uint32))
+
+
+RANDOM_CASES = [
+    # N, C, H, W, O, kh, kw, pad
+    (2, 64, 16, 16, 16, 3, 3, 1),
+    (1, 33, 9, 23, 9, 3, 3, 1),
+    (2, 128, 12, 12, 40, 5, 5, 2),
+    (1, 96, 10, 15, 24, 7, 7, 3),
+    (3, 5, 7, 9, 5, 1, 1, 0),
+    (1, 257, 6, 6, 33, 3, 3, 1),
+    (1, 16, 11, 19, 8, 4, 6, 2),
+    (2, 32, 13, 13, 70, 3, 3, 1),
+    (1, 7, 20, 70, 3, 3, 3, 1),
+    (1, 40, 6, 6, 12, 6, 6, 0),      # fc6-style: k == H, pad 0 -> 1x1 output
+    (4, 64, 1, 1, 20, 1, 1, 0),      # fc7-style 1x1
+    (1, 9, 30, 300, 4, 3, 3, 1),     # wide rows -> column tiling
+]
+
+
+@pytest.mark.parametrize("shape", RANDOM_CASES, ids=lambda s: "x".join(map(str, s)))
+def test_layer_vs_oracle_random(shape):
+    N, C, H, W, Oc, kh, kw, pad = shape
+    rng = np.random.default_rng(list(shape))
+    x = O.f32_exact(rng, (N, C, H, W))
+    w = O.f32_exact(rng, (Oc, C, kh, kw))
+    y, acc, _ = _layer(x, w, pad)
+    want, ints = O.conv_layer(x, w, pad, want_ints=True)
+    assert np.array_equal(acc, ints)
+    _assert_float_parity(y, want)
+    O_area = C * kh * kw
+    assert (np.abs(acc) <= O_area).all() and ((acc - O_area) % 2 == 0).all()
+
+
+def test_edge_all_negative_padding_plus_one():
+    x = -np.ones((1, 4, 4, 4), np.float32)
+    w = np.ones((1, 4, 3, 3), np.float32)
+    _, acc, _ = _layer(x, w, 1)
+    assert acc[0, 0, 0, 0] == 4 * (5 - 4) and acc[0, 0, 1, 1] == -36
+
+
+def test_repeat_runs_bit_identical():
+    rng = np.random.default_rng(7)
+    x = O.f32_exact(rng, (2, 64, 20, 20))
+    w = O.f32_exact(rng, (32, 64, 5, 5))
+    y0, a0, _ = _layer(x, w, 2)
+    for _ in range(5):
+        y1, a1, _ = _layer(x, w, 2)
+        assert np.array_equal(a0, a1) and np.array_equal(y0.view(np.uint32), y1.view(np.uint32))
+
+
+@pytest.mark.parametrize("cfg", [("C2k3", 64, 128, 64, 64, 128, 3), ("C2k5", 64, 128, 64, 64, 128, 5),
+                                 ("C2k7", 64, 128, 64, 64, 128, 7), ("C3", 256, 256, 56, 56, 256, 3)],
+                         ids=lambda c: c[0])
+def test_full_size_configs_sampled(cfg):
+    """BASELINE configs at full size: invariants on every output, oracle on a
+    fixed sample of (image, filter) pairs."""
+    from paper_2007_14178_b200 import XnorConv2d
+    name, N, C, H, W, Oc, k = cfg
+    pad = (k - 1) // 2
+    g = torch.Generator(device="cpu").manual_seed(0)
+    x = (torch.rand((N, C, H, W), generator=g) * 2 - 1).to(_dev())
+    w = (torch.rand((Oc, C, k, k), generator=g) * 2 - 1).to(_dev())
+    layer = XnorConv2d(w, pad=pad)
+    y, acc = layer.forward(x, want_acc=True)
+    y2 = layer.forward(x)  # fused single-call path must agree with the split path
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
+    area = C * k * k
+    assert bool((acc.abs() <= area).all()) and bool(((acc - area) % 2 == 0).all())
+    n_idx = [0, N // 2, N - 1]
+    o_idx = [0, 1, Oc // 3, Oc - 1]
+    xs = x[n_idx].cpu().numpy()
+    ws = w[o_idx].cpu().numpy()
+    want, ints = O.conv_layer(xs, ws, pad, want_ints=True)
+    got_acc = acc[n_idx][:, o_idx].cpu().numpy()
+    got_y = y[n_idx][:, o_idx].cpu().numpy()
+    assert np.array_equal(got_acc, ints)
+    _assert_float_parity(got_y, want)
