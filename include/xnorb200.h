@@ -61,6 +61,10 @@ int xnc_pack_input(const float* x, int N, int C, int H, int W,
 int xnc_pack_weights(const float* w, int O, int C, int kh, int kw,
                      uint32_t* wbits, float* alpha, double* alpha64, void* stream);
 
+/* Same, from float64 weights (the reference's Tensor3 values, unrounded). */
+int xnc_pack_weights_f64(const double* w, int O, int C, int kh, int kw,
+                         uint32_t* wbits, float* alpha, double* alpha64, void* stream);
+
 /* ---- K2: K map = box filter of A with zero padding ----------------------------
  * Float32 op order of xnor_reconstruct's ring/map rows (_kernels_cy.pyx:231-239,
  * :299-311): row sums left->right, column sums top->bottom, * f32(1/(kh*kw)). */
@@ -92,6 +96,62 @@ size_t xnc_layer_workspace_bytes(int N, int C, int H, int W, int kh, int kw, int
 int xnc_layer_forward(const float* x, const uint32_t* wbits, const float* alpha,
                       int N, int C, int H, int W, int O, int kh, int kw, int pad,
                       void* workspace, float* y, int32_t* acc, void* stream);
+
+/* ======================================================================
+ * The reference kernel seam on the device (interop surface).
+ * One entry point per function of the module returned by the reference's
+ * _backend.get_kernels() (_backend.py:28-41), same argument meaning, same
+ * reference TILE-WORD layout (PackedTileGrid, pack.py:1-20) and float order;
+ * plus the float64 module-level operators of the reference's Python API.
+ * Device pointers; caller allocates outputs; enqueue only (except
+ * xnc_xnor_reconstruct, which takes stream-ordered scratch with
+ * cudaMallocAsync, as the reference mallocs per band, _kernels_cy.pyx:285).
+ * ====================================================================== */
+#define XNC_DTYPE_F32 0
+#define XNC_DTYPE_F64 1
+#define XNC_DTYPE_I8 2
+
+/* pack_plane (_kernels_cy.pyx:42-73): plane [h][w] of f32/f64/int8 -> tile
+ * words [tiles_y][tiles_x], bit r*tile_w+c = (plane[ty*sy+r][tx*sx+c] >= 0). */
+int xnc_pack_plane(const void* plane, int dtype, int h, int w, int tiles_y, int tiles_x,
+                   int tile_h, int tile_w, int stride_y, int stride_x, uint64_t* out_words,
+                   void* stream);
+/* unpack (pack.py:123-154): tile words -> +-1 plane over the whole covered
+ * region [cov_h][cov_w]; *mismatch |= 1 when overlapping tiles disagree. */
+int xnc_unpack_plane(const uint64_t* words, int tiles_y, int tiles_x, int tile_h, int tile_w,
+                     int stride_y, int stride_x, int8_t* plane_cov, int* mismatch, void* stream);
+/* sign_plane / _signs_of (binarize.py:56-60): float64 -> int8 +-1, sign(0) = +1. */
+int xnc_sign_plane(const double* x, long n, int8_t* out, void* stream);
+/* xnor_accumulate (_kernels_cy.pyx:76-104): words [C][tiles_y][tiles_x]. */
+int xnc_xnor_accumulate(const uint64_t* words, int channels, int tiles_y, int tiles_x,
+                        const uint64_t* weight_words, uint64_t mask, int tile_w, int stride_y,
+                        int stride_x, int k_area, int32_t* out, int out_h, int out_w,
+                        void* stream);
+/* build_filter (engine.py:102-120) for O filters: w f64 [O][C][kh][kw] ->
+ * tile-layout words [O][C] and float64 alpha [O]. */
+int xnc_filter_words(const double* w, int O, int C, int kh, int kw, int tile_w, uint64_t* words,
+                     double* alpha, void* stream);
+/* box_mean (_kernels_cy.pyx:126-148), f32 or f64: a [h][w] -> tmp [h][w-kw+1],
+ * out [h-kh+1][w-kw+1]. */
+int xnc_box_mean(const void* a, int dtype, int h, int w, int kh, int kw, double scale, void* tmp,
+                 void* out, void* stream);
+/* scale_rows (_kernels_cy.pyx:151-186): padded [C][h][w] -> tmp [h][w-kw+1]. */
+int xnc_scale_rows(const void* padded, int dtype, int channels, int h, int w, int kw, void* tmp,
+                   void* stream);
+/* scale_join (_kernels_cy.pyx:189-204): tmp [out_h+kh-1][out_w], ints [out_h][out_w]. */
+int xnc_scale_join(const void* tmp, int dtype, const int32_t* ints, int kh, double scale,
+                   double weight_scale, int out_h, int out_w, void* out, void* stream);
+/* xnor_reconstruct (_kernels_cy.pyx:242-354): one (padded image, filter) pair,
+ * padded [C][ph][pw] f32/f64 -> out [ph-kh+1][pw-kw+1]; race-free. */
+int xnc_xnor_reconstruct(const uint64_t* weight_words, uint64_t mask, int tile_h, int tile_w,
+                         int stride_y, int stride_x, int k_area, const void* padded, int dtype,
+                         int channels, int ph, int pw, int kh, int kw, double scale,
+                         double weight_scale, void* out, void* stream);
+/* channel_abs_mean (tensor.py:103-105): x f64 [C][H][W] -> A f64 [H][W]. */
+int xnc_channel_abs_mean_f64(const double* x, int C, int H, int W, double* A, void* stream);
+/* apply_scaling (scaling.py:91-98): out = ints * K * alpha, float64. */
+int xnc_apply_scaling_f64(const int32_t* ints, const double* K, double alpha, long n, double* out,
+                          void* stream);
 
 #ifdef __cplusplus
 }

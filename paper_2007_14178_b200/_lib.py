@@ -27,16 +27,29 @@ def lib() -> ctypes.CDLL:
             "g.build()\"` -- the B200 path has no CPU fallback")
     L = ctypes.CDLL(LIB_PATH)
     P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    LG, D, U64 = ctypes.c_long, ctypes.c_double, ctypes.c_uint64
     sig = {
         "xnc_abi_version": ([], I),
         "xnc_strerror": ([I], ctypes.c_char_p),
         "xnc_pack_input": ([P, I, I, I, I, P, P, P], I),
         "xnc_pack_weights": ([P, I, I, I, I, P, P, P, P], I),
+        "xnc_pack_weights_f64": ([P, I, I, I, I, P, P, P, P], I),
         "xnc_scale_map": ([P, I, I, I, I, I, I, P, P], I),
         "xnc_xnor_conv": ([P, P, P, P, I, I, I, I, I, I, I, I, P, P, P], I),
         "xnc_xnor_conv_variant": ([I, P, P, P, P, I, I, I, I, I, I, I, I, P, P, P], I),
         "xnc_layer_workspace_bytes": ([I, I, I, I, I, I, I], S),
         "xnc_layer_forward": ([P, P, P, I, I, I, I, I, I, I, I, P, P, P, P], I),
+        "xnc_pack_plane": ([P, I, I, I, I, I, I, I, I, I, P, P], I),
+        "xnc_unpack_plane": ([P, I, I, I, I, I, I, P, P, P], I),
+        "xnc_sign_plane": ([P, LG, P, P], I),
+        "xnc_xnor_accumulate": ([P, I, I, I, P, U64, I, I, I, I, P, I, I, P], I),
+        "xnc_filter_words": ([P, I, I, I, I, I, P, P, P], I),
+        "xnc_box_mean": ([P, I, I, I, I, I, D, P, P, P], I),
+        "xnc_scale_rows": ([P, I, I, I, I, I, P, P], I),
+        "xnc_scale_join": ([P, I, P, I, D, D, I, I, P, P], I),
+        "xnc_xnor_reconstruct": ([P, U64, I, I, I, I, I, P, I, I, I, I, I, I, D, D, P, P], I),
+        "xnc_channel_abs_mean_f64": ([P, I, I, I, P, P], I),
+        "xnc_apply_scaling_f64": ([P, P, D, LG, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -49,8 +62,13 @@ def lib() -> ctypes.CDLL:
 def exported_symbols() -> list[str]:
     """Names the header declares (kept in sync by tests/test_capi.py)."""
     return ["xnc_abi_version", "xnc_strerror", "xnc_pack_input", "xnc_pack_weights",
-            "xnc_scale_map", "xnc_xnor_conv", "xnc_xnor_conv_variant",
-            "xnc_layer_workspace_bytes", "xnc_layer_forward"]
+            "xnc_pack_weights_f64", "xnc_scale_map", "xnc_xnor_conv", "xnc_xnor_conv_variant",
+            "xnc_layer_workspace_bytes", "xnc_layer_forward", "xnc_pack_plane", "xnc_unpack_plane",
+            "xnc_sign_plane", "xnc_xnor_accumulate", "xnc_filter_words", "xnc_box_mean",
+            "xnc_scale_rows", "xnc_scale_join", "xnc_xnor_reconstruct", "xnc_channel_abs_mean_f64",
+            "xnc_apply_scaling_f64"]
+
+DTYPE_F32, DTYPE_F64, DTYPE_I8 = 0, 1, 2
 
 
 def check(rc: int, what: str) -> None:

@@ -48,6 +48,14 @@ int xnc_pack_weights(const float* w, int O, int C, int kh, int kw, uint32_t* wbi
   return launch_pack_weights(w, O, C, kh, kw, wbits, alpha, alpha64, as_stream(stream));
 }
 
+int xnc_pack_weights_f64(const double* w, int O, int C, int kh, int kw, uint32_t* wbits,
+                         float* alpha, double* alpha64, void* stream) {
+  if (!w || !wbits || !alpha || O < 1 || C < 1 || kh < 1 || kw < 1 || kh > kMaxK ||
+      kw > kMaxK)
+    return XNC_EINVAL;
+  return launch_pack_weights_f64(w, O, C, kh, kw, wbits, alpha, alpha64, as_stream(stream));
+}
+
 int xnc_scale_map(const float* A, int N, int H, int W, int kh, int kw, int pad, float* K,
                   void* stream) {
   if (!A || !K || !conv_shape_ok(N, 1, H, W, kh, kw, pad)) return XNC_EINVAL;

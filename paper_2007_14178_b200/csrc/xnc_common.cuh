@@ -36,6 +36,8 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
                       cudaStream_t s);
 int launch_pack_weights(const float* w, int O, int C, int kh, int kw, uint32_t* wbits,
                         float* alpha, double* alpha64, cudaStream_t s);
+int launch_pack_weights_f64(const double* w, int O, int C, int kh, int kw, uint32_t* wbits,
+                            float* alpha, double* alpha64, cudaStream_t s);
 int launch_scale_map(const float* A, int N, int H, int W, int kh, int kw, int pad, float* K,
                      cudaStream_t s);
 int launch_conv_popc(const uint32_t* bits, const uint32_t* wbits, const float* K,

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) k_conv_popc(
   float kv[P];
   const float* kp = Kmap + ((long)n * oh + yy) * ow + xb;
 #pragma unroll
-  for (int p = 0; p < P; ++p) kv[p] = (xb + p < ow) ? __ldg(kp + p) : 0.0f;
+  for (int p = 0; p < P; ++p) kv[p] = (y != nullptr && xb + p < ow) ? __ldg(kp + p) : 0.0f;
   const bool vec = vec_ok != 0;  // ow % 4 == 0 and 16-byte aligned outputs
 #pragma unroll
   for (int f = 0; f < F; ++f) {

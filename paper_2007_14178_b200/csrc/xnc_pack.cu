@@ -111,15 +111,18 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
 }
 
 // One thread per filter.  wbits layout [Cw][kh][kw][O] (filters contiguous) so
-// the conv kernel stages a filter block with coalesced row copies.
-__global__ void k_pack_weights(const float* __restrict__ w, int O, int C, int kh, int kw,
+// the conv kernel stages a filter block with coalesced row copies.  Templated
+// on the weight dtype: the drop-in API passes the reference's float64 Tensor3
+// values unrounded (sign and alpha are taken from them, binarize.py:65-75).
+template <typename T>
+__global__ void k_pack_weights(const T* __restrict__ w, int O, int C, int kh, int kw,
                                uint32_t* __restrict__ wbits, float* __restrict__ alpha,
                                double* __restrict__ alpha64) {
   int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= O) return;
   const int kk = kh * kw;
   const long n = (long)C * kk;
-  const float* wp = w + (long)o * n;
+  const T* wp = w + (long)o * n;
   double total = 0.0;
   for (long i = 0; i < n; ++i) total = __dadd_rn(total, fabs((double)wp[i]));
   const double a = __ddiv_rn(total, (double)n);
@@ -131,14 +134,20 @@ __global__ void k_pack_weights(const float* __restrict__ w, int O, int C, int kh
       uint32_t word = 0u;
       const int cend = min(32, C - 32 * j);
       for (int cc = 0; cc < cend; ++cc)
-        word |= (wp[(long)(32 * j + cc) * kk + t] >= 0.0f ? 1u : 0u) << cc;
+        word |= (wp[(long)(32 * j + cc) * kk + t] >= T(0) ? 1u : 0u) << cc;
       wbits[((long)j * kk + t) * O + o] = word;
     }
 }
 
 int launch_pack_weights(const float* w, int O, int C, int kh, int kw, uint32_t* wbits,
                         float* alpha, double* alpha64, cudaStream_t s) {
-  k_pack_weights<<<cdiv(O, 64), 64, 0, s>>>(w, O, C, kh, kw, wbits, alpha, alpha64);
+  k_pack_weights<float><<<cdiv(O, 64), 64, 0, s>>>(w, O, C, kh, kw, wbits, alpha, alpha64);
+  return launch_status();
+}
+
+int launch_pack_weights_f64(const double* w, int O, int C, int kh, int kw, uint32_t* wbits,
+                            float* alpha, double* alpha64, cudaStream_t s) {
+  k_pack_weights<double><<<cdiv(O, 64), 64, 0, s>>>(w, O, C, kh, kw, wbits, alpha, alpha64);
   return launch_status();
 }
 

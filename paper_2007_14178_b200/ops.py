@@ -53,6 +53,13 @@ def pack_input(x: torch.Tensor, want_A: bool = True):
     return bits, A
 
 
+def pack_input_into(x: torch.Tensor, bits: torch.Tensor, A: torch.Tensor | None) -> None:
+    """K1 into preallocated buffers."""
+    N, C, H, W = x.shape
+    check(lib().xnc_pack_input(x.data_ptr(), N, C, H, W, bits.data_ptr(), _ptr(A), _stream(x.device)),
+          "xnc_pack_input")
+
+
 @dataclass
 class PackedFilters:
     """Binarized filter bank on the device (build_filter for every filter)."""
@@ -76,6 +83,24 @@ def pack_weights(w: torch.Tensor) -> PackedFilters:
     check(lib().xnc_pack_weights(w.data_ptr(), O, C, kh, kw, wbits.data_ptr(), alpha.data_ptr(),
                                  alpha64.data_ptr(), _stream(w.device)), "xnc_pack_weights")
     return PackedFilters(wbits, alpha, alpha64, O, C, kh, kw)
+
+
+def pack_weights_f64(w: torch.Tensor) -> PackedFilters:
+    """Same from float64 weights (the reference's Tensor3 values, unrounded)."""
+    _need_cuda(w, "w", torch.float64)
+    O, C, kh, kw = w.shape
+    wbits = torch.empty((words(C), kh, kw, O), dtype=torch.int32, device=w.device)
+    alpha = torch.empty(O, dtype=torch.float32, device=w.device)
+    alpha64 = torch.empty(O, dtype=torch.float64, device=w.device)
+    check(lib().xnc_pack_weights_f64(w.data_ptr(), O, C, kh, kw, wbits.data_ptr(), alpha.data_ptr(),
+                                     alpha64.data_ptr(), _stream(w.device)), "xnc_pack_weights_f64")
+    return PackedFilters(wbits, alpha, alpha64, O, C, kh, kw)
+
+
+def scale_map_into(A: torch.Tensor, kh: int, kw: int, pad: int, K: torch.Tensor) -> None:
+    N, H, W = A.shape
+    check(lib().xnc_scale_map(A.data_ptr(), N, H, W, kh, kw, pad, K.data_ptr(), _stream(A.device)),
+          "xnc_scale_map")
 
 
 def scale_map(A: torch.Tensor, kh: int, kw: int, pad: int) -> torch.Tensor:

@@ -117,6 +117,20 @@ def test_layer_vs_oracle_random(shape):
     assert (np.abs(acc) <= O_area).all() and ((acc - O_area) % 2 == 0).all()
 
 
+@pytest.mark.parametrize("shape", RANDOM_CASES[:9] + [(2, 256, 14, 14, 64, 3, 3, 1)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_b1mma_variant_vs_oracle(shape):
+    """The legacy b1 mma.sync AND-popc variant (north star comparison) is exact too."""
+    N, C, H, W, Oc, kh, kw, pad = shape
+    rng = np.random.default_rng(list(shape) + [1])
+    x = O.f32_exact(rng, (N, C, H, W))
+    w = O.f32_exact(rng, (Oc, C, kh, kw))
+    y, acc, _ = _layer(x, w, pad, variant="b1mma")
+    want, ints = O.conv_layer(x, w, pad, want_ints=True)
+    assert np.array_equal(acc, ints)
+    _assert_float_parity(y, want)
+
+
 def test_edge_all_negative_padding_plus_one():
     x = -np.ones((1, 4, 4, 4), np.float32)
     w = np.ones((1, 4, 3, 3), np.float32)
