@@ -65,9 +65,16 @@ class XnorConv2d:
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None,
                 want_acc: bool = False):
-        """x f32 [N, C, H, W] (CUDA) -> y f32 [N, O, H', W'] (and acc i32 if asked)."""
+        """x f32 [N, C, H, W] -> y f32 [N, O, H', W'] (and acc i32 if asked).
+
+        A CUDA x runs on the device and returns a device y.  A host (CPU) x runs
+        the pipelined host path (`forward_host`) and returns a host y."""
         if x.dim() != 4 or x.shape[1] != self.C:
             raise ValueError(f"input {tuple(x.shape)} does not match {self.C} filter channels")
+        if not x.is_cuda:
+            if want_acc:
+                raise ValueError("want_acc is only supported for device inputs")
+            return self.forward_host(x, out=out)
         x = x.contiguous()
         self.out_shape(x.shape)
         if self.variant == "popc" and not want_acc:
@@ -79,6 +86,71 @@ class XnorConv2d:
         return (y, acc) if want_acc else y
 
     __call__ = forward
+
+    # ------------------------------------------------------------------ host path
+    def forward_host(self, x_host: torch.Tensor, out: torch.Tensor | None = None,
+                     chunk: int | None = None, device: torch.device | None = None) -> torch.Tensor:
+        """Host x in, host y out, with the PCIe copies overlapped with compute.
+
+        The batch is cut into chunks; chunk i+1 is copied host->device on one
+        stream while chunk i runs K1 -> K2 -> K3+K4 on a second and chunk i-1
+        is copied device->host on a third (two device buffers per direction,
+        events order buffer reuse).  Pinned host memory is used for both ends
+        (x is staged into a pinned buffer if it is not pinned already)."""
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        N = x_host.shape[0]
+        _, O, oh, ow = self.out_shape(x_host.shape)
+        if out is None:
+            out = torch.empty((N, O, oh, ow), dtype=torch.float32, pin_memory=True)
+        if not x_host.is_pinned():
+            x_host = x_host.contiguous().pin_memory()
+        if chunk is None:
+            chunk = max(1, N // 16)
+        st = self._host_state(dev, x_host.shape, chunk)
+        s_in, s_cmp, s_out = st["streams"]
+        cur = torch.cuda.current_stream(dev)
+        s_in.wait_stream(cur)
+        n_chunks = (N + chunk - 1) // chunk
+        for i in range(n_chunks):
+            a, b = i * chunk, min(N, (i + 1) * chunk)
+            slot = i % 2
+            xb = st["x"][slot][: b - a]
+            yb = st["y"][slot][: b - a]
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(st["x_free"][slot])
+                xb.copy_(x_host[a:b], non_blocking=True)
+                st["x_ready"][slot].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(st["x_ready"][slot])
+                if i >= 2:
+                    s_cmp.wait_event(st["y_free"][slot])
+                ws = st["ws"] if b - a == chunk else self.workspace(xb)
+                ops.layer_forward(xb, self.filters, self.pad, ws, y=yb)
+                st["x_free"][slot].record(s_cmp)
+                st["y_ready"][slot].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(st["y_ready"][slot])
+                out[a:b].copy_(yb, non_blocking=True)
+                st["y_free"][slot].record(s_out)
+        cur.wait_stream(s_out)
+        return out
+
+    def _host_state(self, dev, x_shape, chunk):
+        key = ("host", dev, tuple(x_shape[1:]), chunk)
+        st = self._ws.get(key)
+        if st is None:
+            _, C, H, W = x_shape
+            _, O, oh, ow = self.out_shape((chunk, C, H, W))
+            xs = [torch.empty((chunk, C, H, W), dtype=torch.float32, device=dev) for _ in range(2)]
+            st = {"streams": tuple(torch.cuda.Stream(dev) for _ in range(3)),
+                  "x": xs,
+                  "y": [torch.empty((chunk, O, oh, ow), dtype=torch.float32, device=dev) for _ in range(2)],
+                  "ws": self.workspace(xs[0]),
+                  **{k: [torch.cuda.Event() for _ in range(2)]
+                     for k in ("x_ready", "x_free", "y_ready", "y_free")}}
+            self._ws[key] = st
+        return st
 
 
 def xnor_conv2d_layer(x: torch.Tensor, weight: torch.Tensor, pad: int | None = None,

@@ -176,3 +176,21 @@ def test_full_size_configs_sampled(cfg):
     got_y = y[n_idx][:, o_idx].cpu().numpy()
     assert np.array_equal(got_acc, ints)
     _assert_float_parity(got_y, want)
+
+
+@pytest.mark.parametrize("N,chunk", [(7, 2), (16, None), (5, 5)])
+def test_host_pipelined_forward_matches_device(N, chunk):
+    """XnorConv2d.forward with HOST tensors (pipelined H2D / compute / D2H on three
+    streams) returns exactly the device path's output."""
+    from paper_2007_14178_b200 import XnorConv2d
+    g = torch.Generator().manual_seed(N)
+    x = torch.rand((N, 40, 12, 12), generator=g) * 2 - 1
+    w = torch.rand((24, 40, 3, 3), generator=g) * 2 - 1
+    layer = XnorConv2d(w.to(_dev()), pad=1)
+    y_dev = layer.forward(x.to(_dev())).cpu()
+    y_host = layer.forward_host(x, chunk=chunk)
+    torch.cuda.synchronize()
+    assert not y_host.is_cuda and torch.equal(y_host, y_dev)
+    y2 = layer.forward(x.pin_memory())
+    torch.cuda.synchronize()
+    assert torch.equal(y2, y_dev)
