@@ -48,7 +48,8 @@ CONFIG_TEXT = {
     "C3": "ResNet-stage binary conv 3x3, C=256, 56x56, batch 256 (BASELINE config 3)",
 }
 METRIC = "XNOR-conv Gbinop/s and images/sec at 1/2/4/8 B200 vs host-CPU reference"
-POPC_LANES_PER_CLK_SM = 15.95  # measured, profiles/int_peaks_r1.json
+POPC_LANES_PER_CLK_SM = 15.95  # measured, profiles/int_peaks_r1.jsonl
+UMMA_I8_MAC_PER_CLK_SM = 7874.4  # measured tcgen05 kind::i8 M128 N256 K32, profiles/umma_probe_r1.jsonl
 
 
 def binops(N, C, H, W, O, k):
@@ -231,6 +232,18 @@ def run_ours(args, cfg_name):
     L = lib()
     sptr = stream.cuda_stream
 
+    kernel = layer.kernel_for(x.shape)  # "auto" resolves per shape
+
+    def conv_call():
+        if kernel == "umma":
+            check(L.xnc_xnor_conv_umma(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), K.data_ptr(),
+                                       filt.alpha.data_ptr(), N, C, H, W, Oc, k, k, pad, y.data_ptr(), None,
+                                       sptr), "conv_umma")
+        else:
+            check(L.xnc_xnor_conv_variant(ops.VARIANTS[kernel], bits.data_ptr(), filt.wbits.data_ptr(),
+                                          K.data_ptr(), filt.alpha.data_ptr(), N, C, H, W, Oc, k, k, pad,
+                                          y.data_ptr(), None, sptr), "conv")
+
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
@@ -240,9 +253,7 @@ def run_ours(args, cfg_name):
         check(L.xnc_scale_map(A.data_ptr(), N, H, W, k, k, pad, K.data_ptr(), sptr), "scale")
         if ev is not None:
             ev[2].record(stream)
-        check(L.xnc_xnor_conv_variant(ops.VARIANTS[args.variant], bits.data_ptr(), filt.wbits.data_ptr(),
-                                      K.data_ptr(), filt.alpha.data_ptr(), N, C, H, W, Oc, k, k, pad,
-                                      y.data_ptr(), None, sptr), "conv")
+        conv_call()
         if ev is not None:
             ev[3].record(stream)
 
@@ -334,7 +345,16 @@ def run_ours(args, cfg_name):
         f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
         props = torch.cuda.get_device_properties(dev)
         sms = props.multi_processor_count
-        peak_tbinops = 2 * POPC_LANES_PER_CLK_SM * 32 * sms * f_max / 1e12
+        if kernel == "umma":
+            peak_tbinops = 2 * UMMA_I8_MAC_PER_CLK_SM * sms * f_max / 1e12
+            bound, basis = "tensor", (f"{UMMA_I8_MAC_PER_CLK_SM} tcgen05 kind::i8 MAC/clk/SM (measured, "
+                                      f"profiles/umma_probe_r1.jsonl) x 2 binops x {sms} SMs x "
+                                      f"{f_max / 1e6:.0f} MHz (sm_max_mhz, {peaks_src})")
+        else:
+            peak_tbinops = 2 * POPC_LANES_PER_CLK_SM * 32 * sms * f_max / 1e12
+            bound, basis = "popc", (f"{POPC_LANES_PER_CLK_SM} POPC lanes/clk/SM (measured microbench) x 32 "
+                                    f"bit-MACs x 2 binops x {sms} SMs x {f_max / 1e6:.0f} MHz "
+                                    f"(sm_max_mhz, {peaks_src})")
         conv_ms = per_kernel["xnor_conv"]
         achieved = bops_rank / (conv_ms * 1e-3) / 1e12
         traffic = None
@@ -353,17 +373,15 @@ def run_ours(args, cfg_name):
             "config": {"workload": CONFIG_TEXT[cfg_name], "name": cfg_name, "batch_per_gpu": N,
                        "global_batch": N * ws, "C_in": C, "C_out": Oc, "H": H, "W": W, "k": k, "pad": pad,
                        "parallelism": f"batch-sharded x{ws}, per-rank weight replicas, no collective",
-                       "variant": args.variant,
+                       "variant": args.variant, "conv_kernel": kernel,
                        "l2": "inputs 4*N*C*H*W bytes > 126 MB L2; no flush needed"},
             "images_per_s": imgs,
             "kernel_ms": per_kernel,
             "gpu_launches": 3 * args.steps,
-            "roofline": {"bound": "popc", "kernel": "xnor_conv (K3+K4)", "achieved": achieved,
+            "roofline": {"bound": bound, "kernel": f"xnor_conv (K3+K4, {kernel})", "achieved": achieved,
                          "peak": peak_tbinops, "unit": "Tbinop/s", "frac": achieved / peak_tbinops,
                          "traffic": traffic,
-                         "peak_basis": f"{POPC_LANES_PER_CLK_SM} POPC lanes/clk/SM (measured microbench) x 32 "
-                                       f"bit-MACs x 2 binops x {sms} SMs x {f_max / 1e6:.0f} MHz "
-                                       f"(sm_max_mhz, {peaks_src})"},
+                         "peak_basis": basis},
             "pack_roofline": {"bound": "hbm", "achieved": pack_bytes / (per_kernel["pack_input"] * 1e-3) / 1e9,
                               "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
                               "frac": pack_bytes / (per_kernel["pack_input"] * 1e-3) / 1e9 /
@@ -439,7 +457,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C3")
-    ap.add_argument("--variant", choices=["popc", "b1mma"], default="popc")
+    ap.add_argument("--variant", choices=["popc", "b1mma", "umma", "auto"], default="popc")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-ksweep", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU reference work")

@@ -36,6 +36,10 @@
 extern "C" {
 #endif
 
+#define XNC_DTYPE_F32 0
+#define XNC_DTYPE_F64 1
+#define XNC_DTYPE_I8 2
+
 #define XNC_OK 0
 #define XNC_EINVAL 1      /* bad shape / argument */
 #define XNC_ENOTSUP 2     /* shape outside what the kernels support */
@@ -88,6 +92,23 @@ int xnc_xnor_conv_variant(int variant, const uint32_t* bits, const uint32_t* wbi
                           int W, int O, int kh, int kw, int pad, float* y,
                           int32_t* acc, void* stream);
 
+/* ---- K3 on the tcgen05 tensor cores (kind::i8, TMEM accumulators) ------------
+ * The XNOR sum as an exact u8 x s8 GEMM: acc = S_w[o] - 2 * sum_taps d * s_w, with
+ * d = 1 for a negative input sign and s_w = +-1 the filter sign.
+ * Weights in the tensor-core layout: wq (xnc_umma_weight_bytes bytes, s8 signs
+ * in pre-swizzled 128-byte rows) and sw i32 [O] (sum of each filter's signs),
+ * produced by xnc_pack_weights_umma from f32 (dtype 0) or f64 (dtype 1) weights.
+ * Inputs are the same packed bits / K / alpha as xnc_xnor_conv.
+ * xnc_umma_supported() == 0 means the shape does not fit the kernel's shared
+ * memory plan (then use xnc_xnor_conv). */
+size_t xnc_umma_weight_bytes(int O, int C, int kh, int kw);
+int xnc_umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
+int xnc_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw,
+                          uint8_t* wq, int32_t* sw, void* stream);
+int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
+                       const float* K, const float* alpha, int N, int C, int H, int W,
+                       int O, int kh, int kw, int pad, float* y, int32_t* acc, void* stream);
+
 /* ---- whole layer: K1 -> K2 -> K3+K4 on one stream ------------------------------
  * The batched equivalent of ConvWorkspace.run() (pipeline.py:124-151) over
  * every (image, filter) pair.  workspace: device scratch of at least
@@ -107,10 +128,6 @@ int xnc_layer_forward(const float* x, const uint32_t* wbits, const float* alpha,
  * xnc_xnor_reconstruct, which takes stream-ordered scratch with
  * cudaMallocAsync, as the reference mallocs per band, _kernels_cy.pyx:285).
  * ====================================================================== */
-#define XNC_DTYPE_F32 0
-#define XNC_DTYPE_F64 1
-#define XNC_DTYPE_I8 2
-
 /* pack_plane (_kernels_cy.pyx:42-73): plane [h][w] of f32/f64/int8 -> tile
  * words [tiles_y][tiles_x], bit r*tile_w+c = (plane[ty*sy+r][tx*sx+c] >= 0). */
 int xnc_pack_plane(const void* plane, int dtype, int h, int w, int tiles_y, int tiles_x,

@@ -87,6 +87,34 @@ int xnc_xnor_conv(const uint32_t* bits, const uint32_t* wbits, const float* K,
                                y, acc, stream);
 }
 
+size_t xnc_umma_weight_bytes(int O, int C, int kh, int kw) {
+  if (O < 1 || C < 1 || kh < 1 || kw < 1 || kh > kMaxK || kw > kMaxK) return 0;
+  return umma_weight_bytes(O, C, kh, kw);
+}
+
+int xnc_umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
+  if (O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return 0;
+  return umma_supported(N, C, H, W, O, kh, kw, pad) ? 1 : 0;
+}
+
+int xnc_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw, uint8_t* wq,
+                          int32_t* sw, void* stream) {
+  if (!w || !wq || !sw || O < 1 || C < 1 || kh < 1 || kw < 1 || kh > kMaxK || kw > kMaxK ||
+      (dtype != XNC_DTYPE_F32 && dtype != XNC_DTYPE_F64))
+    return XNC_EINVAL;
+  return launch_pack_weights_umma(w, dtype, O, C, kh, kw, wq, sw, as_stream(stream));
+}
+
+int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
+                       const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
+                       float* y, int32_t* acc, void* stream) {
+  if (!bits || !wq || !sw || O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return XNC_EINVAL;
+  if (!y && !acc) return XNC_EINVAL;
+  if (y && (!K || !alpha)) return XNC_EINVAL;
+  return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, acc,
+                          as_stream(stream));
+}
+
 size_t xnc_layer_workspace_bytes(int N, int C, int H, int W, int kh, int kw, int pad) {
   if (!conv_shape_ok(N, C, H, W, kh, kw, pad)) return 0;
   const size_t oh = H + 2 * pad - kh + 1, ow = W + 2 * pad - kw + 1;

@@ -38,6 +38,10 @@ class XnorConv2d:
         if not w.is_cuda:
             w = w.cuda()
         self.filters = ops.pack_weights(w)
+        if variant in ("umma", "auto"):
+            ops.attach_umma_weights(self.filters, w)
+        elif variant not in ("popc", "b1mma"):
+            raise ValueError(f"unknown variant {variant!r}")
         self.O, self.C, self.kh, self.kw = O, C, kh, kw
         self.variant = variant
         self._ws: dict[tuple, torch.Tensor] = {}
@@ -77,13 +81,22 @@ class XnorConv2d:
             return self.forward_host(x, out=out)
         x = x.contiguous()
         self.out_shape(x.shape)
-        if self.variant == "popc" and not want_acc:
+        variant = self.kernel_for(x.shape)
+        if variant == "popc" and not want_acc:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
         bits, A = ops.pack_input(x)
         K = ops.scale_map(A, self.kh, self.kw, self.pad)
         y, acc = ops.xnor_conv(bits, self.filters, K, self.pad, want_acc=want_acc,
-                               variant=self.variant, y=out)
+                               variant=variant, y=out)
         return (y, acc) if want_acc else y
+
+    def kernel_for(self, x_shape) -> str:
+        """The conv kernel a forward of this input shape runs: 'auto' picks the
+        tcgen05 kernel whenever its shared-memory plan fits the shape, else popc."""
+        if self.variant != "auto":
+            return self.variant
+        N, C, H, W = x_shape
+        return "umma" if ops.umma_supported(N, C, H, W, self.O, self.kh, self.kw, self.pad) else "popc"
 
     __call__ = forward
 

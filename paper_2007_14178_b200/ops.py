@@ -71,6 +71,27 @@ class PackedFilters:
     C: int
     kh: int
     kw: int
+    wq: torch.Tensor | None = None   # u8 tensor-core layout (xnc_pack_weights_umma)
+    sw: torch.Tensor | None = None   # i32 [O] sum of each filter's signs
+
+
+def attach_umma_weights(filt: PackedFilters, w: torch.Tensor) -> PackedFilters:
+    """Add the tcgen05 (kind::i8) weight layout to a PackedFilters (f32 or f64 w)."""
+    if w.dtype not in (torch.float32, torch.float64):
+        raise TypeError("weights must be float32 or float64")
+    _need_cuda(w, "w", w.dtype)
+    O, C, kh, kw = w.shape
+    nbytes = int(lib().xnc_umma_weight_bytes(O, C, kh, kw))
+    filt.wq = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=w.device)
+    filt.sw = torch.empty(O, dtype=torch.int32, device=w.device)
+    check(lib().xnc_pack_weights_umma(w.data_ptr(), 0 if w.dtype == torch.float32 else 1, O, C, kh, kw,
+                                      filt.wq.data_ptr(), filt.sw.data_ptr(), _stream(w.device)),
+          "xnc_pack_weights_umma")
+    return filt
+
+
+def umma_supported(N: int, C: int, H: int, W: int, O: int, kh: int, kw: int, pad: int) -> bool:
+    return bool(lib().xnc_umma_supported(N, C, H, W, O, kh, kw, pad))
 
 
 def pack_weights(w: torch.Tensor) -> PackedFilters:
@@ -114,7 +135,7 @@ def scale_map(A: torch.Tensor, kh: int, kw: int, pad: int) -> torch.Tensor:
     return K
 
 
-VARIANTS = {"popc": 0, "b1mma": 1}
+VARIANTS = {"popc": 0, "b1mma": 1, "umma": 2}
 
 
 def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, pad: int,
@@ -139,10 +160,17 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
         if K is None:
             raise ValueError("K map required for the float output")
         _need_cuda(K, "K", torch.float32)
-    check(lib().xnc_xnor_conv_variant(VARIANTS[variant], bits.data_ptr(), filt.wbits.data_ptr(),
-                                      _ptr(K), filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh,
-                                      filt.kw, pad, _ptr(y), _ptr(acc), _stream(dev)),
-          "xnc_xnor_conv")
+    if variant == "umma":
+        if filt.wq is None:
+            raise ValueError("umma variant needs attach_umma_weights() first")
+        check(lib().xnc_xnor_conv_umma(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), _ptr(K),
+                                       filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
+                                       _ptr(y), _ptr(acc), _stream(dev)), "xnc_xnor_conv_umma")
+    else:
+        check(lib().xnc_xnor_conv_variant(VARIANTS[variant], bits.data_ptr(), filt.wbits.data_ptr(),
+                                          _ptr(K), filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh,
+                                          filt.kw, pad, _ptr(y), _ptr(acc), _stream(dev)),
+              "xnc_xnor_conv")
     return y, acc
 
 

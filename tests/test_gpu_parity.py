@@ -131,6 +131,27 @@ def test_b1mma_variant_vs_oracle(shape):
     _assert_float_parity(y, want)
 
 
+UMMA_CASES = RANDOM_CASES + [(2, 256, 14, 14, 64, 3, 3, 1), (1, 128, 20, 20, 300, 3, 3, 1),
+                             (2, 384, 13, 13, 40, 3, 3, 1), (1, 64, 27, 27, 16, 5, 5, 2),
+                             (1, 256, 9, 9, 256, 3, 3, 1)]
+
+
+@pytest.mark.parametrize("shape", UMMA_CASES, ids=lambda s: "x".join(map(str, s)))
+def test_umma_variant_vs_oracle(shape):
+    """The tcgen05 kind::i8 kernel (u8 d x s8 sign GEMM in TMEM) is exact."""
+    from paper_2007_14178_b200 import ops
+    N, C, H, W, Oc, kh, kw, pad = shape
+    if not ops.umma_supported(N, C, H, W, Oc, kh, kw, pad):
+        pytest.skip("shape outside the tcgen05 kernel's smem plan")
+    rng = np.random.default_rng(list(shape) + [2])
+    x = O.f32_exact(rng, (N, C, H, W))
+    w = O.f32_exact(rng, (Oc, C, kh, kw))
+    y, acc, _ = _layer(x, w, pad, variant="umma")
+    want, ints = O.conv_layer(x, w, pad, want_ints=True)
+    assert np.array_equal(acc, ints)
+    _assert_float_parity(y, want)
+
+
 def test_edge_all_negative_padding_plus_one():
     x = -np.ones((1, 4, 4, 4), np.float32)
     w = np.ones((1, 4, 3, 3), np.float32)
@@ -163,8 +184,10 @@ def test_full_size_configs_sampled(cfg):
     layer = XnorConv2d(w, pad=pad)
     y, acc = layer.forward(x, want_acc=True)
     y2 = layer.forward(x)  # fused single-call path must agree with the split path
+    lu = XnorConv2d(w, pad=pad, variant="umma")
+    yu, accu = lu.forward(x, want_acc=True)  # tcgen05 path: identical at full size
     torch.cuda.synchronize()
-    assert torch.equal(y, y2)
+    assert torch.equal(y, y2) and torch.equal(acc, accu) and torch.equal(y, yu)
     area = C * k * k
     assert bool((acc.abs() <= area).all()) and bool(((acc - area) % 2 == 0).all())
     n_idx = [0, N // 2, N - 1]
