@@ -353,10 +353,11 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   UmmaGeom g;
   size_t smem;
   if (!umma_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_conv_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_done = true;
+  static size_t attr_smem = 0;  // one-time (per size increase) shared-memory opt-in
+  if (smem > attr_smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_conv_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
+    attr_smem = smem;
   }
   const long blocks = (long)N * g.n_mt * g.n_nb;
   k_conv_umma<<<(unsigned)blocks, kUmmaThreads, smem, s>>>(bits, wq, sw, K, alpha, g, y, acc);
