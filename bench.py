@@ -224,15 +224,18 @@ def run_ours(args, cfg_name):
     filt = layer.filters
     oh, ow = ops.out_dims(H, W, k, k, pad)
     y = torch.empty((N, Oc, oh, ow), dtype=torch.float32, device=dev)
-    bits = torch.empty((N, H, W, ops.words(C)), dtype=torch.int32, device=dev)
+    kernel = layer.kernel_for(x.shape)  # "auto" resolves per shape
+    if kernel == "umma":  # the tcgen05 operand: d-bytes (K1 variant)
+        bits = torch.empty((N, H, W, ops.dbytes_channels(C)), dtype=torch.uint8, device=dev)
+    else:
+        bits = torch.empty((N, H, W, ops.words(C)), dtype=torch.int32, device=dev)
     A = torch.empty((N, H, W), dtype=torch.float32, device=dev)
     K = torch.empty((N, oh, ow), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     from paper_2007_14178_b200._lib import check, lib
     L = lib()
     sptr = stream.cuda_stream
-
-    kernel = layer.kernel_for(x.shape)  # "auto" resolves per shape
+    pack_fn = L.xnc_pack_input_umma if kernel == "umma" else L.xnc_pack_input
 
     def conv_call():
         if kernel == "umma":
@@ -247,7 +250,7 @@ def run_ours(args, cfg_name):
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        check(L.xnc_pack_input(x.data_ptr(), N, C, H, W, bits.data_ptr(), A.data_ptr(), sptr), "pack")
+        check(pack_fn(x.data_ptr(), N, C, H, W, bits.data_ptr(), A.data_ptr(), sptr), "pack")
         if ev is not None:
             ev[1].record(stream)
         check(L.xnc_scale_map(A.data_ptr(), N, H, W, k, k, pad, K.data_ptr(), sptr), "scale")
@@ -364,7 +367,8 @@ def run_ours(args, cfg_name):
                 traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
             except Exception:
                 traffic = None
-        pack_bytes = 4.0 * N * C * H * W + 4.0 * N * H * W * ops.words(C) + 4.0 * N * H * W
+        packed = N * H * W * (ops.dbytes_channels(C) if kernel == "umma" else 4 * ops.words(C))
+        pack_bytes = 4.0 * N * C * H * W + packed + 4.0 * N * H * W
         result = {
             "metric": METRIC, "value": value, "unit": "Gbinop/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

@@ -95,17 +95,20 @@ int xnc_xnor_conv_variant(int variant, const uint32_t* bits, const uint32_t* wbi
 /* ---- K3 on the tcgen05 tensor cores (kind::i8, TMEM accumulators) ------------
  * The XNOR sum as an exact u8 x s8 GEMM: acc = S_w[o] - 2 * sum_taps d * s_w, with
  * d = 1 for a negative input sign and s_w = +-1 the filter sign.
+ * Input operand: d-bytes u8 [N][H][W][Cpad], Cpad = ceil(C/128)*128, written by
+ * xnc_pack_input_umma (K1 variant: same single read of x, also writes A).
  * Weights in the tensor-core layout: wq (xnc_umma_weight_bytes bytes, s8 signs
  * in pre-swizzled 128-byte rows) and sw i32 [O] (sum of each filter's signs),
  * produced by xnc_pack_weights_umma from f32 (dtype 0) or f64 (dtype 1) weights.
- * Inputs are the same packed bits / K / alpha as xnc_xnor_conv.
  * xnc_umma_supported() == 0 means the shape does not fit the kernel's shared
  * memory plan (then use xnc_xnor_conv). */
 size_t xnc_umma_weight_bytes(int O, int C, int kh, int kw);
 int xnc_umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 int xnc_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw,
                           uint8_t* wq, int32_t* sw, void* stream);
-int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
+int xnc_pack_input_umma(const float* x, int N, int C, int H, int W, uint8_t* dbytes,
+                        float* A, void* stream);
+int xnc_xnor_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw,
                        const float* K, const float* alpha, int N, int C, int H, int W,
                        int O, int kh, int kw, int pad, float* y, int32_t* acc, void* stream);
 

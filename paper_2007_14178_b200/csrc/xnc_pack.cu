@@ -17,18 +17,31 @@
 
 namespace xnc {
 
+// 32 sign bits -> 32 d-bytes, d = 1 for a negative sign (the tcgen05 operand).
+__device__ __forceinline__ void store_d32(uint8_t* dst, uint32_t d) {
+  uint32_t w[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) w[b] = (((d >> (4 * b)) & 0xFu) * 0x00204081u) & 0x01010101u;
+  reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+// bits (u32 [N][HW][Cw]) and/or dbytes (u8 [N][HW][Cpad], d = 1 for x < 0, zero
+// for c >= C) -- the popc kernels read bits, the tcgen05 kernel reads d-bytes.
 template <int VEC>
 __global__ void __launch_bounds__(256) k_pack_input(const float* __restrict__ x, int C, int HW,
                                                     int Cw, float inv, long groups_per_img,
                                                     long total_groups,
                                                     uint32_t* __restrict__ bits,
-                                                    float* __restrict__ A) {
+                                                    float* __restrict__ A,
+                                                    uint8_t* __restrict__ dbytes, int Cpad) {
   long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= total_groups) return;
   const long n = gid / groups_per_img;
   const int p0 = (int)(gid - n * groups_per_img) * VEC;
   const float* xp = x + (long)n * C * HW + p0;
-  uint32_t* bp = bits + ((long)n * HW + p0) * Cw;
+  uint32_t* bp = bits ? bits + ((long)n * HW + p0) * Cw : nullptr;
+  uint8_t* dp = dbytes ? dbytes + ((long)n * HW + p0) * Cpad : nullptr;
 
   float s[VEC];
 #pragma unroll
@@ -75,8 +88,20 @@ __global__ void __launch_bounds__(256) k_pack_input(const float* __restrict__ x,
         }
       }
     }
+    if (bp) {
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) bp[(long)i * Cw + j] = word[i];
+      for (int i = 0; i < VEC; ++i) bp[(long)i * Cw + j] = word[i];
+    }
+    if (dp) {
+      const uint32_t valid = cend == 32 ? 0xFFFFFFFFu : ((1u << cend) - 1u);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) store_d32(dp + (long)i * Cpad + 32 * j, ~word[i] & valid);
+    }
+  }
+  if (dp) {
+    for (int c = 32 * Cw; c < Cpad; c += 16)
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) *reinterpret_cast<uint4*>(dp + (long)i * Cpad + c) = make_uint4(0, 0, 0, 0);
   }
   if (A != nullptr) {
     float* ap = A + (long)n * HW + p0;
@@ -92,7 +117,7 @@ __global__ void __launch_bounds__(256) k_pack_input(const float* __restrict__ x,
 }
 
 int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
-                      cudaStream_t s) {
+                      cudaStream_t s, uint8_t* dbytes) {
   const int HW = H * W;
   const int Cw = cdiv(C, 32);
   const float inv = (float)(1.0 / (double)C);  // <real_t>(1.0 / channels), _kernels_cy.pyx:258
@@ -101,11 +126,13 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   if (vec4) {
     long gpi = HW / 4, total = gpi * N;
     long blocks = cdivl(total, 256);
-    k_pack_input<4><<<(unsigned)blocks, 256, 0, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A);
+    k_pack_input<4><<<(unsigned)blocks, 256, 0, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, dbytes,
+                                                     round_up(C, 128));
   } else {
     long gpi = HW, total = gpi * N;
     long blocks = cdivl(total, 256);
-    k_pack_input<1><<<(unsigned)blocks, 256, 0, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A);
+    k_pack_input<1><<<(unsigned)blocks, 256, 0, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, dbytes,
+                                                     round_up(C, 128));
   }
   return launch_status();
 }

@@ -84,7 +84,7 @@ class XnorConv2d:
         variant = self.kernel_for(x.shape)
         if variant == "popc" and not want_acc:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
-        bits, A = ops.pack_input(x)
+        bits, A = ops.pack_input_umma(x) if variant == "umma" else ops.pack_input(x)
         K = ops.scale_map(A, self.kh, self.kw, self.pad)
         y, acc = ops.xnor_conv(bits, self.filters, K, self.pad, want_acc=want_acc,
                                variant=variant, y=out)

@@ -217,3 +217,20 @@ def test_host_pipelined_forward_matches_device(N, chunk):
     y2 = layer.forward(x.pin_memory())
     torch.cuda.synchronize()
     assert torch.equal(y2, y_dev)
+
+
+@pytest.mark.parametrize("C", [1, 31, 64, 128, 200, 256])
+def test_pack_input_umma_dbytes(C):
+    """K1's tcgen05 operand: d = 1 exactly where x < 0 (sign -1), 0 for the channel tail."""
+    from paper_2007_14178_b200 import ops
+    rng = np.random.default_rng([C, 9])
+    x = O.f32_exact(rng, (2, C, 7, 12))
+    x[0, 0, 0, :3] = [0.0, -0.0, -1e-30]
+    d, A = ops.pack_input_umma(torch.from_numpy(x).to(_dev()))
+    d = d.cpu().numpy()
+    assert d.shape[-1] == (C + 127) // 128 * 128
+    want = (O.signs(x) < 0).astype(np.uint8).transpose(0, 2, 3, 1)
+    assert np.array_equal(d[..., :C], want) and not d[..., C:].any()
+    for n in range(2):
+        A_ref, _ = O.scale_map_f32(x[n], 3, 3, 1)
+        assert np.array_equal(A[n].cpu().numpy().view(np.uint32), A_ref.view(np.uint32))
