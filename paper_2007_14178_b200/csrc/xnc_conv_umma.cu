@@ -25,15 +25,15 @@
 //   warp 0      B producer: cp.async.bulk of one (tap, K block) filter chunk,
 //               NB x 128 B, pre-swizzled in HBM by k_pack_weights_umma
 //   warp 1      MMA issuer (one thread): per tile and filter block,
-//               2 M=128 halves x 4 K=32 steps per chunk, accumulate in TMEM
+//               MH M=128 row blocks x 4 K=32 steps per chunk, accumulate in TMEM
 //   warp 2      A producer: one TMA tile load per 128-channel K block of the
 //               d-bytes written by K1 (xnc_pack_input_umma): R padded rows x IC
 //               columns x 128 B, zero fill outside the image
 //   warps 4-11  epilogue: TMEM -> registers -> S_w - 2*acc -> (f32 * K) * alpha
 //               -> y, two warps per TMEM lane quadrant
-// Work unit = (tile of 256 extended pixels of one image, filter block of NB).
-// TMEM holds two accumulators (2 halves x NB columns each): the epilogue of one
-// unit overlaps the MMAs of the next.  A K-block plane is released as soon as
+// Work unit = (tile of 128*MH extended pixels of one image, filter block of NB).
+// TMEM holds two accumulators (MH x NB columns each): the epilogue of one unit
+// overlaps the MMAs of the next.  A K-block plane is released as soon as
 // the tile's last filter block has consumed it, so the next tile's TMA load
 // overlaps the remaining MMAs.
 #include <cuda.h>
@@ -44,8 +44,7 @@
 namespace xnc {
 
 constexpr int kU2Threads = 384;
-constexpr int kU2MT = 256;       // extended output pixels per tile (2 x M=128)
-constexpr int kU2Stages = 5;     // B pipeline depth
+constexpr int kU2Stages = 6;     // B pipeline depth
 constexpr int kU2MaxKB = 4;      // K blocks (128 channels each) kept resident: C <= 512
 constexpr int kU2EpiWarp0 = 4;   // first epilogue warp
 constexpr int kU2EpiWarps = 8;
@@ -130,10 +129,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
 }
 
 struct UmmaGeom {
-  int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NB, R, plane_bytes, n_mt, n_nb, tiles, taps;
+  int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NB, R, plane_bytes, n_mt, n_nb, tiles, taps, MH;
   uint32_t box_bytes, tmem_cols;
 };
 
+// MH = M=128 row blocks per tile (tile = 128*MH extended pixels); the two TMEM
+// accumulators hold MH x NB columns each (MH * NB <= 256).
+template <int MH>
 __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
     const __grid_constant__ CUtensorMap a_map, const uint8_t* __restrict__ wq,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
     if (lane == 0) {
       uint32_t it = 0;
       for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, ++it) {
-        const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * kU2MT;
+        const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * (128 * MH);
         const int r0 = m0 / g.IC;
         for (int kb = 0; kb < g.KBn; ++kb) {
           if (it >= 1) mbar_wait(&a_empty[kb], (it - 1) & 1);
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
       const uint32_t a_base = smem_addr(a_s), b_base = smem_addr(b_s);
       uint32_t step = 0, item = 0, it = 0;
       for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, ++it) {
-        const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * kU2MT;
+        const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * (128 * MH);
         const int off0 = m0 - (m0 / g.IC) * g.IC;
         for (int nb = 0; nb < g.n_nb; ++nb, ++item) {
           const uint32_t buf = item & 1;
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
             mbar_wait(&t_empty[buf], ((item >> 1) - 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
           }
-          const uint32_t d0 = tmem + buf * (2 * g.NB);
+          const uint32_t d0 = tmem + buf * (MH * g.NB);
           for (int kb = 0; kb < g.KBn; ++kb) {
             if (nb == 0) {
               mbar_wait(&a_full[kb], it & 1);
@@ -230,8 +232,9 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
               for (int s = 0; s < 4; ++s) {
                 const uint64_t bd = umma_desc_sw128(b_st + s * 32);
                 const uint32_t acc = (kb | tap | s) != 0;
-                umma_i8(d0, umma_desc_sw128(a_tap + s * 32), bd, idesc, acc);
-                umma_i8(d0 + g.NB, umma_desc_sw128(a_tap + 128 * 128 + s * 32), bd, idesc, acc);
+#pragma unroll
+                for (int h = 0; h < MH; ++h)
+                  umma_i8(d0 + h * g.NB, umma_desc_sw128(a_tap + h * 128 * 128 + s * 32), bd, idesc, acc);
               }
               umma_commit(&b_empty[st]);
             }
@@ -249,13 +252,15 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
     const int col0 = (e_w >> 2) * half_cols;
     const size_t plane_out = (size_t)g.oh * g.ow;
     uint32_t item = 0;
+    const bool vec_ok = (g.NB % 16 == 0) && ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(alpha) & 15) == 0);
     for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
-      const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * kU2MT;
-      int rr[2], cc[2];
-      bool ok[2];
-      float kv[2];
+      const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * (128 * MH);
+      int rr[MH], cc[MH];
+      bool ok[MH];
+      float kv[MH];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < MH; ++h) {
         const int e = m0 + h * 128 + quad * 32 + lane;
         rr[h] = e / g.IC;
         cc[h] = e - rr[h] * g.IC;
@@ -266,21 +271,40 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
         const uint32_t buf = item & 1;
         mbar_wait(&t_full[buf], (item >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int c = col0; c < col0 + half_cols; c += 16) {
+          const int obase = nb * g.NB + c;
+          // per-filter constants for these 16 columns (uniform across lanes)
+          int swv[16];
+          float av[16];
+          if (vec_ok && obase + 16 <= g.O) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          for (int c = col0; c < col0 + half_cols; c += 16) {
+            for (int q = 0; q < 4; ++q) {
+              const int4 si = __ldg(reinterpret_cast<const int4*>(sw + obase) + q);
+              const float4 ai = __ldg(reinterpret_cast<const float4*>(alpha + obase) + q);
+              swv[4 * q] = si.x; swv[4 * q + 1] = si.y; swv[4 * q + 2] = si.z; swv[4 * q + 3] = si.w;
+              av[4 * q] = ai.x; av[4 * q + 1] = ai.y; av[4 * q + 2] = ai.z; av[4 * q + 3] = ai.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const bool in = obase + j < g.O;
+              swv[j] = in ? __ldg(sw + obase + j) : 0;
+              av[j] = in ? __ldg(alpha + obase + j) : 0.0f;
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < MH; ++h) {
             uint32_t v[16];
-            tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + buf * (2 * g.NB) + h * g.NB + c, v);
+            tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NB) + h * g.NB + c, v);
             if (!ok[h]) continue;
-            const int obase = nb * g.NB + c;
             const size_t pix = (size_t)n * g.O * plane_out + (size_t)rr[h] * g.ow + cc[h];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const int o = obase + j;
               if (o < g.O) {
-                const int accv = __ldg(sw + o) - 2 * (int)v[j];
+                const int accv = swv[j] - 2 * (int)v[j];
                 const size_t idx = pix + (size_t)o * plane_out;
-                if (y) __stcs(y + idx, __fmul_rn(__fmul_rn((float)accv, kv[h]), __ldg(alpha + o)));
+                if (y) __stcs(y + idx, __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]));
                 if (acc_out) acc_out[idx] = accv;
               }
             }
@@ -341,7 +365,10 @@ __global__ void k_weight_sign_sums(const T* __restrict__ w, int O, int C, int kk
   sw[o] = s;
 }
 
-static int umma_nb(int O) { return O >= 128 ? 128 : round_up(O, 32); }
+// Filters per block.  Independent of the image shape (the weights are packed
+// before the input is seen): 64, or O rounded up to 32 for narrow layers, so
+// 2 accumulators x MH row blocks x NB columns fit the 512 TMEM columns for MH <= 4.
+static int umma_nb(int O) { return O >= 64 ? 64 : round_up(O, 32); }
 
 size_t umma_weight_bytes(int O, int C, int kh, int kw) {
   const int NB = umma_nb(O);
@@ -363,26 +390,36 @@ int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int
   return launch_status();
 }
 
-static bool umma_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, UmmaGeom& g,
-                      size_t& smem) {
-  g.C = C; g.H = H; g.W = W; g.O = O; g.kh = kh; g.kw = kw; g.pad = pad;
+static bool umma_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int pad, int MH, UmmaGeom& g,
+                         size_t& smem) {
+  g.C = C; g.H = H; g.W = W; g.O = O; g.kh = kh; g.kw = kw; g.pad = pad; g.MH = MH;
   g.oh = H + 2 * pad - kh + 1; g.ow = W + 2 * pad - kw + 1;
   g.IC = W + 2 * pad;
   g.KBn = cdiv(C, 128);
   g.NB = umma_nb(O);
   g.taps = kh * kw;
-  // padded input rows a tile touches: pixel indices off0 .. off0+255 + (kh-1)*IC + kw-1
-  g.R = (g.IC - 1 + kU2MT - 1 + kw - 1) / g.IC + kh;
+  const int MT = 128 * MH;
+  // padded input rows a tile touches: pixel indices off0 .. off0+MT-1 + (kh-1)*IC + kw-1
+  g.R = (g.IC - 1 + MT - 1 + kw - 1) / g.IC + kh;
   g.box_bytes = (uint32_t)g.R * g.IC * 128u;
   g.plane_bytes = round_up(g.R * g.IC * 128, 1024);
-  g.n_mt = cdiv(g.oh * g.IC, kU2MT);
+  g.n_mt = cdiv(g.oh * g.IC, MT);
   g.n_nb = cdiv(O, g.NB);
   g.tiles = N * g.n_mt;
-  const int cols = 4 * g.NB;  // two accumulators x two M halves
+  const int cols = 2 * MH * g.NB;  // two accumulators x MH row blocks
   g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   smem = (size_t)g.KBn * g.plane_bytes + (size_t)kU2Stages * g.NB * 128 + 1024;
-  return g.KBn <= kU2MaxKB && g.IC <= 256 && g.R <= 256 && smem <= 226 * 1024 &&
+  return cols <= 512 && g.KBn <= kU2MaxKB && g.IC <= 256 && g.R <= 256 && smem <= 225 * 1024 &&
          (long)N * g.n_mt < 0x7fffffffL;
+}
+
+// Larger pixel tiles cut the filter-chunk traffic per MAC (the B operand is
+// re-read once per tile): prefer 4 x 128 pixels per tile when the input rows fit
+// shared memory, else 2 x 128.
+static bool umma_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, UmmaGeom& g,
+                      size_t& smem) {
+  if (umma_plan_mh(N, C, H, W, O, kh, kw, pad, 4, g, smem)) return true;
+  return umma_plan_mh(N, C, H, W, O, kh, kw, pad, 2, g, smem);
 }
 
 bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
@@ -422,17 +459,19 @@ int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw
                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return XNC_ENOTSUP;
-  static size_t attr_smem = 0;  // one-time (per size increase) shared-memory opt-in
-  if (smem > attr_smem) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
-    attr_smem = smem;
-  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = g.tiles < sms ? g.tiles : sms;
-  k_conv_umma<<<grid, kU2Threads, smem, s>>>(map, wq, sw, K, alpha, g, y, acc);
+  static size_t attr_smem[2] = {0, 0};  // one-time (per size increase) shared-memory opt-in
+  auto kern = g.MH == 4 ? k_conv_umma<4> : k_conv_umma<2>;
+  size_t& attr = attr_smem[g.MH == 4 ? 1 : 0];
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
+    attr = smem;
+  }
+  kern<<<grid, kU2Threads, smem, s>>>(map, wq, sw, K, alpha, g, y, acc);
   return launch_status();
 }
 

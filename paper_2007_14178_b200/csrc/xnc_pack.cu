@@ -17,44 +17,55 @@
 
 namespace xnc {
 
-// 32 sign bits -> 32 d-bytes, d = 1 for a negative sign (the tcgen05 operand).
-__device__ __forceinline__ void store_d32(uint8_t* dst, uint32_t d) {
-  uint32_t w[8];
-#pragma unroll
-  for (int b = 0; b < 8; ++b) w[b] = (((d >> (4 * b)) & 0xFu) * 0x00204081u) & 0x01010101u;
-  reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-  reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+// Kernel K1.  Block = 256 threads x VEC consecutive pixels (linear pixel index
+// q = n*HW + p, contiguous for the whole block because HW % VEC == 0).
+// Phase 1: each thread walks the C channels of its pixels (16-byte coalesced
+// loads, x read once), builds one 32-channel word per pixel per j and the A
+// sum, and parks the words in shared memory as [j][pixel] (16-byte stores).
+// Phase 2: the block writes the packed outputs from shared memory with
+// consecutive lanes on consecutive addresses -- bits as [q][Cw] words and/or
+// the tcgen05 operand as d-bytes [q][Cpad] (d = 1 for x < 0, 0 for c >= C),
+// 512 contiguous bytes per warp store.
+constexpr int kPackThreads = 256;
+
+__device__ __forceinline__ uint4 expand_d16(uint32_t d16) {
+  uint4 r;
+  r.x = ((d16 & 0xFu) * 0x00204081u) & 0x01010101u;
+  r.y = (((d16 >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
+  r.z = (((d16 >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
+  r.w = (((d16 >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
+  return r;
 }
 
-// bits (u32 [N][HW][Cw]) and/or dbytes (u8 [N][HW][Cpad], d = 1 for x < 0, zero
-// for c >= C) -- the popc kernels read bits, the tcgen05 kernel reads d-bytes.
 template <int VEC>
-__global__ void __launch_bounds__(256) k_pack_input(const float* __restrict__ x, int C, int HW,
-                                                    int Cw, float inv, long groups_per_img,
-                                                    long total_groups,
-                                                    uint32_t* __restrict__ bits,
-                                                    float* __restrict__ A,
-                                                    uint8_t* __restrict__ dbytes, int Cpad) {
-  long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= total_groups) return;
-  const long n = gid / groups_per_img;
-  const int p0 = (int)(gid - n * groups_per_img) * VEC;
-  const float* xp = x + (long)n * C * HW + p0;
-  uint32_t* bp = bits ? bits + ((long)n * HW + p0) * Cw : nullptr;
-  uint8_t* dp = dbytes ? dbytes + ((long)n * HW + p0) * Cpad : nullptr;
-
-  float s[VEC];
+__global__ void __launch_bounds__(kPackThreads) k_pack_input(const float* __restrict__ x, int C, int HW,
+                                                             int Cw, float inv, long groups_per_img,
+                                                             long total_groups,
+                                                             uint32_t* __restrict__ bits,
+                                                             float* __restrict__ A,
+                                                             uint8_t* __restrict__ dbytes, int Cpad) {
+  extern __shared__ uint4 pack_smem[];
+  uint32_t* wtile = reinterpret_cast<uint32_t*>(pack_smem);
+  constexpr int PIX = kPackThreads * VEC;     // pixels per block
+  constexpr int JS = PIX + 4;                 // word-plane stride (bank skew, keeps 16 B alignment)
+  const long gid0 = (long)blockIdx.x * kPackThreads;
+  const long gid = gid0 + threadIdx.x;
+  const long q0 = gid0 * VEC;                 // first linear pixel of the block
+  const long q_end = total_groups * VEC;
+  if (gid < total_groups) {
+    const long n = gid / groups_per_img;
+    const int p0 = (int)(gid - n * groups_per_img) * VEC;
+    const float* xp = x + (long)n * C * HW + p0;
+    float s[VEC];
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) s[i] = 0.0f;
-
-  for (int j = 0; j < Cw; ++j) {
-    uint32_t word[VEC];
+    for (int i = 0; i < VEC; ++i) s[i] = 0.0f;
+    for (int j = 0; j < Cw; ++j) {
+      uint32_t word[VEC];
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) word[i] = 0u;
-    const int cend = min(32, C - 32 * j);
-    if (cend == 32) {
+      for (int i = 0; i < VEC; ++i) word[i] = 0u;
+      const int cend = min(32, C - 32 * j);
 #pragma unroll 8
-      for (int cc = 0; cc < 32; ++cc) {
+      for (int cc = 0; cc < cend; ++cc) {
         const float* src = xp + (long)(32 * j + cc) * HW;
         float v[VEC];
         if constexpr (VEC == 4) {
@@ -70,48 +81,44 @@ __global__ void __launch_bounds__(256) k_pack_input(const float* __restrict__ x,
           word[i] |= (v[i] >= 0.0f ? 1u : 0u) << cc;
         }
       }
-    } else {
-      for (int cc = 0; cc < cend; ++cc) {
-        const float* src = xp + (long)(32 * j + cc) * HW;
-        float v[VEC];
-        if constexpr (VEC == 4) {
-          float4 t = __ldcs(reinterpret_cast<const float4*>(src));
-          v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-        } else {
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) v[i] = __ldcs(src + i);
-        }
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) {
-          s[i] = __fadd_rn(s[i], fabsf(v[i]));
-          word[i] |= (v[i] >= 0.0f ? 1u : 0u) << cc;
-        }
+      if constexpr (VEC == 4) {
+        *reinterpret_cast<uint4*>(wtile + j * JS + threadIdx.x * 4) = make_uint4(word[0], word[1], word[2], word[3]);
+      } else {
+        wtile[j * JS + threadIdx.x] = word[0];
       }
     }
-    if (bp) {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) bp[(long)i * Cw + j] = word[i];
-    }
-    if (dp) {
-      const uint32_t valid = cend == 32 ? 0xFFFFFFFFu : ((1u << cend) - 1u);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) store_d32(dp + (long)i * Cpad + 32 * j, ~word[i] & valid);
+    if (A != nullptr) {
+      float* ap = A + (long)n * HW + p0;
+      if constexpr (VEC == 4) {
+        *reinterpret_cast<float4*>(ap) = make_float4(__fmul_rn(s[0], inv), __fmul_rn(s[1], inv),
+                                                     __fmul_rn(s[2], inv), __fmul_rn(s[3], inv));
+      } else {
+        ap[0] = __fmul_rn(s[0], inv);
+      }
     }
   }
-  if (dp) {
-    for (int c = 32 * Cw; c < Cpad; c += 16)
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) *reinterpret_cast<uint4*>(dp + (long)i * Cpad + c) = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const int npix = (int)min((long)PIX, q_end - q0);
+  if (bits != nullptr) {
+    uint32_t* bp = bits + q0 * Cw;
+    for (int idx = threadIdx.x; idx < npix * Cw; idx += kPackThreads) {
+      const int px = idx / Cw, j = idx - px * Cw;
+      bp[idx] = wtile[j * JS + px];
+    }
   }
-  if (A != nullptr) {
-    float* ap = A + (long)n * HW + p0;
-    if constexpr (VEC == 4) {
-      *reinterpret_cast<float4*>(ap) =
-          make_float4(__fmul_rn(s[0], inv), __fmul_rn(s[1], inv), __fmul_rn(s[2], inv),
-                      __fmul_rn(s[3], inv));
-    } else {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) ap[i] = __fmul_rn(s[i], inv);
+  if (dbytes != nullptr) {
+    const int chunks = Cpad >> 4;  // 16 channels per 16-byte chunk
+    uint8_t* dp = dbytes + q0 * Cpad;
+    for (int idx = threadIdx.x; idx < npix * chunks; idx += kPackThreads) {
+      const int px = idx / chunks, ch = idx - px * chunks;
+      const int j = ch >> 1;
+      uint32_t d16 = 0u;
+      if (j < Cw) {
+        const int c0 = ch * 16;
+        const uint32_t valid = C - c0 >= 16 ? 0xFFFFu : (C > c0 ? ((1u << (C - c0)) - 1u) : 0u);
+        d16 = (~(wtile[j * JS + px] >> ((ch & 1) * 16))) & valid;
+      }
+      *reinterpret_cast<uint4*>(dp + (long)px * Cpad + ch * 16) = expand_d16(d16);
     }
   }
 }
@@ -123,16 +130,26 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   const float inv = (float)(1.0 / (double)C);  // <real_t>(1.0 / channels), _kernels_cy.pyx:258
   const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
                     (A == nullptr || (reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  const int vec = vec4 ? 4 : 1;
+  const size_t smem = (size_t)Cw * (kPackThreads * vec + 4) * 4;
+  if (smem > 200 * 1024) return XNC_ENOTSUP;  // C > ~12k channels
+  const long gpi = HW / vec, total = gpi * N;
+  const unsigned blocks = (unsigned)cdivl(total, kPackThreads);
+  const int Cpad = round_up(C, 128);
   if (vec4) {
-    long gpi = HW / 4, total = gpi * N;
-    long blocks = cdivl(total, 256);
-    k_pack_input<4><<<(unsigned)blocks, 256, 0, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, dbytes,
-                                                     round_up(C, 128));
+    static size_t attr4 = 0;
+    if (smem > 48 * 1024 && smem > attr4) {
+      cudaFuncSetAttribute(k_pack_input<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr4 = smem;
+    }
+    k_pack_input<4><<<blocks, kPackThreads, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, dbytes, Cpad);
   } else {
-    long gpi = HW, total = gpi * N;
-    long blocks = cdivl(total, 256);
-    k_pack_input<1><<<(unsigned)blocks, 256, 0, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, dbytes,
-                                                     round_up(C, 128));
+    static size_t attr1 = 0;
+    if (smem > 48 * 1024 && smem > attr1) {
+      cudaFuncSetAttribute(k_pack_input<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr1 = smem;
+    }
+    k_pack_input<1><<<blocks, kPackThreads, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, dbytes, Cpad);
   }
   return launch_status();
 }
