@@ -41,7 +41,10 @@ CONFIGS = {
     "C2k7": (64, 128, 64, 64, 128, 7),
     "C3": (256, 256, 56, 56, 256, 3),
 }
+NETWORK_CONFIGS = {"C4": 256, "C5": 2048}  # XNOR-Net AlexNet forward; C5 = global batch over ranks
 CONFIG_TEXT = {
+    "C4": "binary AlexNet/XNOR-Net full forward, random-init, 224x224 synthetic, batch 256 (BASELINE config 4)",
+    "C5": "batch-sharded XNOR-Net forward, global batch 2048 over the ranks (BASELINE config 5)",
     "C1": "single XNOR conv layer 3x3, C_in=C_out=64, 32x32, batch 1",
     "C2k3": "XNOR conv 3x3, C=128, 64x64, batch 64", "C2k5": "XNOR conv 5x5, C=128, 64x64, batch 64",
     "C2k7": "XNOR conv 7x7, C=128, 64x64, batch 64",
@@ -401,6 +404,74 @@ def run_ours(args, cfg_name):
     return result
 
 
+def run_network(args, cfg_name):
+    """C4 / C5: full XNOR-Net AlexNet forward.  Binary layers through XnorConv2d
+    (tcgen05 / popc kernels), conv1 / pools / fc8 full precision via torch.
+    C5 shards a global batch of 2048 contiguously over the ranks (strong scaling,
+    per-rank weight replicas from the same seed, no collective on the hot path)."""
+    import torch
+    from paper_2007_14178_b200.network import BINARY_MACS_PER_IMAGE, XnorNetAlexNet
+    from paper_2007_14178_b200.shard import shard_bounds
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    gb = NETWORK_CONFIGS[cfg_name] if cfg_name == "C5" else NETWORK_CONFIGS[cfg_name] * ws
+    a, b = shard_bounds(gb, ws, rank)
+    N = b - a
+    g = torch.Generator().manual_seed(1000 + rank)
+    x_host = (torch.rand((N, 3, 224, 224), generator=g) * 2 - 1).pin_memory()
+    x = x_host.to(dev)
+    net = XnorNetAlexNet(dev, seed=7, variant=args.variant)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        net(x)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        torch.distributed.barrier()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            logits = net(x)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws, dev)
+    # e2e: host images in, host logits out, copies timed
+    logits_host = torch.empty(tuple(logits.shape), dtype=torch.float32).pin_memory()
+    e0.record(stream)
+    for _ in range(max(2, min(args.steps, 5))):
+        logits_host.copy_(net(x_host.to(dev, non_blocking=True)), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / max(2, min(args.steps, 5)), ws, dev)
+    bops = 2.0 * BINARY_MACS_PER_IMAGE * gb
+    res = None
+    if rank == 0:
+        res = {"metric": METRIC, "value": bops / (ms * 1e-3) / 1e9, "unit": "Gbinop/s", "n_gpus": ws,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "strong" if cfg_name == "C5" else "weak", "vs_baseline": None,
+               "dtype": "1-bit signs (binary layers), f32 conv1/fc8", "data": "synthetic U(-1,1), random-init weights",
+               "config": {"workload": CONFIG_TEXT[cfg_name], "name": cfg_name, "global_batch": gb,
+                          "batch_per_gpu": N, "variant": args.variant,
+                          "binary_kernels": net.binary_kernels(N),
+                          "parallelism": f"batch-sharded x{ws}, per-rank weight replicas, no collective"},
+               "images_per_s": gb / (ms * 1e-3),
+               "binops_per_image": 2.0 * BINARY_MACS_PER_IMAGE,
+               "gpu_launches": None,
+               "e2e": {"value": bops / (e2e_ms * 1e-3) / 1e9, "unit": "Gbinop/s",
+                       "h2d_bytes_per_step": x_host.numel() * 4 * ws, "d2h_bytes_per_step": logits_host.numel() * 4 * ws,
+                       "ms_per_step": e2e_ms, "api": "XnorNetAlexNet.forward"},
+               "clocks": clk.summary()}
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return res
+
+
 def cpu_baseline_fields(cfg_name, budget_s, ksweep=None):
     cfg = CONFIGS[cfg_name]
     rr = RefRunner(cfg)
@@ -460,7 +531,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="C3")
+    ap.add_argument("--config", choices=sorted(CONFIGS) + sorted(NETWORK_CONFIGS), default="C3")
     ap.add_argument("--variant", choices=["popc", "b1mma", "umma", "auto"], default="popc")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-ksweep", action="store_true")
@@ -469,7 +540,9 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
-        res = run_reference(args, args.config)
+        res = run_reference(args, args.config if args.config in CONFIGS else "C3")
+    elif args.config in NETWORK_CONFIGS:
+        res = run_network(args, args.config)
     else:
         res = run_ours(args, args.config)
         ws, rank, _ = dist_env()

@@ -39,6 +39,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "xnc_common.cuh"
 
 namespace xnc {
@@ -131,6 +134,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
 struct UmmaGeom {
   int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NB, R, plane_bytes, n_mt, n_nb, tiles, taps, MH;
   uint32_t box_bytes, tmem_cols;
+  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
 };
 
 // MH = M=128 row blocks per tile (tile = 128*MH extended pixels); the two TMEM
@@ -179,6 +183,10 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
               const uint32_t st = step % kU2Stages;
               if (step >= kU2Stages) mbar_wait(&b_empty[st], ((step / kU2Stages) - 1) & 1);
+              if ((g.debug & 2) && step >= kU2Stages) {
+                mbar_arrive(&b_full[st]);  // profiling: reuse resident chunks, no traffic
+                continue;
+              }
               mbar_expect_tx(&b_full[st], b_bytes);
               const size_t chunk = ((size_t)nb * g.taps + tap) * g.KBn + kb;
               bulk_load(b_s + st * b_bytes, wq + chunk * b_bytes, b_bytes, &b_full[st]);
@@ -200,14 +208,20 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
     }
   } else if (warp == 1) {
     // ================= MMA issuer
+    // Descriptors are built once and advanced by adding (byte offset >> 4) to
+    // the start-address field (addresses < 256 KB never carry out of it), so
+    // each MMA costs one 64-bit add: the issue loop must stay well ahead of
+    // the tensor core (a 128x128x32 i8 MMA retires in ~67 cycles).
     if (lane == 0) {
       const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(g.NB >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
-      const uint32_t a_base = smem_addr(a_s), b_base = smem_addr(b_s);
+      const uint64_t a_desc0 = umma_desc_sw128(smem_addr(a_s));
+      const uint64_t b_desc0 = umma_desc_sw128(smem_addr(b_s));
+      const uint32_t plane16 = (uint32_t)g.plane_bytes >> 4, b16 = b_bytes >> 4;
       uint32_t step = 0, item = 0, it = 0;
       for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, ++it) {
         const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * (128 * MH);
-        const int off0 = m0 - (m0 / g.IC) * g.IC;
+        const uint32_t tile16 = (uint32_t)(m0 - (m0 / g.IC) * g.IC) * 8u;  // off0 rows x 128 B / 16
         for (int nb = 0; nb < g.n_nb; ++nb, ++item) {
           const uint32_t buf = item & 1;
           if (item >= 2) {
@@ -215,28 +229,29 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
             asm volatile("tcgen05.fence::after_thread_sync;");
           }
           const uint32_t d0 = tmem + buf * (MH * g.NB);
+          uint32_t acc = 0;
           for (int kb = 0; kb < g.KBn; ++kb) {
             if (nb == 0) {
               mbar_wait(&a_full[kb], it & 1);
               asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            const uint32_t plane = a_base + (uint32_t)kb * g.plane_bytes + (uint32_t)off0 * 128u;
-            for (int tap = 0; tap < g.taps; ++tap, ++step) {
-              const uint32_t st = step % kU2Stages;
-              const int ky = tap / g.kw, kx = tap - ky * g.kw;
-              mbar_wait(&b_full[st], (step / kU2Stages) & 1);
-              asm volatile("tcgen05.fence::after_thread_sync;");
-              const uint32_t a_tap = plane + (uint32_t)(ky * g.IC + kx) * 128u;
-              const uint32_t b_st = b_base + st * b_bytes;
+            const uint64_t a_kb = a_desc0 + kb * plane16 + tile16;
+            for (int ky = 0; ky < g.kh; ++ky) {
+              for (int kx = 0; kx < g.kw; ++kx, ++step) {
+                const uint32_t st = step % kU2Stages;
+                mbar_wait(&b_full[st], (step / kU2Stages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint64_t a_tap = a_kb + (uint32_t)(ky * g.IC + kx) * 8u;
+                const uint64_t b_st = b_desc0 + st * b16;
 #pragma unroll
-              for (int s = 0; s < 4; ++s) {
-                const uint64_t bd = umma_desc_sw128(b_st + s * 32);
-                const uint32_t acc = (kb | tap | s) != 0;
+                for (int s = 0; s < 4; ++s) {
 #pragma unroll
-                for (int h = 0; h < MH; ++h)
-                  umma_i8(d0 + h * g.NB, umma_desc_sw128(a_tap + h * 128 * 128 + s * 32), bd, idesc, acc);
+                  for (int h = 0; h < MH; ++h)
+                    umma_i8(d0 + h * g.NB, a_tap + h * 1024 + 2 * s, b_st + 2 * s, idesc, acc | (uint32_t)s);
+                }
+                acc = 1;
+                umma_commit(&b_empty[st]);
               }
-              umma_commit(&b_empty[st]);
             }
             if (nb == g.n_nb - 1) umma_commit(&a_empty[kb]);
           }
@@ -296,7 +311,7 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
           for (int h = 0; h < MH; ++h) {
             uint32_t v[16];
             tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NB) + h * g.NB + c, v);
-            if (!ok[h]) continue;
+            if (!ok[h] || (g.debug & 1)) continue;
             const size_t pix = (size_t)n * g.O * plane_out + (size_t)rr[h] * g.ow + cc[h];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -365,10 +380,28 @@ __global__ void k_weight_sign_sums(const T* __restrict__ w, int O, int C, int kk
   sw[o] = s;
 }
 
-// Filters per block.  Independent of the image shape (the weights are packed
-// before the input is seen): 64, or O rounded up to 32 for narrow layers, so
-// 2 accumulators x MH row blocks x NB columns fit the 512 TMEM columns for MH <= 4.
-static int umma_nb(int O) { return O >= 64 ? 64 : round_up(O, 32); }
+// Tile shape.  NB (filters per block) must not depend on the image shape, since
+// the weights are packed before any input is seen; MH (M=128 row blocks per tile)
+// is picked per shape.  2 accumulators x MH x NB columns must fit 512 TMEM cols.
+// XNC_UMMA_TILE="MH,NB" overrides both (tuning knob, read once per process).
+struct UmmaTilePref {
+  int mh = 2, nb = 128;
+  UmmaTilePref() {
+    if (const char* e = getenv("XNC_UMMA_TILE")) {
+      int a = 0, b = 0;
+      if (sscanf(e, "%d,%d", &a, &b) == 2 && (a == 1 || a == 2 || a == 4) && b >= 32 && b % 32 == 0 &&
+          2 * a * b <= 512) {
+        mh = a;
+        nb = b;
+      }
+    }
+  }
+};
+static const UmmaTilePref& tile_pref() {
+  static UmmaTilePref p;
+  return p;
+}
+static int umma_nb(int O) { return O >= tile_pref().nb ? tile_pref().nb : round_up(O, 32); }
 
 size_t umma_weight_bytes(int O, int C, int kh, int kw) {
   const int NB = umma_nb(O);
@@ -413,13 +446,12 @@ static bool umma_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
          (long)N * g.n_mt < 0x7fffffffL;
 }
 
-// Larger pixel tiles cut the filter-chunk traffic per MAC (the B operand is
-// re-read once per tile): prefer 4 x 128 pixels per tile when the input rows fit
-// shared memory, else 2 x 128.
+// Preferred MH first, then smaller tiles if the input rows do not fit shared memory.
 static bool umma_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, UmmaGeom& g,
                       size_t& smem) {
-  if (umma_plan_mh(N, C, H, W, O, kh, kw, pad, 4, g, smem)) return true;
-  return umma_plan_mh(N, C, H, W, O, kh, kw, pad, 2, g, smem);
+  for (int mh = tile_pref().mh; mh >= 1; mh /= 2)
+    if (umma_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem)) return true;
+  return false;
 }
 
 bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
@@ -459,13 +491,17 @@ int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw
                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return XNC_ENOTSUP;
+  {
+    static const int dbg = getenv("XNC_UMMA_DEBUG") ? atoi(getenv("XNC_UMMA_DEBUG")) : 0;
+    g.debug = dbg;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = g.tiles < sms ? g.tiles : sms;
-  static size_t attr_smem[2] = {0, 0};  // one-time (per size increase) shared-memory opt-in
-  auto kern = g.MH == 4 ? k_conv_umma<4> : k_conv_umma<2>;
-  size_t& attr = attr_smem[g.MH == 4 ? 1 : 0];
+  static size_t attr_smem[3] = {0, 0, 0};  // one-time (per size increase) shared-memory opt-in
+  auto kern = g.MH == 4 ? k_conv_umma<4> : g.MH == 2 ? k_conv_umma<2> : k_conv_umma<1>;
+  size_t& attr = attr_smem[g.MH == 4 ? 2 : g.MH == 2 ? 1 : 0];
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;

@@ -82,6 +82,8 @@ class XnorConv2d:
         x = x.contiguous()
         self.out_shape(x.shape)
         variant = self.kernel_for(x.shape)
+        if variant == "popc-fc":
+            return self._forward_fc(x, out, want_acc)
         if variant == "popc" and not want_acc:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
         bits, A = ops.pack_input_umma(x) if variant == "umma" else ops.pack_input(x)
@@ -92,11 +94,51 @@ class XnorConv2d:
 
     def kernel_for(self, x_shape) -> str:
         """The conv kernel a forward of this input shape runs: 'auto' picks the
-        tcgen05 kernel whenever its shared-memory plan fits the shape, else popc."""
+        tcgen05 kernel whenever its shared-memory plan fits the shape; a fully
+        connected shape (kernel == input, pad 0, 1x1 output) runs the popc kernel
+        with the batch laid out as the image width ('popc-fc'); else popc."""
+        N, C, H, W = x_shape
         if self.variant != "auto":
             return self.variant
+        if ops.umma_supported(N, C, H, W, self.O, self.kh, self.kw, self.pad):
+            return "umma"
+        if self._fc_shape(x_shape):
+            return "popc-fc"
+        return "popc"
+
+    def _fc_shape(self, x_shape) -> bool:
         N, C, H, W = x_shape
-        return "umma" if ops.umma_supported(N, C, H, W, self.O, self.kh, self.kw, self.pad) else "popc"
+        return self.pad == 0 and self.kh == H and self.kw == W and C % 32 == 0 and N > 1
+
+    def _forward_fc(self, x: torch.Tensor, out: torch.Tensor | None, want_acc: bool):
+        """Fully connected binary layer (kernel covers the whole input): every image
+        is one 'pixel' of a 1-row image whose channels are the (y, x, c) words of
+        the image, so the popc kernel's column tiling runs over the batch.  Same
+        arithmetic as the conv view: C' = kh*kw*C valid bits, K = box mean of A
+        over the whole input, alpha per filter."""
+        N, C, H, W = x.shape
+        bits, A = ops.pack_input(x)
+        K = ops.scale_map(A, self.kh, self.kw, 0)                     # [N, 1, 1]
+        fcf = self._fc_filters()
+        y1, acc1 = ops.xnor_conv(bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,
+                                 want_acc=want_acc)                  # [1, O, 1, N]
+        y = y1.view(self.O, N).t().reshape(N, self.O, 1, 1)
+        if out is not None:
+            out.copy_(y)
+            y = out
+        if want_acc:
+            return y, acc1.view(self.O, N).t().reshape(N, self.O, 1, 1).contiguous()
+        return y.contiguous()
+
+    def _fc_filters(self) -> ops.PackedFilters:
+        f = getattr(self, "_fcf", None)
+        if f is None:
+            pf = self.filters
+            wb = pf.wbits.permute(1, 2, 0, 3).contiguous()            # [kh, kw, Cw, O]
+            f = ops.PackedFilters(wb.view(-1, 1, 1, self.O), pf.alpha, pf.alpha64, self.O,
+                                  self.kh * self.kw * self.C, 1, 1)
+            self._fcf = f
+        return f
 
     __call__ = forward
 

@@ -1,0 +1,85 @@
+"""XNOR-Net / AlexNet forward (BASELINE.json configs 4 and 5).
+
+The reference has no network object, so the
+network is composed from reference-expressible binary layers -- stride-1
+binary convolutions with k <= 8 and explicit padding -- with the rest of
+XNOR-Net AlexNet in full precision through torch (cuDNN), off the binary hot
+path:
+
+    conv1  11x11/4, 3 -> 96      full precision      224 -> 55
+    pool   3/2                                       55 -> 27
+    conv2  5x5 pad 2, 96 -> 256  BINARY (XnorConv2d) 27
+    pool   3/2                                       27 -> 13
+    conv3  3x3 pad 1, 256 -> 384 BINARY              13
+    conv4  3x3 pad 1, 384 -> 384 BINARY              13
+    conv5  3x3 pad 1, 384 -> 256 BINARY              13
+    pool   3/2                                       13 -> 6
+    fc6    6x6 valid, 256 -> 4096 BINARY (a k = H = W conv)  1x1
+    fc7    1x1, 4096 -> 4096     BINARY              1x1
+    fc8    4096 -> 1000          full precision
+
+Binary MACs per image: 1.026e9.  Every binary layer
+is the reference semantics end to end: sign(0) = +1, +1 padding, per-filter
+alpha, K from the channel mean of |input| (xnor_conv(x[n], w[o]) for every
+pair).  Weights are random-init (no checkpoints offline).
+"""
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+from .layer import XnorConv2d
+
+BINARY_LAYERS = (  # name, C_in, C_out, k, pad
+    ("conv2", 96, 256, 5, 2),
+    ("conv3", 256, 384, 3, 1),
+    ("conv4", 384, 384, 3, 1),
+    ("conv5", 384, 256, 3, 1),
+    ("fc6", 256, 4096, 6, 0),
+    ("fc7", 4096, 4096, 1, 0),
+)
+BINARY_MACS_PER_IMAGE = (27 * 27 * 256 * 96 * 25 + 13 * 13 * 384 * 256 * 9 + 13 * 13 * 384 * 384 * 9
+                         + 13 * 13 * 256 * 384 * 9 + 4096 * 256 * 36 + 4096 * 4096)
+
+
+class XnorNetAlexNet:
+    """Random-init XNOR-Net AlexNet resident on one device."""
+
+    def __init__(self, device: torch.device | str = "cuda", num_classes: int = 1000, seed: int = 0,
+                 variant: str = "auto"):
+        dev = torch.device(device)
+        g = torch.Generator().manual_seed(seed)
+
+        def rnd(*shape, scale=1.0):
+            return ((torch.rand(shape, generator=g) * 2 - 1) * scale).to(dev)
+
+        self.device = dev
+        self.conv1_w = rnd(96, 3, 11, 11, scale=(3 * 121) ** -0.5)
+        self.conv1_b = rnd(96, scale=0.1)
+        self.binary: dict[str, XnorConv2d] = {}
+        for name, cin, cout, k, pad in BINARY_LAYERS:
+            self.binary[name] = XnorConv2d(rnd(cout, cin, k, k), pad=pad, variant=variant)
+        self.fc8_w = rnd(num_classes, 4096, scale=4096 ** -0.5)
+        self.fc8_b = rnd(num_classes, scale=0.1)
+
+    @torch.no_grad()
+    def forward(self, x: torch.Tensor, return_features: bool = False):
+        """x f32 [N, 3, 224, 224] (CUDA) -> logits f32 [N, num_classes]."""
+        h = F.conv2d(x, self.conv1_w, self.conv1_b, stride=4, padding=2)  # full precision
+        h = F.max_pool2d(F.relu(h), 3, 2)
+        feats = {}
+        for name, *_ in BINARY_LAYERS:
+            h = self.binary[name](h.contiguous())
+            feats[name] = h
+            if name in ("conv2", "conv5"):
+                h = F.max_pool2d(h, 3, 2)
+        logits = F.linear(h.flatten(1), self.fc8_w, self.fc8_b)  # full precision
+        return (logits, feats) if return_features else logits
+
+    __call__ = forward
+
+    def binary_kernels(self, batch: int) -> dict[str, str]:
+        """Which conv kernel (umma / popc) each binary layer runs at this batch."""
+        shapes = {"conv2": (96, 27), "conv3": (256, 13), "conv4": (384, 13), "conv5": (384, 13),
+                  "fc6": (256, 6), "fc7": (4096, 1)}
+        return {n: self.binary[n].kernel_for((batch, c, s, s)) for n, (c, s) in shapes.items()}

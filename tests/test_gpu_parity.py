@@ -99,6 +99,7 @@ RANDOM_CASES = [
     (1, 7, 20, 70, 3, 3, 3, 1),
     (1, 40, 6, 6, 12, 6, 6, 0),      # fc6-style: k == H, pad 0 -> 1x1 output
     (4, 64, 1, 1, 20, 1, 1, 0),      # fc7-style 1x1
+    (6, 64, 6, 6, 40, 6, 6, 0),      # fc6-style, C % 32 == 0 -> batch-as-width popc path
     (1, 9, 30, 300, 4, 3, 3, 1),     # wide rows -> column tiling
 ]
 
@@ -150,6 +151,21 @@ def test_umma_variant_vs_oracle(shape):
     want, ints = O.conv_layer(x, w, pad, want_ints=True)
     assert np.array_equal(acc, ints)
     _assert_float_parity(y, want)
+
+
+@pytest.mark.parametrize("N,C,S,O_,k", [(5, 64, 6, 6, 6), (9, 256, 6, 50, 6), (7, 128, 1, 33, 1)])
+def test_fc_mode_matches_oracle(N, C, S, O_, k):
+    """Fully connected binary layers (k == H == W, pad 0) take the batch-as-width path."""
+    from paper_2007_14178_b200 import XnorConv2d
+    rng = np.random.default_rng([N, C, S, O_])
+    x = O.f32_exact(rng, (N, C, S, S))
+    w = O.f32_exact(rng, (O_, C, k, k))
+    layer = XnorConv2d(torch.from_numpy(w).to(_dev()), pad=0, variant="auto")
+    assert layer.kernel_for(x.shape) in ("popc-fc", "umma")
+    y, acc = layer.forward(torch.from_numpy(x).to(_dev()), want_acc=True)
+    want, ints = O.conv_layer(x, w, 0, want_ints=True)
+    assert np.array_equal(acc.cpu().numpy(), ints)
+    _assert_float_parity(y.cpu().numpy(), want)
 
 
 def test_edge_all_negative_padding_plus_one():
