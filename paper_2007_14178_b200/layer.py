@@ -37,6 +37,7 @@ class XnorConv2d:
         w = weight.detach().to(dtype=torch.float32).contiguous()
         if not w.is_cuda:
             w = w.cuda()
+        self.weight = w  # the float filters (kept for inspection / re-packing)
         self.filters = ops.pack_weights(w)
         if variant in ("umma", "auto"):
             ops.attach_umma_weights(self.filters, w)

@@ -1,0 +1,47 @@
+"""XNOR-Net AlexNet forward (BASELINE configs 4/5): every binary layer of the
+network, on the network's own intermediate activations, matches the oracle on
+sampled (image, filter) pairs; the forward is deterministic."""
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_network_binary_layers_match_oracle():
+    from paper_2007_14178_b200.network import BINARY_LAYERS, XnorNetAlexNet
+    torch.manual_seed(0)
+    net = XnorNetAlexNet("cuda", seed=3)
+    x = torch.rand((3, 3, 224, 224), device="cuda") * 2 - 1
+    logits, feats = net.forward(x, return_features=True)
+    logits2 = net.forward(x)
+    torch.cuda.synchronize()
+    assert logits.shape == (3, 1000) and torch.isfinite(logits).all()
+    assert torch.equal(logits, logits2)
+    # layer inputs: conv1 -> relu -> pool for conv2; pooled / raw previous outputs after
+    h = F.max_pool2d(F.relu(F.conv2d(x, net.conv1_w, net.conv1_b, stride=4, padding=2)), 3, 2)
+    inputs = {}
+    for name, *_ in BINARY_LAYERS:
+        inputs[name] = h
+        h = feats[name]
+        if name in ("conv2", "conv5"):
+            h = F.max_pool2d(h, 3, 2)
+    for name, cin, cout, k, pad in BINARY_LAYERS:
+        layer = net.binary[name]
+        xi = inputs[name][:2].contiguous().cpu().numpy()
+        o_idx = [0, cout // 2, cout - 1]
+        wi = layer.weight[o_idx].cpu().numpy()
+        want = O.conv_layer(xi, wi, pad)
+        got = feats[name][:2][:, o_idx].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), name
+
+
+def test_network_kernel_selection():
+    from paper_2007_14178_b200.network import XnorNetAlexNet
+    net = XnorNetAlexNet("cuda", seed=1)
+    ks = net.binary_kernels(256)
+    assert ks["fc7"] in ("popc-fc", "umma") and ks["fc6"] in ("popc-fc", "umma")
+    assert all(v in ("umma", "popc", "popc-fc") for v in ks.values())
