@@ -21,7 +21,7 @@
 // (tools/microbench/umma_probe.cu: row-shifted descriptors with base_offset = 0
 // verified against a CPU GEMM on a B200, 0 mismatches for shifts 0-9).
 //
-// Persistent, warp-specialised pipeline (one CTA per SM, 384 threads):
+// Persistent, warp-specialised pipeline (one CTA per SM, 640 threads):
 //   warp 0      B producer: cp.async.bulk of one (tap, K block) filter chunk,
 //               NB x 128 B, pre-swizzled in HBM by k_pack_weights_umma
 //   warp 1      MMA issuer (one thread): per tile and filter block,
@@ -29,8 +29,8 @@
 //   warp 2      A producer: one TMA tile load per 128-channel K block of the
 //               d-bytes written by K1 (xnc_pack_input_umma): R padded rows x IC
 //               columns x 128 B, zero fill outside the image
-//   warps 4-11  epilogue: TMEM -> registers -> S_w - 2*acc -> (f32 * K) * alpha
-//               -> y, two warps per TMEM lane quadrant
+//   warps 4-19  epilogue: TMEM -> registers -> S_w - 2*acc -> (f32 * K) * alpha
+//               -> y, four warps per TMEM lane quadrant
 // Work unit = (tile of 128*MH extended pixels of one image, filter block of NB).
 // TMEM holds two accumulators (MH x NB columns each): the epilogue of one unit
 // overlaps the MMAs of the next.  A K-block plane is released as soon as
@@ -46,11 +46,11 @@
 
 namespace xnc {
 
-constexpr int kU2Threads = 384;
+constexpr int kU2Threads = 640;
 constexpr int kU2Stages = 6;     // B pipeline depth
 constexpr int kU2MaxKB = 4;      // K blocks (128 channels each) kept resident: C <= 512
 constexpr int kU2EpiWarp0 = 4;   // first epilogue warp
-constexpr int kU2EpiWarps = 8;
+constexpr int kU2EpiWarps = 16;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -119,6 +119,18 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    smem_addr(bar))
                : "memory");
 }
+
+__device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+      " [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15])
+      : "r"(addr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
   asm volatile(
@@ -261,33 +273,43 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
     }
   } else if (warp >= kU2EpiWarp0 && warp < kU2EpiWarp0 + kU2EpiWarps) {
     // ================= epilogue
+    // 16 warps: warp w reads TMEM lane quadrant (w & 3) and the 16-column chunks
+    // cg, cg+4, ... (cg = (w-4) >> 2) of every accumulator row block.  Each
+    // thread owns one extended pixel per row block; for a chunk it issues the
+    // TMEM loads of all row blocks before one wait, then writes 16 filters x MH
+    // pixels (for a fixed filter the 32 lanes store 32 consecutive pixels).
     const int e_w = warp - kU2EpiWarp0;
     const int quad = warp & 3;              // TMEM lane quadrant this warp may access
-    const int half_cols = g.NB / 2;
-    const int col0 = (e_w >> 2) * half_cols;
+    const int cg = e_w >> 2;
+    const int n_chunks = g.NB / 16;
     const size_t plane_out = (size_t)g.oh * g.ow;
     uint32_t item = 0;
-    const bool vec_ok = (g.NB % 16 == 0) && ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
                         ((reinterpret_cast<uintptr_t>(alpha) & 15) == 0);
     for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
       const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * (128 * MH);
-      int rr[MH], cc[MH];
+      size_t pix[MH];
       bool ok[MH];
       float kv[MH];
 #pragma unroll
       for (int h = 0; h < MH; ++h) {
         const int e = m0 + h * 128 + quad * 32 + lane;
-        rr[h] = e / g.IC;
-        cc[h] = e - rr[h] * g.IC;
-        ok[h] = rr[h] < g.oh && cc[h] < g.ow;
-        kv[h] = (ok[h] && y) ? __ldg(Kmap + (size_t)n * plane_out + (size_t)rr[h] * g.ow + cc[h]) : 0.0f;
+        const int rr = e / g.IC, cc = e - (e / g.IC) * g.IC;
+        ok[h] = rr < g.oh && cc < g.ow;
+        pix[h] = (size_t)n * g.O * plane_out + (size_t)rr * g.ow + cc;
+        kv[h] = (ok[h] && y) ? __ldg(Kmap + (size_t)n * plane_out + (size_t)rr * g.ow + cc) : 0.0f;
       }
       for (int nb = 0; nb < g.n_nb; ++nb, ++item) {
         const uint32_t buf = item & 1;
         mbar_wait(&t_full[buf], (item >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        for (int c = col0; c < col0 + half_cols; c += 16) {
+        for (int ch = cg; ch < n_chunks; ch += 4) {
+          const int c = ch * 16;
           const int obase = nb * g.NB + c;
+          uint32_t v[MH][16];
+#pragma unroll
+          for (int h = 0; h < MH; ++h)
+            tmem_ld16_async(tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NB) + h * g.NB + c, v[h]);
           // per-filter constants for these 16 columns (uniform across lanes)
           int swv[16];
           float av[16];
@@ -307,18 +329,17 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
               av[j] = in ? __ldg(alpha + obase + j) : 0.0f;
             }
           }
+          tmem_wait_ld();
+          if (g.debug & 1) continue;
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
-            uint32_t v[16];
-            tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NB) + h * g.NB + c, v);
-            if (!ok[h] || (g.debug & 1)) continue;
-            const size_t pix = (size_t)n * g.O * plane_out + (size_t)rr[h] * g.ow + cc[h];
+            if (!ok[h]) continue;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const int o = obase + j;
               if (o < g.O) {
-                const int accv = swv[j] - 2 * (int)v[j];
-                const size_t idx = pix + (size_t)o * plane_out;
+                const int accv = swv[j] - 2 * (int)v[h][j];
+                const size_t idx = pix[h] + (size_t)o * plane_out;
                 if (y) __stcs(y + idx, __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]));
                 if (acc_out) acc_out[idx] = accv;
               }

@@ -123,8 +123,75 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_input(const float* __rest
   }
 }
 
+// Small-image path (few pixels, many channels: 13x13 conv3-5 inputs, the 6x6
+// fc6 input, the 1x1 fc7 input): the per-pixel kernel above would run one
+// thread per pixel over thousands of channels on a fraction of the SMs.  Here
+// the words are built by one thread per (pixel, word) and A by one thread per
+// pixel (the channel sum must stay sequential for bit-exactness); x is read
+// twice, from L2 for these sizes.
+__global__ void k_pack_words(const float* __restrict__ x, int C, int HW, int Cw, long npix,
+                             uint32_t* __restrict__ bits, uint8_t* __restrict__ dbytes, int Cpad) {
+  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= npix * Cw) return;
+  long q;
+  int j;
+  if (HW >= 32) {  // pixels fastest: coalesced NCHW reads across the warp
+    j = (int)(tid / npix);
+    q = tid - (long)j * npix;
+  } else {         // words fastest: each thread reads 32 nearby channels
+    q = tid / Cw;
+    j = (int)(tid - q * Cw);
+  }
+  const long n = q / HW, p = q - n * HW;
+  const float* xp = x + (n * C + 32L * j) * HW + p;
+  const int cend = min(32, C - 32 * j);
+  uint32_t word = 0u;
+  for (int cc = 0; cc < cend; ++cc) word |= (__ldg(xp + (long)cc * HW) >= 0.0f ? 1u : 0u) << cc;
+  if (bits) bits[q * Cw + j] = word;
+  if (dbytes) {
+    const uint32_t valid = cend == 32 ? 0xFFFFFFFFu : ((1u << cend) - 1u);
+    const uint32_t d = ~word & valid;
+    uint8_t* dp = dbytes + q * Cpad + 32 * j;
+    reinterpret_cast<uint4*>(dp)[0] = expand_d16(d & 0xFFFFu);
+    reinterpret_cast<uint4*>(dp)[1] = expand_d16(d >> 16);
+    if (j == Cw - 1)  // zero the channel padding up to Cpad
+      for (int c = 32 * Cw; c < Cpad; c += 16) *reinterpret_cast<uint4*>(dbytes + q * Cpad + c) = make_uint4(0, 0, 0, 0);
+  }
+}
+
+__global__ void k_absmean(const float* __restrict__ x, int C, int HW, long npix, float inv,
+                          float* __restrict__ A) {
+  const long q = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= npix) return;
+  const long n = q / HW, p = q - n * HW;
+  const float* xp = x + n * C * (long)HW + p;
+  float s = 0.0f;
+  if (HW == 1 && (C & 3) == 0 && ((reinterpret_cast<uintptr_t>(xp) & 15) == 0)) {
+    for (int c = 0; c < C; c += 4) {  // channels contiguous: 16-byte loads, same sequential order
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xp + c));
+      s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, fabsf(v.x)), fabsf(v.y)), fabsf(v.z)), fabsf(v.w));
+    }
+  } else {
+#pragma unroll 8
+    for (int c = 0; c < C; ++c) s = __fadd_rn(s, fabsf(__ldg(xp + (long)c * HW)));
+  }
+  A[q] = __fmul_rn(s, inv);
+}
+
 int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
                       cudaStream_t s, uint8_t* dbytes) {
+  {
+    const long npix = (long)N * H * W;
+    const long vec_groups = (H * W) % 4 == 0 ? npix / 4 : npix;
+    if (vec_groups < 2L * 148 * kPackThreads) {  // under two waves: use the 2-D small-image path
+      const int Cw = cdiv(C, 32);
+      const long words = npix * Cw;
+      k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, dbytes,
+                                                              round_up(C, 128));
+      if (A) k_absmean<<<(unsigned)cdivl(npix, 128), 128, 0, s>>>(x, C, H * W, npix, (float)(1.0 / (double)C), A);
+      return launch_status();
+    }
+  }
   const int HW = H * W;
   const int Cw = cdiv(C, 32);
   const float inv = (float)(1.0 / (double)C);  // <real_t>(1.0 / channels), _kernels_cy.pyx:258

@@ -101,10 +101,10 @@ class XnorConv2d:
         N, C, H, W = x_shape
         if self.variant != "auto":
             return self.variant
+        if self._fc_shape(x_shape):
+            return "popc-fc"  # 1x1 output: the per-image pixel tiles of the other kernels idle
         if ops.umma_supported(N, C, H, W, self.O, self.kh, self.kw, self.pad):
             return "umma"
-        if self._fc_shape(x_shape):
-            return "popc-fc"
         return "popc"
 
     def _fc_shape(self, x_shape) -> bool:

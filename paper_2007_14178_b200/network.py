@@ -25,10 +25,27 @@ pair).  Weights are random-init (no checkpoints offline).
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 import torch.nn.functional as F
 
 from .layer import XnorConv2d
+
+
+@contextlib.contextmanager
+def _tf32_full_precision_layers():
+    """TF32 tensor cores + cuDNN autotuning for conv1 / fc8, restored on exit."""
+    saved = (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32,
+             torch.backends.cudnn.benchmark)
+    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cudnn.allow_tf32 = True
+    torch.backends.cudnn.benchmark = True
+    try:
+        yield
+    finally:
+        (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32,
+         torch.backends.cudnn.benchmark) = saved
 
 BINARY_LAYERS = (  # name, C_in, C_out, k, pad
     ("conv2", 96, 256, 5, 2),
@@ -64,7 +81,15 @@ class XnorNetAlexNet:
 
     @torch.no_grad()
     def forward(self, x: torch.Tensor, return_features: bool = False):
-        """x f32 [N, 3, 224, 224] (CUDA) -> logits f32 [N, num_classes]."""
+        """x f32 [N, 3, 224, 224] (CUDA) -> logits f32 [N, num_classes].
+
+        conv1 / fc8 run on cuDNN / cuBLAS with TF32 tensor cores (full precision
+        layers of XNOR-Net, outside the binary path); the binary layers are
+        exact reference semantics."""
+        with _tf32_full_precision_layers():
+            return self._forward(x, return_features)
+
+    def _forward(self, x: torch.Tensor, return_features: bool):
         h = F.conv2d(x, self.conv1_w, self.conv1_b, stride=4, padding=2)  # full precision
         h = F.max_pool2d(F.relu(h), 3, 2)
         feats = {}
