@@ -532,7 +532,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS) + sorted(NETWORK_CONFIGS), default="C3")
-    ap.add_argument("--variant", choices=["popc", "b1mma", "umma", "auto"], default="popc")
+    ap.add_argument("--variant", choices=["popc", "b1mma", "umma", "auto"], default="auto")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-ksweep", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU reference work")

@@ -106,6 +106,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
 __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {
   asm volatile(
@@ -215,6 +222,13 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
           if (it >= 1) mbar_wait(&a_empty[kb], (it - 1) & 1);
           mbar_expect_tx(&a_full[kb], g.box_bytes);
           tma_load_4d(a_s + (size_t)kb * g.plane_bytes, &a_map, kb * 128, -g.pad, r0 - g.pad, n, &a_full[kb]);
+        }
+        // warm L2 with the next tile's rows: its loads are issued while this
+        // tile's last MMAs run, and must land before the tensor core drains
+        const int tn = t + gridDim.x;
+        if (tn < g.tiles) {
+          const int nn = tn / g.n_mt, rn = ((tn - nn * g.n_mt) * (128 * MH)) / g.IC;
+          for (int kb = 0; kb < g.KBn; ++kb) tma_prefetch_4d(&a_map, kb * 128, -g.pad, rn - g.pad, nn);
         }
       }
     }
