@@ -153,7 +153,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
 struct UmmaGeom {
   int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NB, R, plane_bytes, n_mt, n_nb, tiles, taps, MH;
   uint32_t box_bytes, tmem_cols;
-  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
+  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once,
+             // bit 2 = load the input rows once
 };
 
 // MH = M=128 row blocks per tile (tile = 128*MH extended pixels); the two TMEM
@@ -220,6 +221,10 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
         const int r0 = m0 / g.IC;
         for (int kb = 0; kb < g.KBn; ++kb) {
           if (it >= 1) mbar_wait(&a_empty[kb], (it - 1) & 1);
+          if ((g.debug & 4) && it >= 1) {  // profiling: keep the first tile's rows, no traffic
+            mbar_arrive(&a_full[kb]);
+            continue;
+          }
           mbar_expect_tx(&a_full[kb], g.box_bytes);
           tma_load_4d(a_s + (size_t)kb * g.plane_bytes, &a_map, kb * 128, -g.pad, r0 - g.pad, n, &a_full[kb]);
         }

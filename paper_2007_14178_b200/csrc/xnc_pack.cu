@@ -183,7 +183,8 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   {
     const long npix = (long)N * H * W;
     const long vec_groups = (H * W) % 4 == 0 ? npix / 4 : npix;
-    if (vec_groups < 2L * 148 * kPackThreads) {  // under two waves: use the 2-D small-image path
+    // few pixels with long channel loops (13x13 / 6x6 / 1x1 layers): the 2-D path
+    if (vec_groups < 2L * 148 * kPackThreads && C >= 256) {
       const int Cw = cdiv(C, 32);
       const long words = npix * Cw;
       k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, dbytes,
