@@ -154,7 +154,8 @@ struct UmmaGeom {
   int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NB, R, plane_bytes, n_mt, n_nb, tiles, taps, MH;
   uint32_t box_bytes, tmem_cols;
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once,
-             // bit 2 = load the input rows once
+             // bit 2 = load the input rows once, bit 3 = no B barrier protocol after the
+             // first stages, bit 4 = no tcgen05 fence after B waits
 };
 
 // MH = M=128 row blocks per tile (tile = 128*MH extended pixels); the two TMEM
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
               const uint32_t st = step % kU2Stages;
               if (step >= kU2Stages) mbar_wait(&b_empty[st], ((step / kU2Stages) - 1) & 1);
+              if ((g.debug & 8) && step >= kU2Stages) continue;  // profiling: no B protocol at all
               if ((g.debug & 2) && step >= kU2Stages) {
                 mbar_arrive(&b_full[st]);  // profiling: reuse resident chunks, no traffic
                 continue;
@@ -270,8 +272,11 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
             for (int ky = 0; ky < g.kh; ++ky) {
               for (int kx = 0; kx < g.kw; ++kx, ++step) {
                 const uint32_t st = step % kU2Stages;
-                mbar_wait(&b_full[st], (step / kU2Stages) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;");
+                const bool b_sync = !(g.debug & 8) || step < kU2Stages;
+                if (b_sync) {
+                  mbar_wait(&b_full[st], (step / kU2Stages) & 1);
+                  if (!(g.debug & 16)) asm volatile("tcgen05.fence::after_thread_sync;");
+                }
                 const uint64_t a_tap = a_kb + (uint32_t)(ky * g.IC + kx) * 8u;
                 const uint64_t b_st = b_desc0 + st * b16;
 #pragma unroll
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
                     umma_i8(d0 + h * g.NB, a_tap + h * 1024 + 2 * s, b_st + 2 * s, idesc, acc | (uint32_t)s);
                 }
                 acc = 1;
-                umma_commit(&b_empty[st]);
+                if (b_sync) umma_commit(&b_empty[st]);
               }
             }
             if (nb == g.n_nb - 1) umma_commit(&a_empty[kb]);

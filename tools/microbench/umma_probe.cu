@@ -116,13 +116,13 @@ __global__ void k_probe(const uint8_t* __restrict__ A, const int8_t* __restrict_
 
 
 // Throughput: every CTA issues `iters` x 4 MMAs (M=128, N=256, K=32) from resident smem.
-__global__ void k_rate(int iters, int n_mma, int32_t* out) {
+__global__ void k_rate(int iters, int n_mma, int shift, int32_t* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t mbar;
   const int tid = threadIdx.x;
-  for (int i = tid; i < (128 + 256) * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u;
+  for (int i = tid; i < (128 + 16 + 256) * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -138,7 +138,7 @@ __global__ void k_rate(int iters, int n_mma, int32_t* out) {
   const uint32_t tmem = tmem_base;
   const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   if (tid == 0) {
-    uint32_t a0 = smem_u32(smem), b0 = a0 + 128 * 128;
+    uint32_t a0 = smem_u32(smem) + shift * 128, b0 = smem_u32(smem) + (128 + 16) * 128;
     for (int it = 0; it < iters; ++it)
       for (int s = 0; s < 4; ++s) {
         uint64_t ad = desc_sw128(a0 + s * 32, 0), bd = desc_sw128(b0 + s * 32, 0);
@@ -196,23 +196,24 @@ int main() {
   {
     int dev; cudaGetDevice(&dev); cudaDeviceProp p; cudaGetDeviceProperties(&p, dev);
     int clk_khz; cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
-    size_t sm2 = (128 + 256) * 128 + 1024;
+    size_t sm2 = (128 + 16 + 256) * 128 + 1024;
     CK(cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    for (int n_mma : {256, 128, 64, 32}) {
+    for (int shift : {0, 1, 3, 8})
+    for (int n_mma : {256, 128}) {
       int iters = 20000 * 256 / n_mma;
-      for (int w = 0; w < 2; ++w) k_rate<<<p.multiProcessorCount, 128, sm2>>>(iters, n_mma, dD);
+      for (int w = 0; w < 2; ++w) k_rate<<<p.multiProcessorCount, 128, sm2>>>(iters, n_mma, shift, dD);
       CK(cudaDeviceSynchronize());
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       float best = 1e30f;
       for (int r = 0; r < 3; ++r) {
         cudaEventRecord(e0);
-        k_rate<<<p.multiProcessorCount, 128, sm2>>>(iters, n_mma, dD);
+        k_rate<<<p.multiProcessorCount, 128, sm2>>>(iters, n_mma, shift, dD);
         cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
         float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
       }
       double macs = (double)p.multiProcessorCount * iters * 4 * 128.0 * n_mma * 32;
-      printf("{\"bench\": \"tcgen05_i8_m128n%dk32\", \"ms\": %.4f, \"rate\": %.4e, \"unit\": \"MAC/s\", "
-             "\"per_sm_per_clk_at_max\": %.1f, \"sms\": %d}\n", n_mma, best, macs / (best * 1e-3),
+      printf("{\"bench\": \"tcgen05_i8_m128n%dk32\", \"a_row_shift\": %d, \"ms\": %.4f, \"rate\": %.4e, \"unit\": \"MAC/s\", "
+             "\"per_sm_per_clk_at_max\": %.1f, \"sms\": %d}\n", n_mma, shift, best, macs / (best * 1e-3),
              macs / (best * 1e-3) / p.multiProcessorCount / (clk_khz * 1e3), p.multiProcessorCount);
     }
   }
