@@ -108,6 +108,9 @@ int xnc_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw
                           uint8_t* wq, int32_t* sw, void* stream);
 int xnc_pack_input_umma(const float* x, int N, int C, int H, int W, uint8_t* dbytes,
                         float* A, void* stream);
+/* Profiling only: per-CTA cycle counters of the last tcgen05 conv launched with
+ * XNC_UMMA_DEBUG bit 7 set (16 u64 slots per CTA, host memory; blocking copy). */
+int xnc_umma_profile(unsigned long long* host_out, int n_ctas);
 int xnc_xnor_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw,
                        const float* K, const float* alpha, int N, int C, int H, int W,
                        int O, int kh, int kw, int pad, float* y, int32_t* acc, void* stream);

@@ -121,6 +121,11 @@ int xnc_xnor_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* 
                           as_stream(stream));
 }
 
+int xnc_umma_profile(unsigned long long* host_out, int n_ctas) {
+  if (!host_out || n_ctas < 1) return XNC_EINVAL;
+  return umma_profile_read(host_out, n_ctas);
+}
+
 size_t xnc_layer_workspace_bytes(int N, int C, int H, int W, int kh, int kw, int pad) {
   if (!conv_shape_ok(N, C, H, W, kh, kw, pad)) return 0;
   const size_t oh = H + 2 * pad - kh + 1, ow = W + 2 * pad - kw + 1;

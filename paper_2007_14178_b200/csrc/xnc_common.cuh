@@ -50,6 +50,7 @@ size_t umma_weight_bytes(int O, int C, int kh, int kw);
 bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw, uint8_t* wq,
                              int32_t* sw, cudaStream_t s);
+int umma_profile_read(unsigned long long* host, int n_ctas);
 int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s);

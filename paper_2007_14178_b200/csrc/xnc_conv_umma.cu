@@ -517,6 +517,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// Profiling counters (XNC_UMMA_DEBUG bit 7): none in this kernel yet.
+__device__ unsigned long long g_umma_prof[1024][16];
+
+int umma_profile_read(unsigned long long* host, int n_ctas) {
+  if (n_ctas > 1024) n_ctas = 1024;
+  cudaError_t e = cudaMemcpyFromSymbol(host, g_umma_prof, sizeof(unsigned long long) * 16 * n_ctas);
+  return e == cudaSuccess ? 0 : XNC_ECUDA_BASE + (int)e;
+}
+
 int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s) {

@@ -116,13 +116,24 @@ __global__ void k_probe(const uint8_t* __restrict__ A, const int8_t* __restrict_
 
 
 // Throughput: every CTA issues `iters` x 4 MMAs (M=128, N=256, K=32) from resident smem.
-__global__ void k_rate(int iters, int n_mma, int shift, int32_t* out) {
+// random != 0: A bytes random 0/1 (the d-byte operand), B bytes random +-1 (the
+// filter signs) instead of constant 0x01 -- tensor-core power is data dependent.
+__global__ void k_rate(int iters, int n_mma, int shift, int32_t* out, int random) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t mbar;
   const int tid = threadIdx.x;
-  for (int i = tid; i < (128 + 16 + 256) * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u;
+  for (int i = tid; i < (128 + 16 + 256) * 128 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x * 97u;
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    uint32_t v = 0x01010101u;
+    if (random) {
+      if (i < (128 + 16) * 128 / 4) v = h & 0x01010101u;                       // A: 0/1
+      else v = 0x01010101u | ((h & 0x01010101u) * 0xFEu);                    // B: 0x01 or 0xFF
+    }
+    reinterpret_cast<uint32_t*>(smem)[i] = v;
+  }
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -198,22 +209,23 @@ int main() {
     int clk_khz; cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
     size_t sm2 = (128 + 16 + 256) * 128 + 1024;
     CK(cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    for (int random : {0, 1})
     for (int shift : {0, 1, 3, 8})
     for (int n_mma : {256, 128}) {
       int iters = 20000 * 256 / n_mma;
-      for (int w = 0; w < 2; ++w) k_rate<<<p.multiProcessorCount, 128, sm2>>>(iters, n_mma, shift, dD);
+      for (int w = 0; w < 2; ++w) k_rate<<<p.multiProcessorCount, 128, sm2>>>(iters, n_mma, shift, dD, random);
       CK(cudaDeviceSynchronize());
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       float best = 1e30f;
       for (int r = 0; r < 3; ++r) {
         cudaEventRecord(e0);
-        k_rate<<<p.multiProcessorCount, 128, sm2>>>(iters, n_mma, shift, dD);
+        k_rate<<<p.multiProcessorCount, 128, sm2>>>(iters, n_mma, shift, dD, random);
         cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
         float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
       }
       double macs = (double)p.multiProcessorCount * iters * 4 * 128.0 * n_mma * 32;
-      printf("{\"bench\": \"tcgen05_i8_m128n%dk32\", \"a_row_shift\": %d, \"ms\": %.4f, \"rate\": %.4e, \"unit\": \"MAC/s\", "
-             "\"per_sm_per_clk_at_max\": %.1f, \"sms\": %d}\n", n_mma, shift, best, macs / (best * 1e-3),
+      printf("{\"bench\": \"tcgen05_i8_m128n%dk32\", \"random_data\": %d, \"a_row_shift\": %d, \"ms\": %.4f, \"rate\": %.4e, \"unit\": \"MAC/s\", "
+             "\"per_sm_per_clk_at_max\": %.1f, \"sms\": %d}\n", n_mma, random, shift, best, macs / (best * 1e-3),
              macs / (best * 1e-3) / p.multiProcessorCount / (clk_khz * 1e3), p.multiProcessorCount);
     }
   }
