@@ -21,11 +21,13 @@ def lib() -> ctypes.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
-    if not os.path.exists(LIB_PATH):
+    # XNC_LIB: an alternative build of the same library (tuning experiments only)
+    path = os.environ.get("XNC_LIB", LIB_PATH)
+    if not os.path.exists(path):
         raise RuntimeError(
-            f"libxnorb200.so not built ({LIB_PATH}); run `python -c \"import __graft_entry__ as g; "
+            f"libxnorb200.so not built ({path}); run `python -c \"import __graft_entry__ as g; "
             "g.build()\"` -- the B200 path has no CPU fallback")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
     LG, D, U64 = ctypes.c_long, ctypes.c_double, ctypes.c_uint64
     sig = {

@@ -1,4 +1,5 @@
-// K3 on the 5th-generation tensor cores: tcgen05.mma.kind::i8, accumulators in TMEM.
+// K3 on the 5th-generation tensor cores: tcgen05.mma.cta_group::2.kind::i8 on
+// CTA pairs, accumulators in TMEM.
 //
 // Exact-integer reformulation of the XNOR sum.  With d = 1 for a negative input
 // sign (0 for +1, for zero padding and for tail channels) and s_w = +-1 the
@@ -15,27 +16,43 @@
 // Implicit GEMM without an im2col buffer.  Per image the output is walked on an
 // "extended" grid of H' rows x IC = W + 2*pad columns (the padded input row
 // length; the last kw-1 columns of every row are discarded).  Output pixel e and
-// tap (ky, kx) then read padded input pixel e + ky*IC + kx: every tap of a
-// 128-row MMA tile is the SAME shared-memory tile shifted by whole 128-byte rows,
-// i.e. one K-major SWIZZLE_128B descriptor per tap and no data movement
-// (tools/microbench/umma_probe.cu: row-shifted descriptors with base_offset = 0
-// verified against a CPU GEMM on a B200, 0 mismatches for shifts 0-9).
+// tap (ky, kx) then read padded input pixel e + ky*IC + kx: every tap of an MMA
+// tile is the SAME shared-memory tile shifted by whole 128-byte rows, i.e. one
+// K-major SWIZZLE_128B descriptor per tap and no data movement.
 //
-// Persistent, warp-specialised pipeline (one CTA per SM, 640 threads):
-//   warp 0      B producer: cp.async.bulk of one (tap, K block) filter chunk,
-//               NB x 128 B, pre-swizzled in HBM by k_pack_weights_umma
-//   warp 1      MMA issuer (one thread): per tile and filter block,
-//               MH M=128 row blocks x 4 K=32 steps per chunk, accumulate in TMEM
-//   warp 2      A producer: one TMA tile load per 128-channel K block of the
-//               d-bytes written by K1 (xnc_pack_input_umma): R padded rows x IC
+// CTA pairs (cluster of 2, cta_group::2).  One MMA instruction computes M = 256
+// pixels (128 from each CTA's shared memory) x N = NP filters (NP/2 from each
+// CTA's shared memory), K = 32 channels, and leaves each CTA its own 128 pixel
+// rows x NP accumulator columns in TMEM.  Why pairs (tools/microbench,
+// profiles/umma_pattern_r1.jsonl):
+//   * the tensor core's instruction queue is only ~2-3 MMAs deep; with the
+//     128x128x32 MMAs of a one-CTA kernel every mbarrier wait in the issuing
+//     thread drained it (83 SM cycles per MMA instead of 64 with one wait per
+//     8 MMAs); with 256-column MMAs (128 cycles each) the same protocol runs at
+//     64.0, i.e. the full rate;
+//   * one CTA cannot issue 128x256 MMAs at 128-pixel tiles without doubling the
+//     filter-chunk traffic per output; in a pair each CTA still streams only
+//     NP/2 filter rows per chunk.
+// Both CTAs must present their A tile at the same shared-memory offset (one
+// descriptor serves both).  A CTA's tile starts at an arbitrary column of a
+// padded row, so each CTA's TMA writes the whole rows to `P0 - (m0 % IC)*128`:
+// SWIZZLE_128B TMA writes are placed by absolute address, so a 128-B aligned
+// destination is exact (tools/microbench/tma_align.cu).
+//
+// Persistent, warp-specialised pipeline (one CTA per SM, 640 threads per CTA):
+//   warp 0      B producer (both CTAs): TMA of this CTA's NP/2 filter rows of one
+//               (tap, K block) chunk, completing on the leader's b_full
+//   warp 1      MMA issuer (leader CTA, one thread): per unit, MH x 4 K=32
+//               MMAs per chunk; tcgen05.commit multicast to both CTAs
+//   warp 2      A producer (both CTAs): one TMA per 128-channel K block of the
+//               d-bytes written by K1 (xnc_pack_input_umma), R padded rows x IC
 //               columns x 128 B, zero fill outside the image
-//   warps 4-19  epilogue: TMEM -> registers -> S_w - 2*acc -> (f32 * K) * alpha
-//               -> y, four warps per TMEM lane quadrant
-// Work unit = (tile of 128*MH extended pixels of one image, filter block of NB).
-// TMEM holds two accumulators (MH x NB columns each): the epilogue of one unit
-// overlaps the MMAs of the next.  A K-block plane is released as soon as
-// the tile's last filter block has consumed it, so the next tile's TMA load
-// overlaps the remaining MMAs.
+//   warp 3      TMEM allocator (both CTAs, cta_group::2)
+//   warps 4-19  epilogue (both CTAs): TMEM -> registers -> S_w - 2*acc ->
+//               (f32 * K) * alpha -> y, four warps per TMEM lane quadrant
+// Work unit = (pair tile of 2*MH*128 extended pixels of one image, filter block
+// of NP).  TMEM holds two accumulators (MH x NP columns each): the epilogue of
+// one unit overlaps the MMAs of the next.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -46,11 +63,25 @@
 
 namespace xnc {
 
-constexpr int kU2Threads = 640;
-constexpr int kU2Stages = 6;     // B pipeline depth
-constexpr int kU2MaxKB = 4;      // K blocks (128 channels each) kept resident: C <= 512
-constexpr int kU2EpiWarp0 = 4;   // first epilogue warp
-constexpr int kU2EpiWarps = 16;
+constexpr int kPThreads = 640;
+#ifndef XNC_PSTAGES
+#define XNC_PSTAGES 6
+#endif
+#ifndef XNC_PCPS
+#define XNC_PCPS 1
+#endif
+constexpr int kPStages = XNC_PSTAGES;  // B pipeline depth (stages)
+constexpr int kPCPS = XNC_PCPS;        // (tap, K block) chunks per B stage: one wait + one commit each
+constexpr int kPMaxKB = 4;       // K blocks (128 channels each) kept resident: C <= 512
+constexpr int kPEpiWarp0 = 4;    // first epilogue warp
+constexpr int kPEpiWarps = 16;
+constexpr int kProfSlots = 16;
+
+// Profiling only (XNC_UMMA_DEBUG bit 7): per-CTA cycle counters, read back with
+// xnc_umma_profile().  Slots: 0 issuer total, 1 issuer wait t_empty, 2 issuer
+// wait a_full, 3 issuer wait b_full, 4 MMAs issued, 5 epilogue (warp 4) total,
+// 6 epilogue wait t_full, 7 B producer wait b_empty, 8 A producer wait a_empty.
+__device__ unsigned long long g_umma_prof[1024][kProfSlots];
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -62,6 +93,23 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t addr) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -80,8 +128,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+__device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, bool prof,
+                                               unsigned long long& acc) {
+  const unsigned long long t0 = prof ? clock64() : 0ull;
+  mbar_wait(bar, parity);
+  if (prof) acc += clock64() - t0;
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -89,20 +140,33 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// arrive on an mbarrier given by its shared::cluster address (possibly the peer's).
+// Default (.release.cta) semantics: a .cluster release would compile to
+// MEMBAR.ALL.GPU + CCTL.IVALL, stalling each epilogue warp until its streaming
+// stores drain (ncu: 10% 'membar' stalls).  Only the TMEM reads must be ordered
+// before the arrive, and tcgen05.fence::before_thread_sync does that.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// TMA tile loads into this CTA's shared memory, completing on the mbarrier at a
+// shared::cluster address (the leader CTA's): .cta_group::2 lets the barrier
+// live in the peer CTA.
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t bar_cluster) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            int c3, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 int c3, uint32_t bar_cluster) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar))
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cluster)
       : "memory");
 }
 
@@ -113,18 +177,22 @@ __device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, 
                : "memory");
 }
 
-__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                        uint32_t accumulate) {
+__device__ __forceinline__ void umma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_addr(bar))
-               : "memory");
+// arrive (once MMAs issued so far complete) on the mbarrier at this offset in
+// both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_addr(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]) {
@@ -137,181 +205,224 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]
       : "r"(addr));
 }
 
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
-      " [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-        "=r"(v[15])
-      : "r"(addr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+// streaming (evict-first) store, predicated without a branch
+__device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}" ::"l"(p),
+               "f"(v), "r"((int)pred)
+               : "memory");
 }
 
-struct UmmaGeom {
-  int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NB, R, plane_bytes, n_mt, n_nb, tiles, taps, MH;
-  uint32_t box_bytes, tmem_cols;
-  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once,
-             // bit 2 = load the input rows once, bit 3 = no B barrier protocol after the
-             // first stages, bit 4 = no tcgen05 fence after B waits
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+struct PairGeom {
+  int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NP, MH, R, taps;
+  int plane_bytes;   // one K-block plane (1024-aligned)
+  int p0_off;        // offset of the tile's first pixel row inside a plane (1024-aligned)
+  int n_mt;          // pair tiles per image
+  int n_nb;          // filter blocks
+  int tiles;         // N * n_mt
+  uint32_t a_box_bytes, b_half_bytes, tmem_cols;
+  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 2 = load the
+             // input rows once, bit 5 = epilogue does only the TMEM
+             // handshake, bit 6 = chunk issue timeline of pair 0 (profile rows 512+),
+             // bit 7 = cycle counters (xnc_umma_profile)
 };
 
-// MH = M=128 row blocks per tile (tile = 128*MH extended pixels); the two TMEM
-// accumulators hold MH x NB columns each (MH * NB <= 256).
+// MH = M=128 row blocks per CTA (pair tile = 2*MH*128 extended pixels); the two
+// TMEM accumulators hold MH x NP columns each (MH * NP <= 256).
 template <int MH>
-__global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
-    const __grid_constant__ CUtensorMap a_map, const uint8_t* __restrict__ wq,
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv_umma_pair(
+    const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
-    const UmmaGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out) {
+    const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-  uint8_t* a_s = smem;                                   // KBn planes of R*IC rows x 128 B
-  uint8_t* b_s = a_s + (size_t)g.KBn * g.plane_bytes;    // stages x NB rows x 128 B
-  const uint32_t b_bytes = (uint32_t)g.NB * 128u;
-  __shared__ __align__(8) uint64_t b_full[kU2Stages], b_empty[kU2Stages];
-  __shared__ __align__(8) uint64_t a_full[kU2MaxKB], a_empty[kU2MaxKB];
+  uint8_t* a_s = smem;                                   // KBn planes
+  uint8_t* b_s = a_s + (size_t)g.KBn * g.plane_bytes;    // stages x NP/2 rows x 128 B
+  __shared__ __align__(8) uint64_t b_full[kPStages], b_empty[kPStages];
+  __shared__ __align__(8) uint64_t a_full[kPMaxKB], a_empty[kPMaxKB];
   __shared__ __align__(8) uint64_t t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   if (tid == 0) {
-    for (int s = 0; s < kU2Stages; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
-    for (int k = 0; k < kU2MaxKB; ++k) { mbar_init(&a_full[k], 1); mbar_init(&a_empty[k], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], kU2EpiWarps); }
+    for (int s = 0; s < kPStages; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
+    for (int k = 0; k < kPMaxKB; ++k) { mbar_init(&a_full[k], 1); mbar_init(&a_empty[k], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], 2 * kPEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2 && lane == 0)
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a_map)) : "memory");
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+  if ((warp == 0 || warp == 2) && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(warp == 0 ? &b_map : &a_map))
+                 : "memory");
+  }
+  if (warp == 3) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(&tmem_base_s)), "r"(g.tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_s;
+  const int tile_px = 2 * MH * 128;
 
   if (warp == 0) {
-    // ================= B producer
+    // ================= B producer: this CTA's NP/2 filter rows of every chunk,
+    // kPCPS chunks per stage (one full barrier per stage)
     if (lane == 0) {
+      const bool prof = g.debug & 128;
+      unsigned long long w_be = 0;
+      const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
+      const int my_tiles = (g.tiles - cluster + n_clusters - 1) / n_clusters;
+      const uint32_t total = (uint32_t)my_tiles * g.n_nb * g.KBn * g.taps;
       uint32_t step = 0;
-      for (int t = blockIdx.x; t < g.tiles; t += gridDim.x)
+      for (int t = cluster; t < g.tiles; t += n_clusters)
         for (int nb = 0; nb < g.n_nb; ++nb)
           for (int kb = 0; kb < g.KBn; ++kb)
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
-              const uint32_t st = step % kU2Stages;
-              if (step >= kU2Stages) mbar_wait(&b_empty[st], ((step / kU2Stages) - 1) & 1);
-              if ((g.debug & 8) && step >= kU2Stages) continue;  // profiling: no B protocol at all
-              if ((g.debug & 2) && step >= kU2Stages) {
-                mbar_arrive(&b_full[st]);  // profiling: reuse resident chunks, no traffic
-                continue;
+              const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
+              if (j == 0) {
+                if (sidx >= kPStages) mbar_wait_prof(&b_empty[st], ((sidx / kPStages) - 1) & 1, prof, w_be);
+                const uint32_t n_in = min((uint32_t)kPCPS, total - step);
+                if (leader) mbar_expect_tx(&b_full[st], n_in * 2 * g.b_half_bytes);
               }
-              mbar_expect_tx(&b_full[st], b_bytes);
-              const size_t chunk = ((size_t)nb * g.taps + tap) * g.KBn + kb;
-              bulk_load(b_s + st * b_bytes, wq + chunk * b_bytes, b_bytes, &b_full[st]);
+              const int row = ((nb * g.taps + tap) * g.KBn + kb) * g.NP + (int)rank * (g.NP / 2);
+              tma_load_2d_pair(b_s + (st * kPCPS + j) * g.b_half_bytes, &b_map, 0, row, full0 + st * 8);
             }
+      if (prof) g_umma_prof[blockIdx.x][7] = w_be;
     }
   } else if (warp == 2) {
-    // ================= A producer (TMA)
+    // ================= A producer: this CTA's pixel rows of every K block
     if (lane == 0) {
+      const bool prof = g.debug & 128;
+      unsigned long long w_ae = 0;
+      const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, ++it) {
-        const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * (128 * MH);
-        const int r0 = m0 / g.IC;
+      for (int t = cluster; t < g.tiles; t += n_clusters, ++it) {
+        const int n = t / g.n_mt;
+        const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
+        const int r0 = m0 / g.IC, c0 = m0 - r0 * g.IC;
         for (int kb = 0; kb < g.KBn; ++kb) {
-          if (it >= 1) mbar_wait(&a_empty[kb], (it - 1) & 1);
+          if (it >= 1) mbar_wait_prof(&a_empty[kb], (it - 1) & 1, prof, w_ae);
           if ((g.debug & 4) && it >= 1) {  // profiling: keep the first tile's rows, no traffic
-            mbar_arrive(&a_full[kb]);
+            if (leader) mbar_arrive_cluster(smem_addr(&a_full[kb]));
             continue;
           }
-          mbar_expect_tx(&a_full[kb], g.box_bytes);
-          tma_load_4d(a_s + (size_t)kb * g.plane_bytes, &a_map, kb * 128, -g.pad, r0 - g.pad, n, &a_full[kb]);
+          if (leader) mbar_expect_tx(&a_full[kb], 2 * g.a_box_bytes);
+          // whole padded rows r0.. so that pixel m0 lands at plane + p0_off
+          uint8_t* dst = a_s + (size_t)kb * g.plane_bytes + g.p0_off - c0 * 128;
+          tma_load_4d_pair(dst, &a_map, kb * 128, -g.pad, r0 - g.pad, n, full0 + kb * 8);
         }
-        // warm L2 with the next tile's rows: its loads are issued while this
-        // tile's last MMAs run, and must land before the tensor core drains
-        const int tn = t + gridDim.x;
+        // warm L2 with the next tile's rows while this tile's MMAs run
+        const int tn = t + n_clusters;
         if (tn < g.tiles) {
-          const int nn = tn / g.n_mt, rn = ((tn - nn * g.n_mt) * (128 * MH)) / g.IC;
+          const int nn = tn / g.n_mt;
+          const int rn = ((tn - nn * g.n_mt) * tile_px + (int)rank * (MH * 128)) / g.IC;
           for (int kb = 0; kb < g.KBn; ++kb) tma_prefetch_4d(&a_map, kb * 128, -g.pad, rn - g.pad, nn);
         }
       }
+      if (prof) g_umma_prof[blockIdx.x][8] = w_ae;
     }
   } else if (warp == 1) {
-    // ================= MMA issuer
+    // ================= MMA issuer (leader CTA only)
     // Descriptors are built once and advanced by adding (byte offset >> 4) to
-    // the start-address field (addresses < 256 KB never carry out of it), so
-    // each MMA costs one 64-bit add: the issue loop must stay well ahead of
-    // the tensor core (a 128x128x32 i8 MMA retires in ~67 cycles).
-    if (lane == 0) {
-      const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(g.NB >> 3) << 17) |
-                             ((uint32_t)(128 >> 4) << 24);
-      const uint64_t a_desc0 = umma_desc_sw128(smem_addr(a_s));
+    // the start-address field (addresses < 256 KB never carry out of it).
+    if (leader && lane == 0) {
+      const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(g.NP >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+      const uint64_t a_desc0 = umma_desc_sw128(smem_addr(a_s + g.p0_off));
       const uint64_t b_desc0 = umma_desc_sw128(smem_addr(b_s));
-      const uint32_t plane16 = (uint32_t)g.plane_bytes >> 4, b16 = b_bytes >> 4;
+      const uint32_t plane16 = (uint32_t)g.plane_bytes >> 4, b16 = g.b_half_bytes >> 4;
+      const bool prof = g.debug & 128;
+      const bool trace = (g.debug & 64) && blockIdx.x == 0;
+      const int my_tiles = (g.tiles - cluster + n_clusters - 1) / n_clusters;
+      const uint32_t total = (uint32_t)my_tiles * g.n_nb * g.KBn * g.taps;
+      unsigned long long w_te = 0, w_af = 0, w_bf = 0, n_mma = 0;
+      const unsigned long long t_start = clock64();
       uint32_t step = 0, item = 0, it = 0;
-      for (int t = blockIdx.x; t < g.tiles; t += gridDim.x, ++it) {
-        const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * (128 * MH);
-        const uint32_t tile16 = (uint32_t)(m0 - (m0 / g.IC) * g.IC) * 8u;  // off0 rows x 128 B / 16
+      for (int t = cluster; t < g.tiles; t += n_clusters, ++it) {
         for (int nb = 0; nb < g.n_nb; ++nb, ++item) {
           const uint32_t buf = item & 1;
           if (item >= 2) {
-            mbar_wait(&t_empty[buf], ((item >> 1) - 1) & 1);
+            mbar_wait_prof(&t_empty[buf], ((item >> 1) - 1) & 1, prof, w_te);
             asm volatile("tcgen05.fence::after_thread_sync;");
           }
-          const uint32_t d0 = tmem + buf * (MH * g.NB);
+          const uint32_t d0 = tmem + buf * (MH * g.NP);
           uint32_t acc = 0;
           for (int kb = 0; kb < g.KBn; ++kb) {
             if (nb == 0) {
-              mbar_wait(&a_full[kb], it & 1);
+              mbar_wait_prof(&a_full[kb], it & 1, prof, w_af);
               asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            const uint64_t a_kb = a_desc0 + kb * plane16 + tile16;
+            const uint64_t a_kb = a_desc0 + kb * plane16;
             for (int ky = 0; ky < g.kh; ++ky) {
               for (int kx = 0; kx < g.kw; ++kx, ++step) {
-                const uint32_t st = step % kU2Stages;
-                const bool b_sync = !(g.debug & 8) || step < kU2Stages;
-                if (b_sync) {
-                  mbar_wait(&b_full[st], (step / kU2Stages) & 1);
-                  if (!(g.debug & 16)) asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
+                const unsigned long long tw0 = trace ? clock64() : 0ull;
+                if (j == 0) {
+                  mbar_wait_prof(&b_full[st], (sidx / kPStages) & 1, prof, w_bf);
+                  asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                if (trace && step < 4096) {  // profiling: chunk issue timeline of CTA pair 0
+                  const unsigned long long tw1 = clock64();
+                  g_umma_prof[512 + step / 8][2 * (step % 8)] = tw0 - t_start;
+                  g_umma_prof[512 + step / 8][2 * (step % 8) + 1] = tw1 - tw0;
                 }
                 const uint64_t a_tap = a_kb + (uint32_t)(ky * g.IC + kx) * 8u;
-                const uint64_t b_st = b_desc0 + st * b16;
+                const uint64_t b_st = b_desc0 + (st * kPCPS + j) * b16;
 #pragma unroll
                 for (int s = 0; s < 4; ++s) {
 #pragma unroll
                   for (int h = 0; h < MH; ++h)
-                    umma_i8(d0 + h * g.NB, a_tap + h * 1024 + 2 * s, b_st + 2 * s, idesc, acc | (uint32_t)s);
+                    umma_i8_pair(d0 + h * g.NP, a_tap + h * 1024 + 2 * s, b_st + 2 * s, idesc,
+                                 acc | (uint32_t)s);
                 }
                 acc = 1;
-                if (b_sync) umma_commit(&b_empty[st]);
+                n_mma += 4 * MH;
+                if (j == kPCPS - 1 || step + 1 == total) umma_commit_pair(&b_empty[st]);
               }
             }
-            if (nb == g.n_nb - 1) umma_commit(&a_empty[kb]);
+            if (nb == g.n_nb - 1) umma_commit_pair(&a_empty[kb]);
           }
-          umma_commit(&t_full[buf]);
+          umma_commit_pair(&t_full[buf]);
         }
       }
+      if (prof) {
+        g_umma_prof[blockIdx.x][0] = clock64() - t_start;
+        g_umma_prof[blockIdx.x][1] = w_te;
+        g_umma_prof[blockIdx.x][2] = w_af;
+        g_umma_prof[blockIdx.x][3] = w_bf;
+        g_umma_prof[blockIdx.x][4] = n_mma;
+      }
     }
-  } else if (warp >= kU2EpiWarp0 && warp < kU2EpiWarp0 + kU2EpiWarps) {
-    // ================= epilogue
+  } else if (warp >= kPEpiWarp0 && warp < kPEpiWarp0 + kPEpiWarps) {
+    // ================= epilogue (both CTAs)
     // 16 warps: warp w reads TMEM lane quadrant (w & 3) and the 16-column chunks
     // cg, cg+4, ... (cg = (w-4) >> 2) of every accumulator row block.  Each
     // thread owns one extended pixel per row block; for a chunk it issues the
     // TMEM loads of all row blocks before one wait, then writes 16 filters x MH
     // pixels (for a fixed filter the 32 lanes store 32 consecutive pixels).
-    const int e_w = warp - kU2EpiWarp0;
-    const int quad = warp & 3;              // TMEM lane quadrant this warp may access
+    const int e_w = warp - kPEpiWarp0;
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int cg = e_w >> 2;
-    const int n_chunks = g.NB / 16;
+    const int n_chunks = g.NP / 16;
     const size_t plane_out = (size_t)g.oh * g.ow;
+    const uint32_t t_empty0 = map_to_rank(smem_addr(&t_empty[0]), 0);
     uint32_t item = 0;
+    const bool prof = (g.debug & 128) && warp == kPEpiWarp0 && lane == 0;
+    unsigned long long w_tf = 0;
+    const unsigned long long t_start = clock64();
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
                         ((reinterpret_cast<uintptr_t>(alpha) & 15) == 0);
-    for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
-      const int n = t / g.n_mt, m0 = (t - n * g.n_mt) * (128 * MH);
+    // 32-bit filter-plane stride for the hot path (host guarantees O*oh*ow < 2^31)
+    const int plane_out32 = g.oh * g.ow;
+    const bool fast = y != nullptr && acc_out == nullptr;
+    for (int t = cluster; t < g.tiles; t += n_clusters) {
+      const int n = t / g.n_mt;
+      const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);
       size_t pix[MH];
       bool ok[MH];
       float kv[MH];
@@ -325,15 +436,15 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
       }
       for (int nb = 0; nb < g.n_nb; ++nb, ++item) {
         const uint32_t buf = item & 1;
-        mbar_wait(&t_full[buf], (item >> 1) & 1);
+        mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        for (int ch = cg; ch < n_chunks; ch += 4) {
+        for (int ch = (g.debug & 32) ? n_chunks : cg; ch < n_chunks; ch += 4) {
           const int c = ch * 16;
-          const int obase = nb * g.NB + c;
+          const int obase = nb * g.NP + c;
           uint32_t v[MH][16];
 #pragma unroll
           for (int h = 0; h < MH; ++h)
-            tmem_ld16_async(tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NB) + h * g.NB + c, v[h]);
+            tmem_ld16_async(tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NP) + h * g.NP + c, v[h]);
           // per-filter constants for these 16 columns (uniform across lanes)
           int swv[16];
           float av[16];
@@ -355,6 +466,20 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
           }
           tmem_wait_ld();
           if (g.debug & 1) continue;
+          if (fast && obase + 16 <= g.O) {
+            // hot path: float output only, all 16 filters valid -- about six
+            // instructions per output (IADD3, I2F, 2 FMUL, IMAD.WIDE, predicated STG)
+#pragma unroll
+            for (int h = 0; h < MH; ++h) {
+              const float* yp = y + pix[h] + (size_t)obase * plane_out;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int accv = swv[j] - 2 * (int)v[h][j];
+                st_cs_pred(yp + j * plane_out32, __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]), ok[h]);
+              }
+            }
+            continue;
+          }
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             if (!ok[h]) continue;
@@ -372,35 +497,39 @@ __global__ void __launch_bounds__(kU2Threads, 1) k_conv_umma(
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&t_empty[buf]);
+        if (lane == 0) mbar_arrive_cluster(t_empty0 + buf * 8);
       }
+    }
+    if (prof) {
+      g_umma_prof[blockIdx.x][5] = clock64() - t_start;
+      g_umma_prof[blockIdx.x][6] = w_tf;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0) {
-    __syncwarp();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
+  cluster_sync();
+  if (warp == 3) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
   }
 }
 
 // ---------------------------------------------------------------- weights
-// wq[nb][tap][kb][row = filter within block][128 B], s8 signs (+1/-1, 0 for tail
-// channels and filters >= O); each (tap, kb) chunk pre-swizzled for a 1024-aligned
-// smem destination (16-byte chunk q of row r stored at q ^ (r & 7)).
+// wq[nb][tap][kb][row = filter within a block of NP][128 B], s8 signs (+1/-1,
+// 0 for tail channels and filters >= O), plain rows: the B TMA applies the
+// 128-byte swizzle.  CTA r of a pair loads rows [r*NP/2, (r+1)*NP/2) of a chunk.
 template <typename T>
-__global__ void k_pack_weights_umma(const T* __restrict__ w, int O, int C, int kh, int kw, int NB,
+__global__ void k_pack_weights_umma(const T* __restrict__ w, int O, int C, int kh, int kw, int NP,
                                     int KBn, uint8_t* __restrict__ wq) {
-  const long total = (long)cdiv(O, NB) * kh * kw * KBn * NB * 8;
+  const long total = (long)cdiv(O, NP) * kh * kw * KBn * NP * 8;
   long it = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (it >= total) return;
   const int q = (int)(it & 7);
   long rest = it >> 3;
-  const int row = (int)(rest % NB); rest /= NB;
+  const int row = (int)(rest % NP); rest /= NP;
   const int kb = (int)(rest % KBn); rest /= KBn;
   const int tap = (int)(rest % (kh * kw));
   const int nb = (int)(rest / (kh * kw));
-  const int o = nb * NB + row;
+  const int o = nb * NP + row;
   uint32_t vals[4] = {0u, 0u, 0u, 0u};
   if (o < O) {
     for (int b = 0; b < 16; ++b) {
@@ -412,8 +541,8 @@ __global__ void k_pack_weights_umma(const T* __restrict__ w, int O, int C, int k
       }
     }
   }
-  uint8_t* chunk = wq + ((((long)nb * kh * kw + tap) * KBn + kb) * NB + row) * 128;
-  *reinterpret_cast<uint4*>(chunk + ((q ^ (row & 7)) << 4)) = make_uint4(vals[0], vals[1], vals[2], vals[3]);
+  uint8_t* rowp = wq + ((((long)nb * kh * kw + tap) * KBn + kb) * NP + row) * 128;
+  *reinterpret_cast<uint4*>(rowp + (q << 4)) = make_uint4(vals[0], vals[1], vals[2], vals[3]);
 }
 
 template <typename T>
@@ -425,84 +554,74 @@ __global__ void k_weight_sign_sums(const T* __restrict__ w, int O, int C, int kk
   sw[o] = s;
 }
 
-// Tile shape.  NB (filters per block) must not depend on the image shape, since
-// the weights are packed before any input is seen; MH (M=128 row blocks per tile)
-// is picked per shape.  2 accumulators x MH x NB columns must fit 512 TMEM cols.
-// XNC_UMMA_TILE="MH,NB" overrides both (tuning knob, read once per process).
-struct UmmaTilePref {
-  int mh = 2, nb = 128;
-  UmmaTilePref() {
-    if (const char* e = getenv("XNC_UMMA_TILE")) {
-      int a = 0, b = 0;
-      if (sscanf(e, "%d,%d", &a, &b) == 2 && (a == 1 || a == 2 || a == 4) && b >= 32 && b % 32 == 0 &&
-          2 * a * b <= 512) {
-        mh = a;
-        nb = b;
-      }
-    }
-  }
-};
-static const UmmaTilePref& tile_pref() {
-  static UmmaTilePref p;
-  return p;
-}
-static int umma_nb(int O) { return O >= tile_pref().nb ? tile_pref().nb : round_up(O, 32); }
+// Filters per pair block.  NP must not depend on the image shape (the weights
+// are packed before any input is seen): 256-column MMAs whenever the filter
+// count is a multiple of 256, else 128 (zero filters pad the last block).
+static int pair_np(int O) { return O % 256 == 0 ? 256 : 128; }
 
 size_t umma_weight_bytes(int O, int C, int kh, int kw) {
-  const int NB = umma_nb(O);
-  return (size_t)cdiv(O, NB) * NB * kh * kw * cdiv(C, 128) * 128;
+  const int NP = pair_np(O);
+  return (size_t)cdiv(O, NP) * NP * kh * kw * cdiv(C, 128) * 128;
 }
 
 int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw, uint8_t* wq,
                              int32_t* sw, cudaStream_t s) {
-  const int NB = umma_nb(O), KBn = cdiv(C, 128);
-  const long total = (long)cdiv(O, NB) * kh * kw * KBn * NB * 8;
+  const int NP = pair_np(O), KBn = cdiv(C, 128);
+  const long total = (long)cdiv(O, NP) * kh * kw * KBn * NP * 8;
   const unsigned blocks = (unsigned)cdivl(total, 256);
   if (dtype == XNC_DTYPE_F64) {
-    k_pack_weights_umma<double><<<blocks, 256, 0, s>>>((const double*)w, O, C, kh, kw, NB, KBn, wq);
+    k_pack_weights_umma<double><<<blocks, 256, 0, s>>>((const double*)w, O, C, kh, kw, NP, KBn, wq);
     k_weight_sign_sums<double><<<cdiv(O, 128), 128, 0, s>>>((const double*)w, O, C, kh * kw, sw);
   } else {
-    k_pack_weights_umma<float><<<blocks, 256, 0, s>>>((const float*)w, O, C, kh, kw, NB, KBn, wq);
+    k_pack_weights_umma<float><<<blocks, 256, 0, s>>>((const float*)w, O, C, kh, kw, NP, KBn, wq);
     k_weight_sign_sums<float><<<cdiv(O, 128), 128, 0, s>>>((const float*)w, O, C, kh * kw, sw);
   }
   return launch_status();
 }
 
-static bool umma_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int pad, int MH, UmmaGeom& g,
+static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int pad, int MH, PairGeom& g,
                          size_t& smem) {
   g.C = C; g.H = H; g.W = W; g.O = O; g.kh = kh; g.kw = kw; g.pad = pad; g.MH = MH;
   g.oh = H + 2 * pad - kh + 1; g.ow = W + 2 * pad - kw + 1;
   g.IC = W + 2 * pad;
   g.KBn = cdiv(C, 128);
-  g.NB = umma_nb(O);
+  g.NP = pair_np(O);
   g.taps = kh * kw;
-  const int MT = 128 * MH;
-  // padded input rows a tile touches: pixel indices off0 .. off0+MT-1 + (kh-1)*IC + kw-1
-  g.R = (g.IC - 1 + MT - 1 + kw - 1) / g.IC + kh;
-  g.box_bytes = (uint32_t)g.R * g.IC * 128u;
-  g.plane_bytes = round_up(g.R * g.IC * 128, 1024);
-  g.n_mt = cdiv(g.oh * g.IC, MT);
-  g.n_nb = cdiv(O, g.NB);
+  const int MT = 128 * MH;  // pixels per CTA tile
+  // pixels a CTA tile reads: m0 .. m0 + MT-1 + (kh-1)*IC + kw-1; rows loaded from
+  // row(m0), whose first pixel may be up to IC-1 columns before m0
+  const int span = MT + (kh - 1) * g.IC + (kw - 1);
+  g.R = (g.IC - 1 + span + g.IC - 1) / g.IC;
+  g.a_box_bytes = (uint32_t)g.R * g.IC * 128u;
+  g.p0_off = round_up((g.IC - 1) * 128, 1024);
+  g.plane_bytes = round_up(g.p0_off + g.R * g.IC * 128, 1024);
+  g.n_mt = cdiv(g.oh * g.IC, 2 * MT);
+  g.n_nb = cdiv(O, g.NP);
   g.tiles = N * g.n_mt;
-  const int cols = 2 * MH * g.NB;  // two accumulators x MH row blocks
+  g.b_half_bytes = (uint32_t)(g.NP / 2) * 128u;
+  const int cols = 2 * MH * g.NP;  // two accumulators x MH row blocks
   g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
-  smem = (size_t)g.KBn * g.plane_bytes + (size_t)kU2Stages * g.NB * 128 + 1024;
-  return cols <= 512 && g.KBn <= kU2MaxKB && g.IC <= 256 && g.R <= 256 && smem <= 225 * 1024 &&
-         (long)N * g.n_mt < 0x7fffffffL;
+  smem = (size_t)g.KBn * g.plane_bytes + (size_t)kPStages * kPCPS * g.b_half_bytes + 1024;
+  return cols <= 512 && g.KBn <= kPMaxKB && g.IC <= 256 && g.R <= 256 && smem <= 225 * 1024 &&
+         (long)N * g.n_mt < 0x7fffffffL && (long)g.n_nb * g.NP * g.oh * g.ow < 0x7fffffffL;
 }
 
-// Preferred MH first, then smaller tiles if the input rows do not fit shared memory.
-static bool umma_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, UmmaGeom& g,
-                      size_t& smem) {
-  for (int mh = tile_pref().mh; mh >= 1; mh /= 2)
-    if (umma_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem)) return true;
+// MH = 2 row blocks per CTA for 128-filter blocks (eight 128-cycle-equivalent
+// MMAs per chunk), 1 for 256-filter blocks; fall back to MH = 1 when the rows do
+// not fit shared memory.  XNC_UMMA_MH overrides (tuning knob).
+static bool pair_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, PairGeom& g, size_t& smem) {
+  static const int mh_env = getenv("XNC_UMMA_MH") ? atoi(getenv("XNC_UMMA_MH")) : 0;
+  int mh = pair_np(O) == 256 ? 1 : 2;
+  if (mh_env == 1 || (mh_env == 2 && pair_np(O) == 128)) mh = mh_env;
+  for (; mh >= 1; mh /= 2)
+    if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem)) return true;
   return false;
 }
 
 bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
-  UmmaGeom g;
+  PairGeom g;
   size_t smem;
-  return umma_plan(N, C, H, W, O, kh, kw, pad, g, smem);
+  return pair_plan(N, C, H, W, O, kh, kw, pad, g, smem);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -517,34 +636,45 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// Profiling counters (XNC_UMMA_DEBUG bit 7): none in this kernel yet.
-__device__ unsigned long long g_umma_prof[1024][16];
-
 int umma_profile_read(unsigned long long* host, int n_ctas) {
   if (n_ctas > 1024) n_ctas = 1024;
-  cudaError_t e = cudaMemcpyFromSymbol(host, g_umma_prof, sizeof(unsigned long long) * 16 * n_ctas);
+  cudaError_t e = cudaMemcpyFromSymbol(host, g_umma_prof, sizeof(unsigned long long) * kProfSlots * n_ctas);
   return e == cudaSuccess ? 0 : XNC_ECUDA_BASE + (int)e;
 }
 
 int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s) {
-  UmmaGeom g;
+  PairGeom g;
   size_t smem;
-  if (!umma_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
+  if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
   auto encode = tensor_map_encoder();
   if (!encode) return XNC_ENOTSUP;
-  // d-bytes [N][H][W][Cpad] u8; TMA box = 128 channels x IC columns x R rows x 1 image
+  // A: d-bytes [N][H][W][Cpad] u8; box = 128 channels x IC columns x R rows x 1 image
   const int Cpad = g.KBn * 128;
-  CUtensorMap map;
-  cuuint64_t dims[4] = {(cuuint64_t)Cpad, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
-  cuuint64_t strides[3] = {(cuuint64_t)Cpad, (cuuint64_t)W * Cpad, (cuuint64_t)H * W * Cpad};
-  cuuint32_t box[4] = {128u, (cuuint32_t)g.IC, (cuuint32_t)g.R, 1u};
-  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
-  CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(dbytes), dims, strides,
-                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return XNC_ENOTSUP;
+  CUtensorMap a_map, b_map;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)Cpad, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)Cpad, (cuuint64_t)W * Cpad, (cuuint64_t)H * W * Cpad};
+    cuuint32_t box[4] = {128u, (cuuint32_t)g.IC, (cuuint32_t)g.R, 1u};
+    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    CUresult cr = encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(dbytes), dims, strides,
+                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return XNC_ENOTSUP;
+  }
+  // B: weight rows [n_nb * taps * KBn * NP][128 B]; box = NP/2 rows
+  {
+    const cuuint64_t rows = (cuuint64_t)g.n_nb * g.taps * g.KBn * g.NP;
+    cuuint64_t dims[2] = {128u, rows};
+    cuuint64_t strides[1] = {128u};
+    cuuint32_t box[2] = {128u, (cuuint32_t)(g.NP / 2)};
+    cuuint32_t estr[2] = {1u, 1u};
+    CUresult cr = encode(&b_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(wq), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return XNC_ENOTSUP;
+  }
   {
     static const int dbg = getenv("XNC_UMMA_DEBUG") ? atoi(getenv("XNC_UMMA_DEBUG")) : 0;
     g.debug = dbg;
@@ -552,16 +682,16 @@ int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = g.tiles < sms ? g.tiles : sms;
-  static size_t attr_smem[3] = {0, 0, 0};  // one-time (per size increase) shared-memory opt-in
-  auto kern = g.MH == 4 ? k_conv_umma<4> : g.MH == 2 ? k_conv_umma<2> : k_conv_umma<1>;
-  size_t& attr = attr_smem[g.MH == 4 ? 2 : g.MH == 2 ? 1 : 0];
+  const int pairs = g.tiles < sms / 2 ? g.tiles : sms / 2;
+  static size_t attr_smem[2] = {0, 0};  // one-time (per size increase) shared-memory opt-in
+  auto kern = g.MH == 2 ? k_conv_umma_pair<2> : k_conv_umma_pair<1>;
+  size_t& attr = attr_smem[g.MH == 2 ? 1 : 0];
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
     attr = smem;
   }
-  kern<<<grid, kU2Threads, smem, s>>>(map, wq, sw, K, alpha, g, y, acc);
+  kern<<<2 * pairs, kPThreads, smem, s>>>(a_map, b_map, sw, K, alpha, g, y, acc);
   return launch_status();
 }
 

@@ -53,6 +53,20 @@ def child(cfg: str, reps: int) -> None:
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
     prof = None
+    if int(os.environ.get("XNC_UMMA_DEBUG", "0")) & 64:
+        import ctypes
+        import numpy as np
+        from paper_2007_14178_b200._lib import lib
+        buf = np.zeros((1024, 16), dtype=np.uint64)
+        lib().xnc_umma_profile(buf.ctypes.data_as(ctypes.c_void_p), 1024)
+        tr = buf[512:].reshape(-1, 2).astype(np.int64)
+        tr = tr[: int(np.argmax(tr[1:, 0] == 0)) + 1] if (tr[1:, 0] == 0).any() else tr
+        np.save(os.path.join(ROOT, "gpurun_out", f"trace_{cfg}.npy"), tr)
+        gaps = np.diff(tr[:, 0])
+        print(json.dumps({"trace_chunks": int(len(tr)), "gap_mean": float(gaps.mean()),
+                          "gap_p50": float(np.median(gaps)), "gap_p90": float(np.percentile(gaps, 90)),
+                          "gap_max": float(gaps.max()), "wait_mean": float(tr[:, 1].mean()),
+                          "wait_p90": float(np.percentile(tr[:, 1], 90))}), flush=True)
     if int(os.environ.get("XNC_UMMA_DEBUG", "0")) & 128:
         import ctypes
         import numpy as np
@@ -62,9 +76,12 @@ def child(cfg: str, reps: int) -> None:
         tot = buf[:, 0].astype(np.float64)
         names = ["issuer_total", "wait_t_empty", "wait_a_full", "wait_b_full", "mmas", "epi_total",
                  "epi_wait_t_full", "bprod_wait_b_empty", "aprod_wait_a_empty", "issue_blocks"]
+        lead = buf[0::2]  # CTA pairs: the MMA issuer runs on the even (leader) CTA
         prof = {n: round(float(buf[:, i].astype(np.float64).mean()), 0) for i, n in enumerate(names)}
+        for i in (0, 1, 2, 3, 4):
+            prof[names[i]] = round(float(lead[:, i].astype(np.float64).mean()), 0)
         prof["issuer_total_max"] = float(tot.max())
-        prof["cycles_per_mma"] = round(float((tot / np.maximum(buf[:, 4], 1)).mean()), 2)
+        prof["cycles_per_mma"] = round(float((lead[:, 0] / np.maximum(lead[:, 4], 1)).mean()), 2)
     macs = N * O * (H + 2 * pad - k + 1) * (W + 2 * pad - k + 1) * C * k * k
     print(json.dumps({"cfg": cfg, "debug": os.environ.get("XNC_UMMA_DEBUG", "0"),
                       "tile": os.environ.get("XNC_UMMA_TILE", "default"), "ms": round(ms, 4),
