@@ -228,17 +228,14 @@ def run_ours(args, cfg_name):
     oh, ow = ops.out_dims(H, W, k, k, pad)
     y = torch.empty((N, Oc, oh, ow), dtype=torch.float32, device=dev)
     kernel = layer.kernel_for(x.shape)  # "auto" resolves per shape
-    if kernel == "umma":  # the tcgen05 operand: d-bytes (K1 variant)
-        bits = torch.empty((N, H, W, ops.dbytes_channels(C)), dtype=torch.uint8, device=dev)
-    else:
-        bits = torch.empty((N, H, W, ops.words(C)), dtype=torch.int32, device=dev)
+    bits = torch.empty((N, H, W, ops.words(C)), dtype=torch.int32, device=dev)  # every conv kernel reads bits
     A = torch.empty((N, H, W), dtype=torch.float32, device=dev)
     K = torch.empty((N, oh, ow), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     from paper_2007_14178_b200._lib import check, lib
     L = lib()
     sptr = stream.cuda_stream
-    pack_fn = L.xnc_pack_input_umma if kernel == "umma" else L.xnc_pack_input
+    pack_fn = L.xnc_pack_input
 
     def conv_call():
         if kernel == "umma":
@@ -370,7 +367,7 @@ def run_ours(args, cfg_name):
                 traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
             except Exception:
                 traffic = None
-        packed = N * H * W * (ops.dbytes_channels(C) if kernel == "umma" else 4 * ops.words(C))
+        packed = N * H * W * 4 * ops.words(C)
         pack_bytes = 4.0 * N * C * H * W + packed + 4.0 * N * H * W
         result = {
             "metric": METRIC, "value": value, "unit": "Gbinop/s", "n_gpus": ws, "steps": args.steps,

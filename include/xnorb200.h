@@ -92,26 +92,24 @@ int xnc_xnor_conv_variant(int variant, const uint32_t* bits, const uint32_t* wbi
                           int W, int O, int kh, int kw, int pad, float* y,
                           int32_t* acc, void* stream);
 
-/* ---- K3 on the tcgen05 tensor cores (kind::i8, TMEM accumulators) ------------
+/* ---- K3 on the tcgen05 tensor cores (kind::i8, TMEM accumulators, CTA pairs) --
  * The XNOR sum as an exact u8 x s8 GEMM: acc = S_w[o] - 2 * sum_taps d * s_w, with
  * d = 1 for a negative input sign and s_w = +-1 the filter sign.
- * Input operand: d-bytes u8 [N][H][W][Cpad], Cpad = ceil(C/128)*128, written by
- * xnc_pack_input_umma (K1 variant: same single read of x, also writes A).
+ * Input: the same packed bits as xnc_xnor_conv (u32 [N][H][W][Cw], from
+ * xnc_pack_input); the kernel expands them to its byte operand in shared memory.
  * Weights in the tensor-core layout: wq (xnc_umma_weight_bytes bytes, s8 signs
- * in pre-swizzled 128-byte rows) and sw i32 [O] (sum of each filter's signs),
- * produced by xnc_pack_weights_umma from f32 (dtype 0) or f64 (dtype 1) weights.
+ * in 128-byte rows) and sw i32 [O] (sum of each filter's signs), produced by
+ * xnc_pack_weights_umma from f32 (dtype 0) or f64 (dtype 1) weights.
  * xnc_umma_supported() == 0 means the shape does not fit the kernel's shared
  * memory plan (then use xnc_xnor_conv). */
 size_t xnc_umma_weight_bytes(int O, int C, int kh, int kw);
 int xnc_umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 int xnc_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw,
                           uint8_t* wq, int32_t* sw, void* stream);
-int xnc_pack_input_umma(const float* x, int N, int C, int H, int W, uint8_t* dbytes,
-                        float* A, void* stream);
 /* Profiling only: per-CTA cycle counters of the last tcgen05 conv launched with
  * XNC_UMMA_DEBUG bit 7 set (16 u64 slots per CTA, host memory; blocking copy). */
 int xnc_umma_profile(unsigned long long* host_out, int n_ctas);
-int xnc_xnor_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw,
+int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
                        const float* K, const float* alpha, int N, int C, int H, int W,
                        int O, int kh, int kw, int pad, float* y, int32_t* acc, void* stream);
 

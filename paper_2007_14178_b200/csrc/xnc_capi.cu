@@ -105,19 +105,13 @@ int xnc_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw
   return launch_pack_weights_umma(w, dtype, O, C, kh, kw, wq, sw, as_stream(stream));
 }
 
-int xnc_pack_input_umma(const float* x, int N, int C, int H, int W, uint8_t* dbytes, float* A,
-                        void* stream) {
-  if (!x || !dbytes || N < 1 || C < 1 || H < 1 || W < 1) return XNC_EINVAL;
-  return launch_pack_input(x, N, C, H, W, nullptr, A, as_stream(stream), dbytes);
-}
-
-int xnc_xnor_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw, const float* K,
+int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                        const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                        float* y, int32_t* acc, void* stream) {
-  if (!dbytes || !wq || !sw || O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return XNC_EINVAL;
+  if (!bits || !wq || !sw || O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return XNC_EINVAL;
   if (!y && !acc) return XNC_EINVAL;
   if (y && (!K || !alpha)) return XNC_EINVAL;
-  return launch_conv_umma(dbytes, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, acc,
+  return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, acc,
                           as_stream(stream));
 }
 

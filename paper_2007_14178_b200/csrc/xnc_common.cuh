@@ -33,7 +33,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Kernel launchers implemented in the per-kernel translation units.
 namespace xnc {
 int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
-                      cudaStream_t s, uint8_t* dbytes = nullptr);
+                      cudaStream_t s);
 int launch_pack_weights(const float* w, int O, int C, int kh, int kw, uint32_t* wbits,
                         float* alpha, double* alpha64, cudaStream_t s);
 int launch_pack_weights_f64(const double* w, int O, int C, int kh, int kw, uint32_t* wbits,
@@ -51,7 +51,7 @@ bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw, uint8_t* wq,
                              int32_t* sw, cudaStream_t s);
 int umma_profile_read(unsigned long long* host, int n_ctas);
-int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw, const float* K,
+int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s);
 }  // namespace xnc

@@ -10,8 +10,8 @@
 // result is bit-identical to the reference decode `k_area - 2*popc(diff)`
 // summed over channels (_kernels_cy.pyx:100-104); the alpha*K epilogue
 // (_kernels_cy.pyx:349) is applied from TMEM.  Zero-filled taps are d = 0 = the
-// +1 padding of zero_pad-then-binarize (reference.py:87): TMA's out-of-bounds
-// zero fill IS the reference padding rule.
+// +1 padding of zero_pad-then-binarize (reference.py:87): padding pixels are
+// written as d = 0.
 //
 // Implicit GEMM without an im2col buffer.  Per image the output is walked on an
 // "extended" grid of H' rows x IC = W + 2*pad columns (the padded input row
@@ -33,21 +33,24 @@
 //   * one CTA cannot issue 128x256 MMAs at 128-pixel tiles without doubling the
 //     filter-chunk traffic per output; in a pair each CTA still streams only
 //     NP/2 filter rows per chunk.
-// Both CTAs must present their A tile at the same shared-memory offset (one
-// descriptor serves both).  A CTA's tile starts at an arbitrary column of a
-// padded row, so each CTA's TMA writes the whole rows to `P0 - (m0 % IC)*128`:
-// SWIZZLE_128B TMA writes are placed by absolute address, so a 128-B aligned
-// destination is exact (tools/microbench/tma_align.cu).
+// The A operand comes from the packed sign bits K1 writes (u32 [N][H][W][Cw],
+// 25.7 MB at C3, L2-resident after K1): two producer warps per CTA expand each
+// pixel's 128-channel block into 128 d-bytes in shared memory (d = NOT bit,
+// 0 for tail channels and for padding pixels), already in the SWIZZLE_128B
+// layout the MMA descriptor reads.  The plane holds exactly the extended
+// pixels m0 .. m0 + MT-1 + (kh-1)*IC + kw-1 of the CTA's tile, so both CTAs of
+// a pair present their tile at the same offset (one descriptor serves both).
+// This replaces an 8x larger d-byte tensor in HBM (205 MB written by K1 and
+// re-read by TMA at C3).
 //
 // Persistent, warp-specialised pipeline (one CTA per SM, 640 threads per CTA):
 //   warp 0      B producer (both CTAs): TMA of this CTA's NP/2 filter rows of one
 //               (tap, K block) chunk, completing on the leader's b_full
 //   warp 1      MMA issuer (leader CTA, one thread): per unit, MH x 4 K=32
 //               MMAs per chunk; tcgen05.commit multicast to both CTAs
-//   warp 2      A producer (both CTAs): one TMA per 128-channel K block of the
-//               d-bytes written by K1 (xnc_pack_input_umma), R padded rows x IC
-//               columns x 128 B, zero fill outside the image
-//   warp 3      TMEM allocator (both CTAs, cta_group::2)
+//   warps 2-3   A producers (both CTAs): per 128-channel K block, packed bits ->
+//               swizzled d-bytes in shared memory, arrive on the leader's a_full;
+//               warp 3 also allocates TMEM (cta_group::2)
 //   warps 4-19  epilogue (both CTAs): TMEM -> registers -> S_w - 2*acc ->
 //               (f32 * K) * alpha -> y, four warps per TMEM lane quadrant
 // Work unit = (pair tile of 2*MH*128 extended pixels of one image, filter block
@@ -72,7 +75,10 @@ constexpr int kPThreads = 640;
 #endif
 constexpr int kPStages = XNC_PSTAGES;  // B pipeline depth (stages)
 constexpr int kPCPS = XNC_PCPS;        // (tap, K block) chunks per B stage: one wait + one commit each
-constexpr int kPMaxKB = 4;       // K blocks (128 channels each) kept resident: C <= 512
+constexpr int kPMaxKB = 4;       // K blocks (128 channels each) of a tile resident: C <= 512
+constexpr int kPMaxA = 2 * kPMaxKB;  // A plane ring: two tiles' planes when they fit
+constexpr int kPAWarp0 = 2;      // first A-producer warp
+constexpr int kPAWarps = 2;
 constexpr int kPEpiWarp0 = 4;    // first epilogue warp
 constexpr int kPEpiWarps = 16;
 constexpr int kProfSlots = 16;
@@ -215,32 +221,43 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct PairGeom {
-  int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NP, MH, R, taps;
+  int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NP, MH, taps, Cw;
+  int P;             // extended pixel rows one K-block plane holds
   int plane_bytes;   // one K-block plane (1024-aligned)
-  int p0_off;        // offset of the tile's first pixel row inside a plane (1024-aligned)
+  int NA;            // A plane ring slots (KBn, or 2*KBn: next tile's planes built during this tile)
   int n_mt;          // pair tiles per image
   int n_nb;          // filter blocks
   int tiles;         // N * n_mt
-  uint32_t a_box_bytes, b_half_bytes, tmem_cols;
-  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 2 = load the
-             // input rows once, bit 5 = epilogue does only the TMEM
-             // handshake, bit 6 = chunk issue timeline of pair 0 (profile rows 512+),
-             // bit 7 = cycle counters (xnc_umma_profile)
+  uint32_t b_half_bytes, tmem_cols;
+  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 2 = build the
+             // input planes once, bit 5 = epilogue does only the TMEM handshake, bit 6 = chunk
+             // issue timeline of pair 0 (profile rows 512+), bit 7 = cycle counters (xnc_umma_profile)
 };
+
+// 16 sign bits -> 16 d-bytes (d = 1 where the bit is 0, i.e. x < 0), masked
+__device__ __forceinline__ uint4 d_bytes16(uint32_t bits16, uint32_t valid16) {
+  const uint32_t d = ~bits16 & valid16;
+  uint4 r;
+  r.x = ((d & 0xFu) * 0x00204081u) & 0x01010101u;
+  r.y = (((d >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
+  r.z = (((d >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
+  r.w = (((d >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
+  return r;
+}
 
 // MH = M=128 row blocks per CTA (pair tile = 2*MH*128 extended pixels); the two
 // TMEM accumulators hold MH x NP columns each (MH * NP <= 256).
 template <int MH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv_umma_pair(
-    const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap b_map,
+    const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
     const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
-  uint8_t* b_s = a_s + (size_t)g.KBn * g.plane_bytes;    // stages x NP/2 rows x 128 B
+  uint8_t* b_s = a_s + (size_t)g.NA * g.plane_bytes;     // stages x NP/2 rows x 128 B
   __shared__ __align__(8) uint64_t b_full[kPStages], b_empty[kPStages];
-  __shared__ __align__(8) uint64_t a_full[kPMaxKB], a_empty[kPMaxKB];
+  __shared__ __align__(8) uint64_t a_full[kPMaxA], a_empty[kPMaxA];
   __shared__ __align__(8) uint64_t t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base_s;
 
@@ -250,14 +267,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   if (tid == 0) {
     for (int s = 0; s < kPStages; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
-    for (int k = 0; k < kPMaxKB; ++k) { mbar_init(&a_full[k], 1); mbar_init(&a_empty[k], 1); }
+    for (int k = 0; k < kPMaxA; ++k) { mbar_init(&a_full[k], 2 * kPAWarps); mbar_init(&a_empty[k], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], 2 * kPEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if ((warp == 0 || warp == 2) && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(warp == 0 ? &b_map : &a_map))
-                 : "memory");
-  }
+  if (warp == 0 && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&b_map)) : "memory");
   if (warp == 3) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(&tmem_base_s)), "r"(g.tmem_cols));
@@ -294,38 +309,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
             }
       if (prof) g_umma_prof[blockIdx.x][7] = w_be;
     }
-  } else if (warp == 2) {
-    // ================= A producer: this CTA's pixel rows of every K block
-    if (lane == 0) {
-      const bool prof = g.debug & 128;
-      unsigned long long w_ae = 0;
-      const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
-      uint32_t it = 0;
-      for (int t = cluster; t < g.tiles; t += n_clusters, ++it) {
-        const int n = t / g.n_mt;
-        const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
-        const int r0 = m0 / g.IC, c0 = m0 - r0 * g.IC;
-        for (int kb = 0; kb < g.KBn; ++kb) {
-          if (it >= 1) mbar_wait_prof(&a_empty[kb], (it - 1) & 1, prof, w_ae);
-          if ((g.debug & 4) && it >= 1) {  // profiling: keep the first tile's rows, no traffic
-            if (leader) mbar_arrive_cluster(smem_addr(&a_full[kb]));
-            continue;
+  } else if (warp >= kPAWarp0 && warp < kPAWarp0 + kPAWarps) {
+    // ================= A producers: packed bits -> swizzled d-bytes, per K block
+    const int pt = tid - kPAWarp0 * 32, n_pt = kPAWarps * 32;
+    const bool prof = (g.debug & 128) && pt == 0;
+    unsigned long long w_ae = 0;
+    const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
+    const bool vec4 = (g.Cw & 3) == 0 && (reinterpret_cast<uintptr_t>(bits) & 15) == 0;
+    uint32_t it = 0;
+    for (int t = cluster; t < g.tiles; t += n_clusters, ++it) {
+      const int n = t / g.n_mt;
+      const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
+      const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
+      for (int kb = 0; kb < g.KBn; ++kb) {
+        const uint32_t use = it * g.KBn + kb, sl = use % g.NA;  // ring slot of this plane
+        if (use >= (uint32_t)g.NA) {
+          if (lane == 0) mbar_wait_prof(&a_empty[sl], ((use / g.NA) - 1) & 1, prof, w_ae);
+          __syncwarp();
+        }
+        if (!((g.debug & 4) && it >= 1)) {  // bit 2 (profiling): keep the first tile's planes
+          uint8_t* plane = a_s + (size_t)sl * g.plane_bytes;
+          // valid-channel masks of the block's four words
+          uint32_t vmask[4];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int rem = g.C - (kb * 128 + w * 32);
+            vmask[w] = rem >= 32 ? 0xFFFFFFFFu : rem <= 0 ? 0u : ((1u << rem) - 1u);
           }
-          if (leader) mbar_expect_tx(&a_full[kb], 2 * g.a_box_bytes);
-          // whole padded rows r0.. so that pixel m0 lands at plane + p0_off
-          uint8_t* dst = a_s + (size_t)kb * g.plane_bytes + g.p0_off - c0 * 128;
-          tma_load_4d_pair(dst, &a_map, kb * 128, -g.pad, r0 - g.pad, n, full0 + kb * 8);
+          for (int p = pt; p < g.P; p += n_pt) {
+            const int e = m0 + p;
+            const int pr = e / g.IC, pc = e - pr * g.IC;
+            const int r = pr - g.pad, c = pc - g.pad;
+            uint32_t wd[4] = {0u, 0u, 0u, 0u};
+            uint32_t vm[4] = {0u, 0u, 0u, 0u};  // padding pixel: all d = 0
+            if (r >= 0 && r < g.H && c >= 0 && c < g.W) {
+              const uint32_t* src = img + ((size_t)r * g.W + c) * g.Cw + kb * 4;
+              if (vec4) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4*>(src));
+                wd[0] = q.x; wd[1] = q.y; wd[2] = q.z; wd[3] = q.w;
+              } else {
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+                  if (kb * 4 + w < g.Cw) wd[w] = __ldg(src + w);
+              }
+#pragma unroll
+              for (int w = 0; w < 4; ++w) vm[w] = vmask[w];
+            }
+            uint8_t* row = plane + (size_t)p * 128;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t b16 = (wd[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu;
+              const uint32_t v16 = (vm[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu;
+              *reinterpret_cast<uint4*>(row + ((q ^ (p & 7)) << 4)) = d_bytes16(b16, v16);
+            }
+          }
+          // generic-proxy smem writes -> visible to the tensor core (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        // warm L2 with the next tile's rows while this tile's MMAs run
-        const int tn = t + n_clusters;
-        if (tn < g.tiles) {
-          const int nn = tn / g.n_mt;
-          const int rn = ((tn - nn * g.n_mt) * tile_px + (int)rank * (MH * 128)) / g.IC;
-          for (int kb = 0; kb < g.KBn; ++kb) tma_prefetch_4d(&a_map, kb * 128, -g.pad, rn - g.pad, nn);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(full0 + sl * 8);
       }
-      if (prof) g_umma_prof[blockIdx.x][8] = w_ae;
     }
+    if (prof) g_umma_prof[blockIdx.x][8] = w_ae;
   } else if (warp == 1) {
     // ================= MMA issuer (leader CTA only)
     // Descriptors are built once and advanced by adding (byte offset >> 4) to
@@ -333,7 +378,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     if (leader && lane == 0) {
       const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(g.NP >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
-      const uint64_t a_desc0 = umma_desc_sw128(smem_addr(a_s + g.p0_off));
+      const uint64_t a_desc0 = umma_desc_sw128(smem_addr(a_s));
       const uint64_t b_desc0 = umma_desc_sw128(smem_addr(b_s));
       const uint32_t plane16 = (uint32_t)g.plane_bytes >> 4, b16 = g.b_half_bytes >> 4;
       const bool prof = g.debug & 128;
@@ -353,11 +398,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
           const uint32_t d0 = tmem + buf * (MH * g.NP);
           uint32_t acc = 0;
           for (int kb = 0; kb < g.KBn; ++kb) {
+            const uint32_t use = it * g.KBn + kb, sl = use % g.NA;
             if (nb == 0) {
-              mbar_wait_prof(&a_full[kb], it & 1, prof, w_af);
+              mbar_wait_prof(&a_full[sl], (use / g.NA) & 1, prof, w_af);
               asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            const uint64_t a_kb = a_desc0 + kb * plane16;
+            const uint64_t a_kb = a_desc0 + sl * plane16;
             for (int ky = 0; ky < g.kh; ++ky) {
               for (int kx = 0; kx < g.kw; ++kx, ++step) {
                 const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
@@ -385,7 +431,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
                 if (j == kPCPS - 1 || step + 1 == total) umma_commit_pair(&b_empty[st]);
               }
             }
-            if (nb == g.n_nb - 1) umma_commit_pair(&a_empty[kb]);
+            if (nb == g.n_nb - 1) umma_commit_pair(&a_empty[sl]);
           }
           umma_commit_pair(&t_full[buf]);
         }
@@ -585,25 +631,25 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   g.oh = H + 2 * pad - kh + 1; g.ow = W + 2 * pad - kw + 1;
   g.IC = W + 2 * pad;
   g.KBn = cdiv(C, 128);
+  g.Cw = cdiv(C, 32);
   g.NP = pair_np(O);
   g.taps = kh * kw;
   const int MT = 128 * MH;  // pixels per CTA tile
-  // pixels a CTA tile reads: m0 .. m0 + MT-1 + (kh-1)*IC + kw-1; rows loaded from
-  // row(m0), whose first pixel may be up to IC-1 columns before m0
-  const int span = MT + (kh - 1) * g.IC + (kw - 1);
-  g.R = (g.IC - 1 + span + g.IC - 1) / g.IC;
-  g.a_box_bytes = (uint32_t)g.R * g.IC * 128u;
-  g.p0_off = round_up((g.IC - 1) * 128, 1024);
-  g.plane_bytes = round_up(g.p0_off + g.R * g.IC * 128, 1024);
+  // extended pixels a CTA tile reads: m0 .. m0 + MT-1 + (kh-1)*IC + kw-1
+  g.P = MT + (kh - 1) * g.IC + (kw - 1);
+  g.plane_bytes = round_up(g.P * 128, 1024);
   g.n_mt = cdiv(g.oh * g.IC, 2 * MT);
   g.n_nb = cdiv(O, g.NP);
   g.tiles = N * g.n_mt;
   g.b_half_bytes = (uint32_t)(g.NP / 2) * 128u;
   const int cols = 2 * MH * g.NP;  // two accumulators x MH row blocks
   g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
-  smem = (size_t)g.KBn * g.plane_bytes + (size_t)kPStages * kPCPS * g.b_half_bytes + 1024;
-  return cols <= 512 && g.KBn <= kPMaxKB && g.IC <= 256 && g.R <= 256 && smem <= 225 * 1024 &&
-         (long)N * g.n_mt < 0x7fffffffL && (long)g.n_nb * g.NP * g.oh * g.ow < 0x7fffffffL;
+  const size_t b_bytes = (size_t)kPStages * kPCPS * g.b_half_bytes + 1024;
+  g.NA = 2 * g.KBn;  // double-buffered planes when they fit, else one tile's worth
+  if ((size_t)g.NA * g.plane_bytes + b_bytes > 225 * 1024) g.NA = g.KBn;
+  smem = (size_t)g.NA * g.plane_bytes + b_bytes;
+  return cols <= 512 && g.KBn <= kPMaxKB && smem <= 225 * 1024 && (long)N * g.n_mt < 0x7fffffffL &&
+         (long)g.n_nb * g.NP * g.oh * g.ow < 0x7fffffffL;
 }
 
 // MH = 2 row blocks per CTA for 128-filter blocks (eight 128-cycle-equivalent
@@ -642,7 +688,7 @@ int umma_profile_read(unsigned long long* host, int n_ctas) {
   return e == cudaSuccess ? 0 : XNC_ECUDA_BASE + (int)e;
 }
 
-int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw, const float* K,
+int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s) {
   PairGeom g;
@@ -650,20 +696,8 @@ int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw
   if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
   auto encode = tensor_map_encoder();
   if (!encode) return XNC_ENOTSUP;
-  // A: d-bytes [N][H][W][Cpad] u8; box = 128 channels x IC columns x R rows x 1 image
-  const int Cpad = g.KBn * 128;
-  CUtensorMap a_map, b_map;
-  {
-    cuuint64_t dims[4] = {(cuuint64_t)Cpad, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
-    cuuint64_t strides[3] = {(cuuint64_t)Cpad, (cuuint64_t)W * Cpad, (cuuint64_t)H * W * Cpad};
-    cuuint32_t box[4] = {128u, (cuuint32_t)g.IC, (cuuint32_t)g.R, 1u};
-    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
-    CUresult cr = encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(dbytes), dims, strides,
-                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return XNC_ENOTSUP;
-  }
   // B: weight rows [n_nb * taps * KBn * NP][128 B]; box = NP/2 rows
+  CUtensorMap b_map;
   {
     const cuuint64_t rows = (cuuint64_t)g.n_nb * g.taps * g.KBn * g.NP;
     cuuint64_t dims[2] = {128u, rows};
@@ -691,7 +725,7 @@ int launch_conv_umma(const uint8_t* dbytes, const uint8_t* wq, const int32_t* sw
     if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
     attr = smem;
   }
-  kern<<<2 * pairs, kPThreads, smem, s>>>(a_map, b_map, sw, K, alpha, g, y, acc);
+  kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc);
   return launch_status();
 }
 

@@ -22,33 +22,30 @@ namespace xnc {
 // Phase 1: each thread walks the C channels of its pixels (16-byte coalesced
 // loads, x read once), builds one 32-channel word per pixel per j and the A
 // sum, and parks the words in shared memory as [j][pixel] (16-byte stores).
-// Phase 2: the block writes the packed outputs from shared memory with
-// consecutive lanes on consecutive addresses -- bits as [q][Cw] words and/or
-// the tcgen05 operand as d-bytes [q][Cpad] (d = 1 for x < 0, 0 for c >= C),
-// 512 contiguous bytes per warp store.
-constexpr int kPackThreads = 256;
+// Phase 2: the block writes the bits [q][Cw] from shared memory with
+// consecutive lanes on consecutive words (coalesced warp stores).  Every conv
+// kernel (popc, b1 mma.sync and the tcgen05 pair kernel, which expands the
+// bits to its byte operand in shared memory) reads this one format.
+#ifndef XNC_PACK_THREADS
+#define XNC_PACK_THREADS 512  // sweep (tools/pack_sweep.py): 512 x unroll 8 = 6.4 TB/s at C3, 256 = 5.0
+#endif
+#ifndef XNC_PACK_UNROLL
+#define XNC_PACK_UNROLL 8
+#endif
+constexpr int kPackThreads = XNC_PACK_THREADS;  // preferred block size (smaller if smem is short)
+constexpr int kPackUnroll = XNC_PACK_UNROLL;  // channel loads in flight per thread
 
-__device__ __forceinline__ uint4 expand_d16(uint32_t d16) {
-  uint4 r;
-  r.x = ((d16 & 0xFu) * 0x00204081u) & 0x01010101u;
-  r.y = (((d16 >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
-  r.z = (((d16 >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
-  r.w = (((d16 >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
-  return r;
-}
-
-template <int VEC>
-__global__ void __launch_bounds__(kPackThreads) k_pack_input(const float* __restrict__ x, int C, int HW,
+template <int VEC, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_pack_input(const float* __restrict__ x, int C, int HW,
                                                              int Cw, float inv, long groups_per_img,
                                                              long total_groups,
                                                              uint32_t* __restrict__ bits,
-                                                             float* __restrict__ A,
-                                                             uint8_t* __restrict__ dbytes, int Cpad) {
+                                                             float* __restrict__ A) {
   extern __shared__ uint4 pack_smem[];
   uint32_t* wtile = reinterpret_cast<uint32_t*>(pack_smem);
-  constexpr int PIX = kPackThreads * VEC;     // pixels per block
+  constexpr int PIX = THREADS * VEC;          // pixels per block
   constexpr int JS = PIX + 4;                 // word-plane stride (bank skew, keeps 16 B alignment)
-  const long gid0 = (long)blockIdx.x * kPackThreads;
+  const long gid0 = (long)blockIdx.x * THREADS;
   const long gid = gid0 + threadIdx.x;
   const long q0 = gid0 * VEC;                 // first linear pixel of the block
   const long q_end = total_groups * VEC;
@@ -64,7 +61,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_input(const float* __rest
 #pragma unroll
       for (int i = 0; i < VEC; ++i) word[i] = 0u;
       const int cend = min(32, C - 32 * j);
-#pragma unroll 8
+#pragma unroll kPackUnroll
       for (int cc = 0; cc < cend; ++cc) {
         const float* src = xp + (long)(32 * j + cc) * HW;
         float v[VEC];
@@ -101,24 +98,9 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_input(const float* __rest
   const int npix = (int)min((long)PIX, q_end - q0);
   if (bits != nullptr) {
     uint32_t* bp = bits + q0 * Cw;
-    for (int idx = threadIdx.x; idx < npix * Cw; idx += kPackThreads) {
+    for (int idx = threadIdx.x; idx < npix * Cw; idx += THREADS) {
       const int px = idx / Cw, j = idx - px * Cw;
       bp[idx] = wtile[j * JS + px];
-    }
-  }
-  if (dbytes != nullptr) {
-    const int chunks = Cpad >> 4;  // 16 channels per 16-byte chunk
-    uint8_t* dp = dbytes + q0 * Cpad;
-    for (int idx = threadIdx.x; idx < npix * chunks; idx += kPackThreads) {
-      const int px = idx / chunks, ch = idx - px * chunks;
-      const int j = ch >> 1;
-      uint32_t d16 = 0u;
-      if (j < Cw) {
-        const int c0 = ch * 16;
-        const uint32_t valid = C - c0 >= 16 ? 0xFFFFu : (C > c0 ? ((1u << (C - c0)) - 1u) : 0u);
-        d16 = (~(wtile[j * JS + px] >> ((ch & 1) * 16))) & valid;
-      }
-      *reinterpret_cast<uint4*>(dp + (long)px * Cpad + ch * 16) = expand_d16(d16);
     }
   }
 }
@@ -130,7 +112,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_input(const float* __rest
 // pixel (the channel sum must stay sequential for bit-exactness); x is read
 // twice, from L2 for these sizes.
 __global__ void k_pack_words(const float* __restrict__ x, int C, int HW, int Cw, long npix,
-                             uint32_t* __restrict__ bits, uint8_t* __restrict__ dbytes, int Cpad) {
+                             uint32_t* __restrict__ bits) {
   const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= npix * Cw) return;
   long q;
@@ -147,16 +129,7 @@ __global__ void k_pack_words(const float* __restrict__ x, int C, int HW, int Cw,
   const int cend = min(32, C - 32 * j);
   uint32_t word = 0u;
   for (int cc = 0; cc < cend; ++cc) word |= (__ldg(xp + (long)cc * HW) >= 0.0f ? 1u : 0u) << cc;
-  if (bits) bits[q * Cw + j] = word;
-  if (dbytes) {
-    const uint32_t valid = cend == 32 ? 0xFFFFFFFFu : ((1u << cend) - 1u);
-    const uint32_t d = ~word & valid;
-    uint8_t* dp = dbytes + q * Cpad + 32 * j;
-    reinterpret_cast<uint4*>(dp)[0] = expand_d16(d & 0xFFFFu);
-    reinterpret_cast<uint4*>(dp)[1] = expand_d16(d >> 16);
-    if (j == Cw - 1)  // zero the channel padding up to Cpad
-      for (int c = 32 * Cw; c < Cpad; c += 16) *reinterpret_cast<uint4*>(dbytes + q * Cpad + c) = make_uint4(0, 0, 0, 0);
-  }
+  bits[q * Cw + j] = word;
 }
 
 __global__ void k_absmean(const float* __restrict__ x, int C, int HW, long npix, float inv,
@@ -179,16 +152,15 @@ __global__ void k_absmean(const float* __restrict__ x, int C, int HW, long npix,
 }
 
 int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
-                      cudaStream_t s, uint8_t* dbytes) {
+                      cudaStream_t s) {
   {
     const long npix = (long)N * H * W;
     const long vec_groups = (H * W) % 4 == 0 ? npix / 4 : npix;
     // few pixels with long channel loops (13x13 / 6x6 / 1x1 layers): the 2-D path
-    if (vec_groups < 2L * 148 * kPackThreads && C >= 256) {
+    if (vec_groups < 2L * 148 * 256 && C >= 256) {
       const int Cw = cdiv(C, 32);
       const long words = npix * Cw;
-      k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, dbytes,
-                                                              round_up(C, 128));
+      k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits);
       if (A) k_absmean<<<(unsigned)cdivl(npix, 128), 128, 0, s>>>(x, C, H * W, npix, (float)(1.0 / (double)C), A);
       return launch_status();
     }
@@ -199,25 +171,30 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
                     (A == nullptr || (reinterpret_cast<uintptr_t>(A) & 15) == 0);
   const int vec = vec4 ? 4 : 1;
-  const size_t smem = (size_t)Cw * (kPackThreads * vec + 4) * 4;
-  if (smem > 200 * 1024) return XNC_ENOTSUP;  // C > ~12k channels
   const long gpi = HW / vec, total = gpi * N;
-  const unsigned blocks = (unsigned)cdivl(total, kPackThreads);
-  const int Cpad = round_up(C, 128);
+  // largest block (up to kPackThreads) whose word tile still lets two blocks share an SM
+  int threads = kPackThreads;
+  while (threads > 128 && (size_t)Cw * (threads * vec + 4) * 4 > 100 * 1024) threads /= 2;
+  const size_t smem = (size_t)Cw * (threads * vec + 4) * 4;
+  if (smem > 200 * 1024) return XNC_ENOTSUP;  // C > ~12k channels
+  const unsigned blocks = (unsigned)cdivl(total, threads);
+  static size_t opted[2][3] = {{0, 0, 0}, {0, 0, 0}};  // one-time smem opt-in per instantiation
+  auto go = [&](auto kern, int t) {
+    size_t& o = opted[vec4 ? 1 : 0][t == 512 ? 2 : t == 256 ? 1 : 0];
+    if (smem > 48 * 1024 && smem > o) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      o = smem;
+    }
+    kern<<<blocks, t, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A);
+  };
   if (vec4) {
-    static size_t attr4 = 0;
-    if (smem > 48 * 1024 && smem > attr4) {
-      cudaFuncSetAttribute(k_pack_input<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr4 = smem;
-    }
-    k_pack_input<4><<<blocks, kPackThreads, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, dbytes, Cpad);
+    if (threads == 512) go(k_pack_input<4, 512>, 512);
+    else if (threads == 256) go(k_pack_input<4, 256>, 256);
+    else go(k_pack_input<4, 128>, 128);
   } else {
-    static size_t attr1 = 0;
-    if (smem > 48 * 1024 && smem > attr1) {
-      cudaFuncSetAttribute(k_pack_input<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr1 = smem;
-    }
-    k_pack_input<1><<<blocks, kPackThreads, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, dbytes, Cpad);
+    if (threads == 512) go(k_pack_input<1, 512>, 512);
+    else if (threads == 256) go(k_pack_input<1, 256>, 256);
+    else go(k_pack_input<1, 128>, 128);
   }
   return launch_status();
 }

@@ -82,12 +82,16 @@ class XnorConv2d:
             return self.forward_host(x, out=out)
         x = x.contiguous()
         self.out_shape(x.shape)
+        return self._forward_device(x, out, want_acc)
+
+    def _forward_device(self, x: torch.Tensor, out: torch.Tensor | None = None,
+                        want_acc: bool = False):
         variant = self.kernel_for(x.shape)
         if variant == "popc-fc":
             return self._forward_fc(x, out, want_acc)
         if variant == "popc" and not want_acc:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
-        bits, A = ops.pack_input_umma(x) if variant == "umma" else ops.pack_input(x)
+        bits, A = ops.pack_input(x)
         K = ops.scale_map(A, self.kh, self.kw, self.pad)
         y, acc = ops.xnor_conv(bits, self.filters, K, self.pad, want_acc=want_acc,
                                variant=variant, y=out)
@@ -181,8 +185,7 @@ class XnorConv2d:
                 s_cmp.wait_event(st["x_ready"][slot])
                 if i >= 2:
                     s_cmp.wait_event(st["y_free"][slot])
-                ws = st["ws"] if b - a == chunk else self.workspace(xb)
-                ops.layer_forward(xb, self.filters, self.pad, ws, y=yb)
+                self._forward_device(xb, yb)
                 st["x_free"][slot].record(s_cmp)
                 st["y_ready"][slot].record(s_cmp)
             with torch.cuda.stream(s_out):

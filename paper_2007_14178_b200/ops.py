@@ -60,22 +60,6 @@ def pack_input_into(x: torch.Tensor, bits: torch.Tensor, A: torch.Tensor | None)
           "xnc_pack_input")
 
 
-def dbytes_channels(C: int) -> int:
-    """Channel stride of the tcgen05 d-byte operand (128-channel K blocks)."""
-    return (C + 127) // 128 * 128
-
-
-def pack_input_umma(x: torch.Tensor, want_A: bool = True):
-    """K1 (tcgen05 variant): x f32 [N,C,H,W] -> (d-bytes u8 [N,H,W,Cpad], A f32 [N,H,W])."""
-    _need_cuda(x, "x", torch.float32)
-    N, C, H, W = x.shape
-    d = torch.empty((N, H, W, dbytes_channels(C)), dtype=torch.uint8, device=x.device)
-    A = torch.empty((N, H, W), dtype=torch.float32, device=x.device) if want_A else None
-    check(lib().xnc_pack_input_umma(x.data_ptr(), N, C, H, W, d.data_ptr(), _ptr(A), _stream(x.device)),
-          "xnc_pack_input_umma")
-    return d, A
-
-
 @dataclass
 class PackedFilters:
     """Binarized filter bank on the device (build_filter for every filter)."""
@@ -160,19 +144,12 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
               acc: torch.Tensor | None = None, W: int | None = None):
     """K3+K4: (y f32 [N,O,H',W'] or None, acc i32 [N,O,H',W'] or None).
 
-    popc / b1mma read `bits` (i32 [N,H,W,Cw]); umma reads d-bytes
-    (u8 [N,H,W,Cpad], from pack_input_umma) in the same argument."""
+    Every variant reads the packed bits `bits` (i32 [N,H,W,Cw], from pack_input)."""
     C = filt.C if C is None else C
-    if variant == "umma":
-        _need_cuda(bits, "dbytes", torch.uint8)
-        N, H, W, Cp = bits.shape
-        if Cp != dbytes_channels(C) or filt.C != C:
-            raise ValueError(f"d-bytes hold {Cp} channels per pixel; filters have {filt.C}")
-    else:
-        _need_cuda(bits, "bits", torch.int32)
-        N, H, W, Cw = bits.shape
-        if words(C) != Cw or filt.C != C:
-            raise ValueError(f"bits hold {Cw} words per pixel; filters have {filt.C} channels")
+    _need_cuda(bits, "bits", torch.int32)
+    N, H, W, Cw = bits.shape
+    if words(C) != Cw or filt.C != C:
+        raise ValueError(f"bits hold {Cw} words per pixel; filters have {filt.C} channels")
     oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
     dev = bits.device
     if want_y and y is None:

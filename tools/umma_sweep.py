@@ -39,7 +39,7 @@ def child(cfg: str, reps: int) -> None:
     w = torch.rand((O, C, k, k), device="cuda", generator=g) * 2 - 1
     filt = ops.pack_weights(w)
     ops.attach_umma_weights(filt, w)
-    d, A = ops.pack_input_umma(x)
+    d, A = ops.pack_input(x)
     K = ops.scale_map(A, k, k, pad)
     y = torch.empty((N, O, H + 2 * pad - k + 1, W + 2 * pad - k + 1), device="cuda")
     for _ in range(3):
