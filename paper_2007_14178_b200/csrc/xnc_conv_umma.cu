@@ -600,10 +600,16 @@ __global__ void k_weight_sign_sums(const T* __restrict__ w, int O, int C, int kk
   sw[o] = s;
 }
 
-// Filters per pair block.  NP must not depend on the image shape (the weights
-// are packed before any input is seen): 256-column MMAs whenever the filter
-// count is a multiple of 256, else 128 (zero filters pad the last block).
-static int pair_np(int O) { return O % 256 == 0 ? 256 : 128; }
+// Filters per pair block (the MMA's N, <= 256).  NP must not depend on the image
+// shape (the weights are packed before any input is seen).  The fewest blocks
+// that cover O, split evenly and rounded up to 32 (each CTA's half a multiple of
+// 16 rows): O = 256 -> 256, 384 -> 2 x 192, 300 -> 2 x 160, 128 -> 128.  Wide
+// MMAs matter: at N = 128 each pipeline wait costs ~2x the MMA time it hides
+// (profiles/umma_pair_rate_r1.jsonl), so 384 filters run as 2 x 192, not 3 x 128.
+static int pair_np(int O) {
+  const int blocks = cdiv(O, 256);
+  return round_up(cdiv(O, blocks), 32);
+}
 
 size_t umma_weight_bytes(int O, int C, int kh, int kw) {
   const int NP = pair_np(O);
@@ -652,13 +658,13 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
          (long)g.n_nb * g.NP * g.oh * g.ow < 0x7fffffffL;
 }
 
-// MH = 2 row blocks per CTA for 128-filter blocks (eight 128-cycle-equivalent
-// MMAs per chunk), 1 for 256-filter blocks; fall back to MH = 1 when the rows do
-// not fit shared memory.  XNC_UMMA_MH overrides (tuning knob).
+// MH = 2 row blocks per CTA for narrow filter blocks (NP <= 128: two MMAs per
+// K step), 1 for wider ones; fall back to MH = 1 when the rows do not fit shared
+// memory.  XNC_UMMA_MH overrides (tuning knob).
 static bool pair_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, PairGeom& g, size_t& smem) {
   static const int mh_env = getenv("XNC_UMMA_MH") ? atoi(getenv("XNC_UMMA_MH")) : 0;
-  int mh = pair_np(O) == 256 ? 1 : 2;
-  if (mh_env == 1 || (mh_env == 2 && pair_np(O) == 128)) mh = mh_env;
+  int mh = pair_np(O) > 128 ? 1 : 2;
+  if (mh_env == 1 || (mh_env == 2 && pair_np(O) <= 128)) mh = mh_env;
   for (; mh >= 1; mh /= 2)
     if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem)) return true;
   return false;
