@@ -66,7 +66,11 @@
 
 namespace xnc {
 
-constexpr int kPThreads = 640;
+#ifndef XNC_EPI_WARPS
+#define XNC_EPI_WARPS 16
+#endif
+constexpr int kPEpiWarps = XNC_EPI_WARPS;  // multiple of 4 (one group per TMEM lane quadrant)
+constexpr int kPThreads = 128 + 32 * kPEpiWarps;
 #ifndef XNC_PSTAGES
 #define XNC_PSTAGES 6
 #endif
@@ -80,7 +84,6 @@ constexpr int kPMaxA = 2 * kPMaxKB;  // A plane ring: two tiles' planes when the
 constexpr int kPAWarp0 = 2;      // first A-producer warp
 constexpr int kPAWarps = 2;
 constexpr int kPEpiWarp0 = 4;    // first epilogue warp
-constexpr int kPEpiWarps = 16;
 constexpr int kProfSlots = 16;
 
 // Profiling only (XNC_UMMA_DEBUG bit 7): per-CTA cycle counters, read back with
@@ -134,10 +137,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// try_wait with a suspend-time hint (ns): the thread sleeps until the phase
+// completes or the hint elapses instead of re-polling
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity), "r"(hint_ns)
+        : "memory");
+  }
+}
+
+#ifndef XNC_EPI_HINT
+#define XNC_EPI_HINT 0
+#endif
+#ifndef XNC_PROD_HINT
+#define XNC_PROD_HINT 0
+#endif
+
 __device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, bool prof,
-                                               unsigned long long& acc) {
+                                               unsigned long long& acc, uint32_t hint_ns = 0) {
   const unsigned long long t0 = prof ? clock64() : 0ull;
-  mbar_wait(bar, parity);
+  if (hint_ns) mbar_wait_hint(bar, parity, hint_ns);
+  else mbar_wait(bar, parity);
   if (prof) acc += clock64() - t0;
 }
 
@@ -229,7 +254,8 @@ struct PairGeom {
   int n_nb;          // filter blocks
   int tiles;         // N * n_mt
   uint32_t b_half_bytes, tmem_cols;
-  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 2 = build the
+  int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
+             // (kPCPS == 1 only), bit 8 = no B protocol at all after the first fill, bit 2 = build the
              // input planes once, bit 5 = epilogue does only the TMEM handshake, bit 6 = chunk
              // issue timeline of pair 0 (profile rows 512+), bit 7 = cycle counters (xnc_umma_profile)
 };
@@ -300,8 +326,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
               const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
               if (j == 0) {
-                if (sidx >= kPStages) mbar_wait_prof(&b_empty[st], ((sidx / kPStages) - 1) & 1, prof, w_be);
+                if (sidx >= kPStages) mbar_wait_prof(&b_empty[st], ((sidx / kPStages) - 1) & 1, prof, w_be, XNC_PROD_HINT);
                 const uint32_t n_in = min((uint32_t)kPCPS, total - step);
+                if ((g.debug & 256) && sidx >= kPStages) break;  // profiling: no B protocol after the fill
+                if ((g.debug & 2) && sidx >= kPStages) {  // profiling: reuse resident chunks, no traffic
+                  if (leader) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&b_full[st])) : "memory");
+                  step += kPCPS - 1 - j;
+                  tap += kPCPS - 1;
+                  continue;
+                }
                 if (leader) mbar_expect_tx(&b_full[st], n_in * 2 * g.b_half_bytes);
               }
               const int row = ((nb * g.taps + tap) * g.KBn + kb) * g.NP + (int)rank * (g.NP / 2);
@@ -324,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       for (int kb = 0; kb < g.KBn; ++kb) {
         const uint32_t use = it * g.KBn + kb, sl = use % g.NA;  // ring slot of this plane
         if (use >= (uint32_t)g.NA) {
-          if (lane == 0) mbar_wait_prof(&a_empty[sl], ((use / g.NA) - 1) & 1, prof, w_ae);
+          if (lane == 0) mbar_wait_prof(&a_empty[sl], ((use / g.NA) - 1) & 1, prof, w_ae, XNC_PROD_HINT);
           __syncwarp();
         }
         if (!((g.debug & 4) && it >= 1)) {  // bit 2 (profiling): keep the first tile's planes
@@ -408,7 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
               for (int kx = 0; kx < g.kw; ++kx, ++step) {
                 const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
                 const unsigned long long tw0 = trace ? clock64() : 0ull;
-                if (j == 0) {
+                const bool b_proto = !((g.debug & 256) && sidx >= kPStages);
+                if (j == 0 && b_proto) {
                   mbar_wait_prof(&b_full[st], (sidx / kPStages) & 1, prof, w_bf);
                   asm volatile("tcgen05.fence::after_thread_sync;");
                 }
@@ -428,7 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
                 }
                 acc = 1;
                 n_mma += 4 * MH;
-                if (j == kPCPS - 1 || step + 1 == total) umma_commit_pair(&b_empty[st]);
+                if (b_proto && (j == kPCPS - 1 || step + 1 == total)) umma_commit_pair(&b_empty[st]);
               }
             }
             if (nb == g.n_nb - 1) umma_commit_pair(&a_empty[sl]);
@@ -482,9 +516,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       }
       for (int nb = 0; nb < g.n_nb; ++nb, ++item) {
         const uint32_t buf = item & 1;
-        mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf);
+        mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        for (int ch = (g.debug & 32) ? n_chunks : cg; ch < n_chunks; ch += 4) {
+        for (int ch = (g.debug & 32) ? n_chunks : cg; ch < n_chunks; ch += kPEpiWarps / 4) {
           const int c = ch * 16;
           const int obase = nb * g.NP + c;
           uint32_t v[MH][16];
