@@ -72,10 +72,10 @@ namespace xnc {
 constexpr int kPEpiWarps = XNC_EPI_WARPS;  // multiple of 4 (one group per TMEM lane quadrant)
 constexpr int kPThreads = 128 + 32 * kPEpiWarps;
 #ifndef XNC_PSTAGES
-#define XNC_PSTAGES 6
+#define XNC_PSTAGES 2
 #endif
 #ifndef XNC_PCPS
-#define XNC_PCPS 1
+#define XNC_PCPS 3
 #endif
 constexpr int kPStages = XNC_PSTAGES;  // B pipeline depth (stages)
 constexpr int kPCPS = XNC_PCPS;        // (tap, K block) chunks per B stage: one wait + one commit each
@@ -89,7 +89,8 @@ constexpr int kProfSlots = 16;
 // Profiling only (XNC_UMMA_DEBUG bit 7): per-CTA cycle counters, read back with
 // xnc_umma_profile().  Slots: 0 issuer total, 1 issuer wait t_empty, 2 issuer
 // wait a_full, 3 issuer wait b_full, 4 MMAs issued, 5 epilogue (warp 4) total,
-// 6 epilogue wait t_full, 7 B producer wait b_empty, 8 A producer wait a_empty.
+// 6 epilogue wait t_full, 7 B producer wait b_empty, 8 A producer wait a_empty,
+// 10 epilogue (warp 4) TMEM load + constants, 11 epilogue math + stores.
 __device__ unsigned long long g_umma_prof[1024][kProfSlots];
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -214,6 +215,29 @@ __device__ __forceinline__ void umma_i8_pair(uint32_t tmem_d, uint64_t adesc, ui
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// The same two, issued by one elected lane of a converged warp.  Keeping the
+// issue loop warp-uniform lets ptxas hold most of the issue path in uniform
+// registers; run by a single divergent lane the loop needed ~110 instructions
+// (five R2UR per MMA, an ELECT loop per MMA) per chunk of four MMAs and capped
+// the issue rate at ~180 SM cycles per 128-cycle MMA (131 after this change,
+// measured with every barrier protocol switched off).
+__device__ __forceinline__ void umma_i8_pair_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                   uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_pair_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_addr(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
 }
 
 // arrive (once MMAs issued so far complete) on the mbarrier at this offset in
@@ -408,14 +432,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     // ================= MMA issuer (leader CTA only)
     // Descriptors are built once and advanced by adding (byte offset >> 4) to
     // the start-address field (addresses < 256 KB never carry out of it).
-    if (leader && lane == 0) {
+    if (leader) {  // the whole warp runs the loop; one elected lane issues
       const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(g.NP >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
       const uint64_t a_desc0 = umma_desc_sw128(smem_addr(a_s));
       const uint64_t b_desc0 = umma_desc_sw128(smem_addr(b_s));
       const uint32_t plane16 = (uint32_t)g.plane_bytes >> 4, b16 = g.b_half_bytes >> 4;
-      const bool prof = g.debug & 128;
-      const bool trace = (g.debug & 64) && blockIdx.x == 0;
+      const bool prof = (g.debug & 128) && lane == 0;
+      const bool trace = (g.debug & 64) && blockIdx.x == 0 && lane == 0;
       const int my_tiles = (g.tiles - cluster + n_clusters - 1) / n_clusters;
       const uint32_t total = (uint32_t)my_tiles * g.n_nb * g.KBn * g.taps;
       unsigned long long w_te = 0, w_af = 0, w_bf = 0, n_mma = 0;
@@ -457,17 +481,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
                 for (int s = 0; s < 4; ++s) {
 #pragma unroll
                   for (int h = 0; h < MH; ++h)
-                    umma_i8_pair(d0 + h * g.NP, a_tap + h * 1024 + 2 * s, b_st + 2 * s, idesc,
+                    umma_i8_pair_elect(d0 + h * g.NP, a_tap + h * 1024 + 2 * s, b_st + 2 * s, idesc,
                                  acc | (uint32_t)s);
                 }
                 acc = 1;
                 n_mma += 4 * MH;
-                if (b_proto && (j == kPCPS - 1 || step + 1 == total)) umma_commit_pair(&b_empty[st]);
+                if (b_proto && (j == kPCPS - 1 || step + 1 == total)) umma_commit_pair_elect(&b_empty[st]);
               }
             }
-            if (nb == g.n_nb - 1) umma_commit_pair(&a_empty[sl]);
+            if (nb == g.n_nb - 1) umma_commit_pair_elect(&a_empty[sl]);
           }
-          umma_commit_pair(&t_full[buf]);
+          umma_commit_pair_elect(&t_full[buf]);
         }
       }
       if (prof) {
@@ -493,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     const uint32_t t_empty0 = map_to_rank(smem_addr(&t_empty[0]), 0);
     uint32_t item = 0;
     const bool prof = (g.debug & 128) && warp == kPEpiWarp0 && lane == 0;
-    unsigned long long w_tf = 0;
+    unsigned long long w_tf = 0, w_ld = 0, w_st = 0;
     const unsigned long long t_start = clock64();
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
                         ((reinterpret_cast<uintptr_t>(alpha) & 15) == 0);
@@ -521,6 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         for (int ch = (g.debug & 32) ? n_chunks : cg; ch < n_chunks; ch += kPEpiWarps / 4) {
           const int c = ch * 16;
           const int obase = nb * g.NP + c;
+          const unsigned long long tc0 = prof ? clock64() : 0ull;
           uint32_t v[MH][16];
 #pragma unroll
           for (int h = 0; h < MH; ++h)
@@ -545,6 +570,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
             }
           }
           tmem_wait_ld();
+          const unsigned long long tc1 = prof ? clock64() : 0ull;
+          if (prof) w_ld += tc1 - tc0;
           if (g.debug & 1) continue;
           if (fast && obase + 16 <= g.O) {
             // hot path: float output only, all 16 filters valid -- about six
@@ -558,6 +585,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
                 st_cs_pred(yp + j * plane_out32, __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]), ok[h]);
               }
             }
+            if (prof) w_st += clock64() - tc1;
             continue;
           }
 #pragma unroll
@@ -583,6 +611,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     if (prof) {
       g_umma_prof[blockIdx.x][5] = clock64() - t_start;
       g_umma_prof[blockIdx.x][6] = w_tf;
+      g_umma_prof[blockIdx.x][10] = w_ld;
+      g_umma_prof[blockIdx.x][11] = w_st;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");

@@ -18,7 +18,8 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t addr) {
 // MODE 0: back-to-back MMAs; MODE 1: per group of 4: try_wait(done barrier) + fence, commit multicast;
 // MODE 2: as 1 but the wait sits between the group's 2nd and 3rd MMA; MODE 3: as 1 with a
 // commit only (no wait); MODE 4: as 1 with a wait only (no commit).  out[64 + pair] = cycles
-// spent inside the waits.
+// spent inside the waits.  MODE 5: as 0 but every MMA accumulates into the same
+// accumulator; MODE 6: as 0 alternating the accumulator on every MMA; MODE 7: as 1 with one accumulator.
 template <int NP, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) k_pair(int n_groups, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -64,18 +65,19 @@ __global__ void __cluster_dims__(2, 1, 1) k_pair(int n_groups, long long* out) {
       tw += clock64() - a;
     };
     for (int g = 0; g < n_groups; ++g) {
-      if (MODE == 1 || MODE == 4) wait_ready();
+      if (MODE == 1 || MODE == 4 || MODE == 7) wait_ready();
       const int tap = g % 9;
       const uint64_t a = a0 + (uint32_t)((tap / 3) * 58 + tap % 3) * 8u;
       const uint64_t b = b0 + (uint32_t)(g % 6) * (64 * 128 / 16);
-      const uint32_t d = tmem + (g & 1) * NP;
+      const uint32_t d = tmem + ((MODE == 5 || MODE == 7) ? 0u : (g & 1) * NP);
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         if (MODE == 2 && s == 2) wait_ready();
+        const uint32_t dd = MODE == 6 ? tmem + (s & 1) * NP : d;
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                     ::"r"(d), "l"(a + 2 * s), "l"(b + 2 * s), "r"(idesc), "r"((uint32_t)(g >= 2 || s > 0)));
+                     ::"r"(dd), "l"(a + 2 * s), "l"(b + 2 * s), "r"(idesc), "r"((uint32_t)(g >= 2 || s > 0)));
       }
-      if (MODE == 1 || MODE == 2 || MODE == 3)
+      if (MODE == 1 || MODE == 2 || MODE == 3 || MODE == 7)
         asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                      ::"r"(smem_u32(&cbar)), "h"((uint16_t)3) : "memory");
     }
@@ -133,7 +135,8 @@ int main() {
   long long* d_out; CK(cudaMalloc(&d_out, 4096));
   run<256, 0>(p.multiProcessorCount, d_out); run<256, 1>(p.multiProcessorCount, d_out);
   run<256, 2>(p.multiProcessorCount, d_out); run<256, 3>(p.multiProcessorCount, d_out);
-  run<256, 4>(p.multiProcessorCount, d_out);
+  run<256, 4>(p.multiProcessorCount, d_out); run<256, 5>(p.multiProcessorCount, d_out);
+  run<256, 6>(p.multiProcessorCount, d_out); run<256, 7>(p.multiProcessorCount, d_out);
   run<128, 0>(p.multiProcessorCount, d_out); run<128, 1>(p.multiProcessorCount, d_out);
   run<128, 2>(p.multiProcessorCount, d_out); run<128, 3>(p.multiProcessorCount, d_out);
   run<128, 4>(p.multiProcessorCount, d_out);

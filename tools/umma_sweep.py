@@ -73,9 +73,11 @@ def child(cfg: str, reps: int) -> None:
         from paper_2007_14178_b200._lib import lib
         buf = np.zeros((148, 16), dtype=np.uint64)
         lib().xnc_umma_profile(buf.ctypes.data_as(ctypes.c_void_p), 148)
+        buf[:, 9] = 0
         tot = buf[:, 0].astype(np.float64)
         names = ["issuer_total", "wait_t_empty", "wait_a_full", "wait_b_full", "mmas", "epi_total",
-                 "epi_wait_t_full", "bprod_wait_b_empty", "aprod_wait_a_empty", "issue_blocks"]
+                 "epi_wait_t_full", "bprod_wait_b_empty", "aprod_wait_a_empty", "issue_blocks", "epi_ld",
+                 "epi_store"]
         lead = buf[0::2]  # CTA pairs: the MMA issuer runs on the even (leader) CTA
         prof = {n: round(float(buf[:, i].astype(np.float64).mean()), 0) for i, n in enumerate(names)}
         for i in (0, 1, 2, 3, 4):
