@@ -277,6 +277,7 @@ struct PairGeom {
   int n_mt;          // pair tiles per image
   int n_nb;          // filter blocks
   int tiles;         // N * n_mt
+  int units;         // tiles * n_nb work units (pair tile, filter block), strided over the pairs
   uint32_t b_half_bytes, tmem_cols;
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
              // (kPCPS == 1 only), bit 8 = no B protocol at all after the first fill, bit 2 = build the
@@ -341,11 +342,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       const bool prof = g.debug & 128;
       unsigned long long w_be = 0;
       const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
-      const int my_tiles = (g.tiles - cluster + n_clusters - 1) / n_clusters;
-      const uint32_t total = (uint32_t)my_tiles * g.n_nb * g.KBn * g.taps;
+      const int my_units = (g.units - cluster + n_clusters - 1) / n_clusters;
+      const uint32_t total = (uint32_t)my_units * g.KBn * g.taps;
       uint32_t step = 0;
-      for (int t = cluster; t < g.tiles; t += n_clusters)
-        for (int nb = 0; nb < g.n_nb; ++nb)
+      for (int u = cluster; u < g.units; u += n_clusters) {
+        const int nb = u % g.n_nb;
           for (int kb = 0; kb < g.KBn; ++kb)
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
               const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
@@ -364,6 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
               const int row = ((nb * g.taps + tap) * g.KBn + kb) * g.NP + (int)rank * (g.NP / 2);
               tma_load_2d_pair(b_s + (st * kPCPS + j) * g.b_half_bytes, &b_map, 0, row, full0 + st * 8);
             }
+      }
       if (prof) g_umma_prof[blockIdx.x][7] = w_be;
     }
   } else if (warp >= kPAWarp0 && warp < kPAWarp0 + kPAWarps) {
@@ -373,8 +375,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     unsigned long long w_ae = 0;
     const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
     const bool vec4 = (g.Cw & 3) == 0 && (reinterpret_cast<uintptr_t>(bits) & 15) == 0;
-    uint32_t it = 0;
-    for (int t = cluster; t < g.tiles; t += n_clusters, ++it) {
+    uint32_t it = 0;  // units of this pair so far: every unit builds its KBn planes
+    for (int u = cluster; u < g.units; u += n_clusters, ++it) {
+      const int t = u / g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
       const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
@@ -384,7 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
           if (lane == 0) mbar_wait_prof(&a_empty[sl], ((use / g.NA) - 1) & 1, prof, w_ae, XNC_PROD_HINT);
           __syncwarp();
         }
-        if (!((g.debug & 4) && it >= 1)) {  // bit 2 (profiling): keep the first tile's planes
+        if (!((g.debug & 4) && use >= (uint32_t)g.NA)) {  // bit 2 (profiling): planes built once
           uint8_t* plane = a_s + (size_t)sl * g.plane_bytes;
           // valid-channel masks of the block's four words
           uint32_t vmask[4];
@@ -440,13 +443,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       const uint32_t plane16 = (uint32_t)g.plane_bytes >> 4, b16 = g.b_half_bytes >> 4;
       const bool prof = (g.debug & 128) && lane == 0;
       const bool trace = (g.debug & 64) && blockIdx.x == 0 && lane == 0;
-      const int my_tiles = (g.tiles - cluster + n_clusters - 1) / n_clusters;
-      const uint32_t total = (uint32_t)my_tiles * g.n_nb * g.KBn * g.taps;
+      const int my_units = (g.units - cluster + n_clusters - 1) / n_clusters;
+      const uint32_t total = (uint32_t)my_units * g.KBn * g.taps;
       unsigned long long w_te = 0, w_af = 0, w_bf = 0, n_mma = 0;
       const unsigned long long t_start = clock64();
-      uint32_t step = 0, item = 0, it = 0;
-      for (int t = cluster; t < g.tiles; t += n_clusters, ++it) {
-        for (int nb = 0; nb < g.n_nb; ++nb, ++item) {
+      uint32_t step = 0, item = 0;
+      for (int u = cluster; u < g.units; u += n_clusters, ++item) {
+        {
           const uint32_t buf = item & 1;
           if (item >= 2) {
             mbar_wait_prof(&t_empty[buf], ((item >> 1) - 1) & 1, prof, w_te);
@@ -455,11 +458,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
           const uint32_t d0 = tmem + buf * (MH * g.NP);
           uint32_t acc = 0;
           for (int kb = 0; kb < g.KBn; ++kb) {
-            const uint32_t use = it * g.KBn + kb, sl = use % g.NA;
-            if (nb == 0) {
-              mbar_wait_prof(&a_full[sl], (use / g.NA) & 1, prof, w_af);
-              asm volatile("tcgen05.fence::after_thread_sync;");
-            }
+            const uint32_t use = item * g.KBn + kb, sl = use % g.NA;
+            mbar_wait_prof(&a_full[sl], (use / g.NA) & 1, prof, w_af);
+            asm volatile("tcgen05.fence::after_thread_sync;");
             const uint64_t a_kb = a_desc0 + sl * plane16;
             for (int ky = 0; ky < g.kh; ++ky) {
               for (int kx = 0; kx < g.kw; ++kx, ++step) {
@@ -489,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
                 if (b_proto && (j == kPCPS - 1 || step + 1 == total)) umma_commit_pair_elect(&b_empty[st]);
               }
             }
-            if (nb == g.n_nb - 1) umma_commit_pair_elect(&a_empty[sl]);
+            umma_commit_pair_elect(&a_empty[sl]);
           }
           umma_commit_pair_elect(&t_full[buf]);
         }
@@ -524,7 +525,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     // 32-bit filter-plane stride for the hot path (host guarantees O*oh*ow < 2^31)
     const int plane_out32 = g.oh * g.ow;
     const bool fast = y != nullptr && acc_out == nullptr;
-    for (int t = cluster; t < g.tiles; t += n_clusters) {
+    for (int u = cluster; u < g.units; u += n_clusters, ++item) {
+      const int t = u / g.n_nb, nb = u - t * g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);
       size_t pix[MH];
@@ -538,7 +540,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         pix[h] = (size_t)n * g.O * plane_out + (size_t)rr * g.ow + cc;
         kv[h] = (ok[h] && y) ? __ldg(Kmap + (size_t)n * plane_out + (size_t)rr * g.ow + cc) : 0.0f;
       }
-      for (int nb = 0; nb < g.n_nb; ++nb, ++item) {
+      {
         const uint32_t buf = item & 1;
         mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -711,14 +713,18 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   g.n_mt = cdiv(g.oh * g.IC, 2 * MT);
   g.n_nb = cdiv(O, g.NP);
   g.tiles = N * g.n_mt;
+  g.units = g.tiles * g.n_nb;
   g.b_half_bytes = (uint32_t)(g.NP / 2) * 128u;
   const int cols = 2 * MH * g.NP;  // two accumulators x MH row blocks
   g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   const size_t b_bytes = (size_t)kPStages * kPCPS * g.b_half_bytes + 1024;
-  g.NA = 2 * g.KBn;  // double-buffered planes when they fit, else one tile's worth
-  if ((size_t)g.NA * g.plane_bytes + b_bytes > 225 * 1024) g.NA = g.KBn;
+  // A plane ring: two units' planes when they fit (the next unit's planes are
+  // built during this unit's MMAs), else fewer; long K (fully connected layers
+  // viewed as 1 x N images) streams through the ring.
+  g.NA = 2 * g.KBn < kPMaxA ? 2 * g.KBn : kPMaxA;
+  while (g.NA > 1 && (size_t)g.NA * g.plane_bytes + b_bytes > 225 * 1024) --g.NA;
   smem = (size_t)g.NA * g.plane_bytes + b_bytes;
-  return cols <= 512 && g.KBn <= kPMaxKB && smem <= 225 * 1024 && (long)N * g.n_mt < 0x7fffffffL &&
+  return cols <= 512 && smem <= 225 * 1024 && (long)g.units < 0x7fffffffL &&
          (long)g.n_nb * g.NP * g.oh * g.ow < 0x7fffffffL;
 }
 
@@ -786,7 +792,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int pairs = g.tiles < sms / 2 ? g.tiles : sms / 2;
+  const int pairs = g.units < sms / 2 ? g.units : sms / 2;
   static size_t attr_smem[2] = {0, 0};  // one-time (per size increase) shared-memory opt-in
   auto kern = g.MH == 2 ? k_conv_umma_pair<2> : k_conv_umma_pair<1>;
   size_t& attr = attr_smem[g.MH == 2 ? 1 : 0];
