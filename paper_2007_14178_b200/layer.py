@@ -87,8 +87,8 @@ class XnorConv2d:
     def _forward_device(self, x: torch.Tensor, out: torch.Tensor | None = None,
                         want_acc: bool = False):
         variant = self.kernel_for(x.shape)
-        if variant == "popc-fc":
-            return self._forward_fc(x, out, want_acc)
+        if variant in ("popc-fc", "umma-fc"):
+            return self._forward_fc(x, out, want_acc, variant)
         if variant == "popc" and not want_acc:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
         bits, A = ops.pack_input(x)
@@ -106,7 +106,12 @@ class XnorConv2d:
         if self.variant != "auto":
             return self.variant
         if self._fc_shape(x_shape):
-            return "popc-fc"  # 1x1 output: the per-image pixel tiles of the other kernels idle
+            # 1x1 output: one 'pixel' per image, so the batch becomes the image width
+            # (a 1 x N image of kh*kw*C channels); tensor cores when the plan fits
+            Cp = self.kh * self.kw * C
+            if self.filters.wq is not None and ops.umma_supported(1, Cp, 1, N, self.O, 1, 1, 0):
+                return "umma-fc"
+            return "popc-fc"
         if ops.umma_supported(N, C, H, W, self.O, self.kh, self.kw, self.pad):
             return "umma"
         return "popc"
@@ -115,18 +120,20 @@ class XnorConv2d:
         N, C, H, W = x_shape
         return self.pad == 0 and self.kh == H and self.kw == W and C % 32 == 0 and N > 1
 
-    def _forward_fc(self, x: torch.Tensor, out: torch.Tensor | None, want_acc: bool):
+    def _forward_fc(self, x: torch.Tensor, out: torch.Tensor | None, want_acc: bool,
+                    variant: str = "popc-fc"):
         """Fully connected binary layer (kernel covers the whole input): every image
         is one 'pixel' of a 1-row image whose channels are the (y, x, c) words of
-        the image, so the popc kernel's column tiling runs over the batch.  Same
+        the image, so the conv kernels' pixel tiling runs over the batch.  Same
         arithmetic as the conv view: C' = kh*kw*C valid bits, K = box mean of A
-        over the whole input, alpha per filter."""
+        over the whole input, alpha per filter (the reference's (c, ky, kx) sum)."""
         N, C, H, W = x.shape
         bits, A = ops.pack_input(x)
         K = ops.scale_map(A, self.kh, self.kw, 0)                     # [N, 1, 1]
-        fcf = self._fc_filters()
+        fcf = self._fc_filters(umma=variant == "umma-fc")
         y1, acc1 = ops.xnor_conv(bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,
-                                 want_acc=want_acc)                  # [1, O, 1, N]
+                                 want_acc=want_acc,
+                                 variant="umma" if variant == "umma-fc" else "popc")  # [1, O, 1, N]
         y = y1.view(self.O, N).t().reshape(N, self.O, 1, 1)
         if out is not None:
             out.copy_(y)
@@ -135,7 +142,9 @@ class XnorConv2d:
             return y, acc1.view(self.O, N).t().reshape(N, self.O, 1, 1).contiguous()
         return y.contiguous()
 
-    def _fc_filters(self) -> ops.PackedFilters:
+    def _fc_filters(self, umma: bool = False) -> ops.PackedFilters:
+        """The filters as 1x1 filters over kh*kw*C channels in (y, x, c) order; alpha
+        stays the original filters' (summed in the reference's (c, ky, kx) order)."""
         f = getattr(self, "_fcf", None)
         if f is None:
             pf = self.filters
@@ -143,6 +152,11 @@ class XnorConv2d:
             f = ops.PackedFilters(wb.view(-1, 1, 1, self.O), pf.alpha, pf.alpha64, self.O,
                                   self.kh * self.kw * self.C, 1, 1)
             self._fcf = f
+        if umma and f.wq is None:
+            wp = self.weight.permute(0, 2, 3, 1).reshape(self.O, -1, 1, 1).contiguous()
+            tmp = ops.PackedFilters(f.wbits, f.alpha, f.alpha64, f.O, f.C, 1, 1)
+            ops.attach_umma_weights(tmp, wp)                           # signs + S_w only
+            f.wq, f.sw = tmp.wq, tmp.sw
         return f
 
     __call__ = forward

@@ -153,7 +153,8 @@ def test_umma_variant_vs_oracle(shape):
     _assert_float_parity(y, want)
 
 
-@pytest.mark.parametrize("N,C,S,O_,k", [(5, 64, 6, 6, 6), (9, 256, 6, 50, 6), (7, 128, 1, 33, 1)])
+@pytest.mark.parametrize("N,C,S,O_,k", [(5, 64, 6, 6, 6), (9, 256, 6, 50, 6), (7, 128, 1, 33, 1),
+                                        (300, 256, 6, 260, 6), (40, 1024, 1, 512, 1)])
 def test_fc_mode_matches_oracle(N, C, S, O_, k):
     """Fully connected binary layers (k == H == W, pad 0) take the batch-as-width path."""
     from paper_2007_14178_b200 import XnorConv2d
@@ -161,7 +162,9 @@ def test_fc_mode_matches_oracle(N, C, S, O_, k):
     x = O.f32_exact(rng, (N, C, S, S))
     w = O.f32_exact(rng, (O_, C, k, k))
     layer = XnorConv2d(torch.from_numpy(w).to(_dev()), pad=0, variant="auto")
-    assert layer.kernel_for(x.shape) in ("popc-fc", "umma")
+    assert layer.kernel_for(x.shape) in ("popc-fc", "umma-fc")
+    if N > 1:  # the tensor-core FC path must be the one taken (long K streams through its ring)
+        assert layer.kernel_for(x.shape) == "umma-fc"
     y, acc = layer.forward(torch.from_numpy(x).to(_dev()), want_acc=True)
     want, ints = O.conv_layer(x, w, 0, want_ints=True)
     assert np.array_equal(acc.cpu().numpy(), ints)
