@@ -6,7 +6,7 @@ binary convolutions with k <= 8 and explicit padding -- with the rest of
 XNOR-Net AlexNet in full precision through torch (cuDNN), off the binary hot
 path:
 
-    conv1  11x11/4, 3 -> 96      full precision      224 -> 55
+    conv1  11x11/4, 3 -> 96      full precision      224 -> 55  (as 3x3 over 4x4 space-to-depth)
     pool   3/2                                       55 -> 27
     conv2  5x5 pad 2, 96 -> 256  BINARY (XnorConv2d) 27
     pool   3/2                                       27 -> 13
@@ -73,6 +73,13 @@ class XnorNetAlexNet:
         self.device = dev
         self.conv1_w = rnd(96, 3, 11, 11, scale=(3 * 121) ** -0.5)
         self.conv1_b = rnd(96, scale=0.1)
+        # conv1 as a 3x3/1 conv over the 4x4 space-to-depth input (48 channels):
+        # the 11x11 kernel zero-padded to 12x12 and split into 4x4 phases.  Same
+        # products and sums as the 11x11/4 conv, in a shape cuDNN runs ~2x faster
+        # (tools/conv1_probe.py: 1.18 vs 2.13 ms at batch 256 incl. ReLU + pool).
+        w12 = F.pad(self.conv1_w, (0, 1, 0, 1))
+        self.conv1_w_s2d = (w12.view(96, 3, 3, 4, 3, 4).permute(0, 1, 3, 5, 2, 4)
+                            .reshape(96, 48, 3, 3).contiguous())
         self.binary: dict[str, XnorConv2d] = {}
         for name, cin, cout, k, pad in BINARY_LAYERS:
             self.binary[name] = XnorConv2d(rnd(cout, cin, k, k), pad=pad, variant=variant)
@@ -89,9 +96,14 @@ class XnorNetAlexNet:
         with _tf32_full_precision_layers():
             return self._forward(x, return_features)
 
+    def front_end(self, x: torch.Tensor) -> torch.Tensor:
+        """conv1 (11x11, stride 4, pad 2; full precision, via space-to-depth) -> ReLU
+        -> max-pool 3/2: the input of the first binary layer."""
+        h = F.conv2d(F.pixel_unshuffle(F.pad(x, (2, 2, 2, 2)), 4), self.conv1_w_s2d, self.conv1_b)
+        return F.max_pool2d(F.relu_(h), 3, 2)
+
     def _forward(self, x: torch.Tensor, return_features: bool):
-        h = F.conv2d(x, self.conv1_w, self.conv1_b, stride=4, padding=2)  # full precision
-        h = F.max_pool2d(F.relu(h), 3, 2)
+        h = self.front_end(x)
         feats = {}
         for name, *_ in BINARY_LAYERS:
             h = self.binary[name](h.contiguous())

@@ -22,7 +22,11 @@ def test_network_binary_layers_match_oracle():
     assert logits.shape == (3, 1000) and torch.isfinite(logits).all()
     assert torch.equal(logits, logits2)
     # layer inputs: conv1 -> relu -> pool for conv2; pooled / raw previous outputs after
-    h = F.max_pool2d(F.relu(F.conv2d(x, net.conv1_w, net.conv1_b, stride=4, padding=2)), 3, 2)
+    with torch.no_grad():
+        h = net.front_end(x)
+        # the space-to-depth front end is the 11x11/4 conv (TF32 on both sides)
+        ref = F.max_pool2d(F.relu(F.conv2d(x, net.conv1_w, net.conv1_b, stride=4, padding=2)), 3, 2)
+    assert torch.allclose(h, ref, rtol=1e-2, atol=1e-2)
     inputs = {}
     for name, *_ in BINARY_LAYERS:
         inputs[name] = h
