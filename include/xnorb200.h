@@ -121,6 +121,12 @@ size_t xnc_layer_workspace_bytes(int N, int C, int H, int W, int kh, int kw, int
 int xnc_layer_forward(const float* x, const uint32_t* wbits, const float* alpha,
                       int N, int C, int H, int W, int O, int kh, int kw, int pad,
                       void* workspace, float* y, int32_t* acc, void* stream);
+/* The same layer on the tcgen05 pair kernel (weights from xnc_pack_weights_umma;
+ * alpha from xnc_pack_weights).  XNC_ENOTSUP when xnc_umma_supported() is 0. */
+int xnc_layer_forward_umma(const float* x, const uint8_t* wq, const int32_t* sw,
+                           const float* alpha, int N, int C, int H, int W, int O, int kh,
+                           int kw, int pad, void* workspace, float* y, int32_t* acc,
+                           void* stream);
 
 /* ======================================================================
  * The reference kernel seam on the device (interop surface).

@@ -146,4 +146,23 @@ int xnc_layer_forward(const float* x, const uint32_t* wbits, const float* alpha,
   return launch_conv_popc(bits, wbits, K, alpha, N, C, H, W, O, kh, kw, pad, y, acc, s);
 }
 
+int xnc_layer_forward_umma(const float* x, const uint8_t* wq, const int32_t* sw, const float* alpha,
+                           int N, int C, int H, int W, int O, int kh, int kw, int pad, void* workspace,
+                           float* y, int32_t* acc, void* stream) {
+  if (!x || !wq || !sw || !alpha || !workspace || O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad))
+    return XNC_EINVAL;
+  if (!umma_supported(N, C, H, W, O, kh, kw, pad)) return XNC_ENOTSUP;
+  const size_t Cw = (C + 31) / 32;
+  char* ws = static_cast<char*>(workspace);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(ws);
+  float* A = reinterpret_cast<float*>(ws + align256((size_t)N * H * W * Cw * 4));
+  float* K = reinterpret_cast<float*>(reinterpret_cast<char*>(A) + align256((size_t)N * H * W * 4));
+  cudaStream_t s = as_stream(stream);
+  int rc = launch_pack_input(x, N, C, H, W, bits, A, s);
+  if (rc) return rc;
+  rc = launch_scale_map(A, N, H, W, kh, kw, pad, K, s);
+  if (rc) return rc;
+  return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, acc, s);
+}
+
 }  // extern "C"

@@ -91,6 +91,8 @@ class XnorConv2d:
             return self._forward_fc(x, out, want_acc, variant)
         if variant == "popc" and not want_acc:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
+        if variant == "umma" and not want_acc:  # one C-ABI call: K1 -> K2 -> tcgen05 K3+K4
+            return ops.layer_forward_umma(x, self.filters, self.pad, self.workspace(x), y=out)
         bits, A = ops.pack_input(x)
         K = ops.scale_map(A, self.kh, self.kw, self.pad)
         y, acc = ops.xnor_conv(bits, self.filters, K, self.pad, want_acc=want_acc,

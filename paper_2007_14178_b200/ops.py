@@ -194,3 +194,22 @@ def layer_forward(x: torch.Tensor, filt: PackedFilters, pad: int, workspace: tor
                                   H, W, filt.O, filt.kh, filt.kw, pad, workspace.data_ptr(), _ptr(y),
                                   _ptr(acc), _stream(x.device)), "xnc_layer_forward")
     return y
+
+
+def layer_forward_umma(x: torch.Tensor, filt: PackedFilters, pad: int, workspace: torch.Tensor,
+                       y: torch.Tensor | None = None, acc: torch.Tensor | None = None):
+    """K1 -> K2 -> tcgen05 K3+K4 in one C-ABI call (xnc_layer_forward_umma)."""
+    _need_cuda(x, "x", torch.float32)
+    N, C, H, W = x.shape
+    if C != filt.C:
+        raise ValueError(f"{C} input channels vs {filt.C} filter channels")
+    if filt.wq is None:
+        raise ValueError("layer_forward_umma needs attach_umma_weights() first")
+    oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    if y is None:
+        y = torch.empty((N, filt.O, oh, ow), dtype=torch.float32, device=x.device)
+    check(lib().xnc_layer_forward_umma(x.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(),
+                                       filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
+                                       workspace.data_ptr(), _ptr(y), _ptr(acc), _stream(x.device)),
+          "xnc_layer_forward_umma")
+    return y

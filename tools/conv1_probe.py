@@ -93,3 +93,28 @@ for name, fn in [("s2d_nchw", s2d_nchw), ("s2d_nhwc", s2d_nhwc), ("s2d_bf16_nhwc
     torch.cuda.synchronize()
     err = float((y.float() - ref).abs().max())
     print(json.dumps({"variant": name, "ms": round(s.elapsed_time(e) / 20, 4), "max_abs_diff_vs_nchw": err}))
+
+
+# space-to-depth straight into NHWC (one gather), conv/ReLU/pool in channels_last
+def s2d_direct_nhwc(contig=True):
+    xp = F.pad(x, (2, 2, 2, 2))                                   # [N, 3, 228, 228]
+    s = xp.view(256, 3, 57, 4, 57, 4).permute(0, 2, 4, 1, 3, 5).reshape(256, 57, 57, 48)
+    s = s.permute(0, 3, 1, 2)                                      # NCHW view, NHWC memory
+    h = F.conv2d(s, wsl, b)
+    h = F.max_pool2d(F.relu_(h), 3, 2)
+    return h.contiguous() if contig else h
+
+
+for name, fn in [("s2d_direct_nhwc", s2d_direct_nhwc), ("s2d_direct_nhwc_keep", lambda: s2d_direct_nhwc(False))]:
+    for _ in range(5):
+        y = fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(20):
+        y = fn()
+    e.record()
+    torch.cuda.synchronize()
+    err = float((y.float() - ref).abs().max())
+    print(json.dumps({"variant": name, "ms": round(s.elapsed_time(e) / 20, 4), "max_abs_diff_vs_nchw": err,
+                      "out_channels_last": bool(y.is_contiguous(memory_format=torch.channels_last))}))
