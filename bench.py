@@ -318,6 +318,35 @@ def run_ours(args, cfg_name):
            "ms_per_step": e2e_ms,
            "api": "XnorConv2d.forward(host tensor) -> pipelined H2D / K1-K4 / D2H on 3 streams"}
 
+    # ---- vanilla GPU row (Table 1): the same layer as a
+    # full-precision cuDNN conv2d (FP32 and TF32), inputs resident, same event protocol
+    def vanilla_ms(xv, wv, pad_v, tf32):
+        import torch.nn.functional as F
+        saved = (torch.backends.cudnn.allow_tf32, torch.backends.cudnn.benchmark)
+        torch.backends.cudnn.allow_tf32, torch.backends.cudnn.benchmark = tf32, True
+        try:
+            for _ in range(3):
+                F.conv2d(xv, wv, padding=pad_v)
+            torch.cuda.synchronize(dev)
+            a_v, b_v = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_v.record(stream)
+            for _ in range(5):
+                F.conv2d(xv, wv, padding=pad_v)
+            b_v.record(stream)
+            torch.cuda.synchronize(dev)
+            return a_v.elapsed_time(b_v) / 5
+        finally:
+            torch.backends.cudnn.allow_tf32, torch.backends.cudnn.benchmark = saved
+
+    vanilla = None
+    if not args.no_ksweep and cfg_name == "C3":
+        w_dev = w_host.to(dev)
+        fp32_ms, tf32_ms = vanilla_ms(x, w_dev, pad, False), vanilla_ms(x, w_dev, pad, True)
+        vanilla = {"what": "torch.nn.functional.conv2d (cuDNN), same x / w, float outputs, resident",
+                   "fp32_ms": fp32_ms, "tf32_ms": tf32_ms, "xnor_step_ms": ms_step,
+                   "speedup_vs_fp32": fp32_ms / ms_step, "speedup_vs_tf32": tf32_ms / ms_step}
+        del w_dev
+
     # ---- k-sweep (BASELINE config 2): GPU throughput per kernel size, same protocol
     ksweep = None
     if not args.no_ksweep and cfg_name == "C3":
@@ -338,8 +367,10 @@ def run_ours(args, cfg_name):
             b_ev.record(stream)
             torch.cuda.synchronize(dev)
             ms_k = a_ev.elapsed_time(b_ev) / reps
+            v32 = vanilla_ms(xk, lk.weight, (kk - 1) // 2, False)
             ksweep[kname] = {"k": kk, "ms_per_layer": ms_k,
-                             "gpu_Gbinop_s": binops(Nk, Ck, Hk, Wk, Ok, kk) / (ms_k * 1e-3) / 1e9}
+                             "gpu_Gbinop_s": binops(Nk, Ck, Hk, Wk, Ok, kk) / (ms_k * 1e-3) / 1e9,
+                             "vanilla_fp32_ms": v32, "speedup_vs_vanilla_fp32": v32 / ms_k}
             del xk, yk, lk
 
     result = None
@@ -393,6 +424,7 @@ def run_ours(args, cfg_name):
             "e2e": e2e,
             "clocks": clk.summary(),
             "ksweep": ksweep,
+            "vanilla_gpu": vanilla,
             "gpu": props.name,
         }
     if ws > 1:
