@@ -260,9 +260,12 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]
       : "r"(addr));
 }
 
+#ifndef XNC_ST_HINT
+#define XNC_ST_HINT ".cs"
+#endif
 // streaming (evict-first) store, predicated without a branch
 __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}" ::"l"(p),
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global" XNC_ST_HINT ".f32 [%0], %1;\n\t}" ::"l"(p),
                "f"(v), "r"((int)pred)
                : "memory");
 }
