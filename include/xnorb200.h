@@ -106,6 +106,16 @@ size_t xnc_umma_weight_bytes(int O, int C, int kh, int kw);
 int xnc_umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 int xnc_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw,
                           uint8_t* wq, int32_t* sw, void* stream);
+/* Optional per-channel affines (a bias or a folded batch norm, y' = (y * scale) +
+ * shift with one rounding per op): on the input of K1 before the sign and |.|
+ * (scale/shift f32 [C]), or on the output of the tcgen05 conv after alpha*K
+ * (f32 [O]; "optional bias/BN for the next binary layer").  Both NULL = none. */
+int xnc_pack_input_affine(const float* x, int N, int C, int H, int W, const float* in_scale,
+                          const float* in_shift, uint32_t* bits, float* A, void* stream);
+int xnc_xnor_conv_umma_affine(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
+                              const float* K, const float* alpha, int N, int C, int H, int W,
+                              int O, int kh, int kw, int pad, const float* out_scale,
+                              const float* out_shift, float* y, int32_t* acc, void* stream);
 /* Profiling only: per-CTA cycle counters of the last tcgen05 conv launched with
  * XNC_UMMA_DEBUG bit 7 set (16 u64 slots per CTA, host memory; blocking copy). */
 int xnc_umma_profile(unsigned long long* host_out, int n_ctas);

@@ -105,6 +105,24 @@ int xnc_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw
   return launch_pack_weights_umma(w, dtype, O, C, kh, kw, wq, sw, as_stream(stream));
 }
 
+int xnc_pack_input_affine(const float* x, int N, int C, int H, int W, const float* in_scale,
+                          const float* in_shift, uint32_t* bits, float* A, void* stream) {
+  if (!x || !bits || N < 1 || C < 1 || H < 1 || W < 1 || (!in_scale != !in_shift)) return XNC_EINVAL;
+  return launch_pack_input(x, N, C, H, W, bits, A, as_stream(stream), in_scale, in_shift);
+}
+
+int xnc_xnor_conv_umma_affine(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
+                              const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
+                              const float* out_scale, const float* out_shift, float* y, int32_t* acc,
+                              void* stream) {
+  if (!bits || !wq || !sw || O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return XNC_EINVAL;
+  if (!y && !acc) return XNC_EINVAL;
+  if (y && (!K || !alpha)) return XNC_EINVAL;
+  if (!out_scale != !out_shift) return XNC_EINVAL;
+  return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, acc, as_stream(stream),
+                          out_scale, out_shift);
+}
+
 int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                        const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                        float* y, int32_t* acc, void* stream) {

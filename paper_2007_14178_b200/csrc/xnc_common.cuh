@@ -33,7 +33,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Kernel launchers implemented in the per-kernel translation units.
 namespace xnc {
 int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
-                      cudaStream_t s);
+                      cudaStream_t s, const float* in_scale = nullptr, const float* in_shift = nullptr);
 int launch_pack_weights(const float* w, int O, int C, int kh, int kw, uint32_t* wbits,
                         float* alpha, double* alpha64, cudaStream_t s);
 int launch_pack_weights_f64(const double* w, int O, int C, int kh, int kw, uint32_t* wbits,
@@ -53,5 +53,6 @@ int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int
 int umma_profile_read(unsigned long long* host, int n_ctas);
 int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
-                     float* y, int32_t* acc, cudaStream_t s);
+                     float* y, int32_t* acc, cudaStream_t s, const float* out_scale = nullptr,
+                     const float* out_shift = nullptr);
 }  // namespace xnc

@@ -305,7 +305,8 @@ template <int MH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv_umma_pair(
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
-    const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out) {
+    const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out,
+    const float* __restrict__ out_scale, const float* __restrict__ out_shift) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
@@ -587,7 +588,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const int accv = swv[j] - 2 * (int)v[h][j];
-                st_cs_pred(yp + j * plane_out32, __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]), ok[h]);
+                float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
+                if (out_scale != nullptr)  // optional per-filter affine (bias / folded BN of the next layer)
+                  val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + obase + j)), __ldg(out_shift + obase + j));
+                st_cs_pred(yp + j * plane_out32, val, ok[h]);
               }
             }
             if (prof) w_st += clock64() - tc1;
@@ -602,7 +606,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
               if (o < g.O) {
                 const int accv = swv[j] - 2 * (int)v[h][j];
                 const size_t idx = pix[h] + (size_t)o * plane_out;
-                if (y) __stcs(y + idx, __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]));
+                if (y) {
+                  float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
+                  if (out_scale != nullptr)
+                    val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
+                  __stcs(y + idx, val);
+                }
                 if (acc_out) acc_out[idx] = accv;
               }
             }
@@ -769,7 +778,8 @@ int umma_profile_read(unsigned long long* host, int n_ctas) {
 
 int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
-                     float* y, int32_t* acc, cudaStream_t s) {
+                     float* y, int32_t* acc, cudaStream_t s, const float* out_scale,
+                     const float* out_shift) {
   PairGeom g;
   size_t smem;
   if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
@@ -804,7 +814,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
     attr = smem;
   }
-  kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc);
+  kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift);
   return launch_status();
 }
 

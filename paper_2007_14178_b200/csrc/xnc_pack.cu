@@ -40,7 +40,9 @@ __global__ void __launch_bounds__(THREADS) k_pack_input(const float* __restrict_
                                                              int Cw, float inv, long groups_per_img,
                                                              long total_groups,
                                                              uint32_t* __restrict__ bits,
-                                                             float* __restrict__ A) {
+                                                             float* __restrict__ A,
+                                                             const float* __restrict__ in_scale,
+                                                             const float* __restrict__ in_shift) {
   extern __shared__ uint4 pack_smem[];
   uint32_t* wtile = reinterpret_cast<uint32_t*>(pack_smem);
   constexpr int PIX = THREADS * VEC;          // pixels per block
@@ -71,6 +73,11 @@ __global__ void __launch_bounds__(THREADS) k_pack_input(const float* __restrict_
         } else {
 #pragma unroll
           for (int i = 0; i < VEC; ++i) v[i] = __ldcs(src + i);
+        }
+        if (in_scale != nullptr) {  // optional per-channel affine (folded BN) before sign and |.|
+          const float sc = __ldg(in_scale + 32 * j + cc), sh = __ldg(in_shift + 32 * j + cc);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) v[i] = __fadd_rn(__fmul_rn(v[i], sc), sh);
         }
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
@@ -111,8 +118,13 @@ __global__ void __launch_bounds__(THREADS) k_pack_input(const float* __restrict_
 // the words are built by one thread per (pixel, word) and A by one thread per
 // pixel (the channel sum must stay sequential for bit-exactness); x is read
 // twice, from L2 for these sizes.
+__device__ __forceinline__ float affine_in(float v, const float* sc, const float* sh, int c) {
+  return sc != nullptr ? __fadd_rn(__fmul_rn(v, __ldg(sc + c)), __ldg(sh + c)) : v;
+}
+
 __global__ void k_pack_words(const float* __restrict__ x, int C, int HW, int Cw, long npix,
-                             uint32_t* __restrict__ bits) {
+                             uint32_t* __restrict__ bits, const float* __restrict__ in_scale,
+                             const float* __restrict__ in_shift) {
   const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= npix * Cw) return;
   long q;
@@ -128,31 +140,33 @@ __global__ void k_pack_words(const float* __restrict__ x, int C, int HW, int Cw,
   const float* xp = x + (n * C + 32L * j) * HW + p;
   const int cend = min(32, C - 32 * j);
   uint32_t word = 0u;
-  for (int cc = 0; cc < cend; ++cc) word |= (__ldg(xp + (long)cc * HW) >= 0.0f ? 1u : 0u) << cc;
+  for (int cc = 0; cc < cend; ++cc)
+    word |= (affine_in(__ldg(xp + (long)cc * HW), in_scale, in_shift, 32 * j + cc) >= 0.0f ? 1u : 0u) << cc;
   bits[q * Cw + j] = word;
 }
 
 __global__ void k_absmean(const float* __restrict__ x, int C, int HW, long npix, float inv,
-                          float* __restrict__ A) {
+                          float* __restrict__ A, const float* __restrict__ in_scale,
+                          const float* __restrict__ in_shift) {
   const long q = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= npix) return;
   const long n = q / HW, p = q - n * HW;
   const float* xp = x + n * C * (long)HW + p;
   float s = 0.0f;
-  if (HW == 1 && (C & 3) == 0 && ((reinterpret_cast<uintptr_t>(xp) & 15) == 0)) {
+  if (HW == 1 && (C & 3) == 0 && ((reinterpret_cast<uintptr_t>(xp) & 15) == 0) && in_scale == nullptr) {
     for (int c = 0; c < C; c += 4) {  // channels contiguous: 16-byte loads, same sequential order
       const float4 v = __ldg(reinterpret_cast<const float4*>(xp + c));
       s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, fabsf(v.x)), fabsf(v.y)), fabsf(v.z)), fabsf(v.w));
     }
   } else {
 #pragma unroll 8
-    for (int c = 0; c < C; ++c) s = __fadd_rn(s, fabsf(__ldg(xp + (long)c * HW)));
+    for (int c = 0; c < C; ++c) s = __fadd_rn(s, fabsf(affine_in(__ldg(xp + (long)c * HW), in_scale, in_shift, c)));
   }
   A[q] = __fmul_rn(s, inv);
 }
 
 int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
-                      cudaStream_t s) {
+                      cudaStream_t s, const float* in_scale, const float* in_shift) {
   {
     const long npix = (long)N * H * W;
     const long vec_groups = (H * W) % 4 == 0 ? npix / 4 : npix;
@@ -160,8 +174,11 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
     if (vec_groups < 2L * 148 * 256 && C >= 256) {
       const int Cw = cdiv(C, 32);
       const long words = npix * Cw;
-      k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits);
-      if (A) k_absmean<<<(unsigned)cdivl(npix, 128), 128, 0, s>>>(x, C, H * W, npix, (float)(1.0 / (double)C), A);
+      k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, in_scale,
+                                                              in_shift);
+      if (A)
+        k_absmean<<<(unsigned)cdivl(npix, 128), 128, 0, s>>>(x, C, H * W, npix, (float)(1.0 / (double)C), A,
+                                                             in_scale, in_shift);
       return launch_status();
     }
   }
@@ -185,7 +202,7 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       o = smem;
     }
-    kern<<<blocks, t, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A);
+    kern<<<blocks, t, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, in_scale, in_shift);
   };
   if (vec4) {
     if (threads == 512) go(k_pack_input<4, 512>, 512);

@@ -25,7 +25,12 @@ def default_pad(kernel_h: int, kernel_w: int) -> int:
 class XnorConv2d:
     """Binary conv layer with packed weights resident on one device."""
 
-    def __init__(self, weight: torch.Tensor, pad: int | None = None, variant: str = "popc"):
+    def __init__(self, weight: torch.Tensor, pad: int | None = None, variant: str = "popc",
+                 in_affine=None, out_affine=None):
+        """in_affine = (scale, shift) f32 [C]: the layer binarizes x*scale + shift
+        (a folded batch norm in front of the sign, computed inside K1); out_affine =
+        (scale, shift) f32 [O]: y*scale + shift is written instead of y (the next
+        binary layer's batch norm, fused into the conv epilogue)."""
         if weight.dim() != 4:
             raise ValueError(f"weight must be [O, C, kh, kw], got {tuple(weight.shape)}")
         O, C, kh, kw = weight.shape
@@ -45,6 +50,11 @@ class XnorConv2d:
             raise ValueError(f"unknown variant {variant!r}")
         self.O, self.C, self.kh, self.kw = O, C, kh, kw
         self.variant = variant
+        dev = w.device
+        self.in_affine = None if in_affine is None else tuple(
+            t.detach().to(device=dev, dtype=torch.float32).contiguous() for t in in_affine)
+        self.out_affine = None if out_affine is None else tuple(
+            t.detach().to(device=dev, dtype=torch.float32).contiguous() for t in out_affine)
         self._ws: dict[tuple, torch.Tensor] = {}
 
     @property
@@ -89,14 +99,15 @@ class XnorConv2d:
         variant = self.kernel_for(x.shape)
         if variant in ("popc-fc", "umma-fc"):
             return self._forward_fc(x, out, want_acc, variant)
-        if variant == "popc" and not want_acc:
+        plain = self.in_affine is None and self.out_affine is None
+        if variant == "popc" and not want_acc and plain:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
-        if variant == "umma" and not want_acc:  # one C-ABI call: K1 -> K2 -> tcgen05 K3+K4
+        if variant == "umma" and not want_acc and plain:  # one C-ABI call: K1 -> K2 -> tcgen05 K3+K4
             return ops.layer_forward_umma(x, self.filters, self.pad, self.workspace(x), y=out)
-        bits, A = ops.pack_input(x)
+        bits, A = ops.pack_input(x, in_affine=self.in_affine)
         K = ops.scale_map(A, self.kh, self.kw, self.pad)
         y, acc = ops.xnor_conv(bits, self.filters, K, self.pad, want_acc=want_acc,
-                               variant=variant, y=out)
+                               variant=variant, y=out, out_affine=self.out_affine)
         return (y, acc) if want_acc else y
 
     def kernel_for(self, x_shape) -> str:
@@ -130,11 +141,11 @@ class XnorConv2d:
         arithmetic as the conv view: C' = kh*kw*C valid bits, K = box mean of A
         over the whole input, alpha per filter (the reference's (c, ky, kx) sum)."""
         N, C, H, W = x.shape
-        bits, A = ops.pack_input(x)
+        bits, A = ops.pack_input(x, in_affine=self.in_affine)
         K = ops.scale_map(A, self.kh, self.kw, 0)                     # [N, 1, 1]
         fcf = self._fc_filters(umma=variant == "umma-fc")
         y1, acc1 = ops.xnor_conv(bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,
-                                 want_acc=want_acc,
+                                 want_acc=want_acc, out_affine=self.out_affine,
                                  variant="umma" if variant == "umma-fc" else "popc")  # [1, O, 1, N]
         y = y1.view(self.O, N).t().reshape(N, self.O, 1, 1)
         if out is not None:

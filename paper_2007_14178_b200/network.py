@@ -8,13 +8,13 @@ path:
 
     conv1  11x11/4, 3 -> 96      full precision      224 -> 55  (as 3x3 over 4x4 space-to-depth)
     pool   3/2                                       55 -> 27
-    conv2  5x5 pad 2, 96 -> 256  BINARY (XnorConv2d) 27
+    bn2 -> conv2  5x5 pad 2, 96 -> 256  BINARY (XnorConv2d) 27
     pool   3/2                                       27 -> 13
-    conv3  3x3 pad 1, 256 -> 384 BINARY              13
-    conv4  3x3 pad 1, 384 -> 384 BINARY              13
+    bn3 -> conv3  3x3 pad 1, 256 -> 384 BINARY       13  (epilogue applies bn4)
+    conv4  3x3 pad 1, 384 -> 384 BINARY              13  (epilogue applies bn5)
     conv5  3x3 pad 1, 384 -> 256 BINARY              13
     pool   3/2                                       13 -> 6
-    fc6    6x6 valid, 256 -> 4096 BINARY (a k = H = W conv)  1x1
+    bn6 -> fc6  6x6 valid, 256 -> 4096 BINARY (a k = H = W conv)  1x1  (epilogue applies bn7)
     fc7    1x1, 4096 -> 4096     BINARY              1x1
     fc8    4096 -> 1000          full precision
 
@@ -80,9 +80,28 @@ class XnorNetAlexNet:
         w12 = F.pad(self.conv1_w, (0, 1, 0, 1))
         self.conv1_w_s2d = (w12.view(96, 3, 3, 4, 3, 4).permute(0, 1, 3, 5, 2, 4)
                             .reshape(96, 48, 3, 3).contiguous())
+        # XNOR-Net's binary block is BatchNorm -> BinActiv -> BinConv (-> Pool); the
+        # batch norms are folded to a per-channel affine (scale, shift), random-init
+        # like everything else.  After a pool it runs inside K1 of the next layer
+        # (in_affine); between two binary layers it is fused into the first layer's
+        # conv epilogue (out_affine), so the stored feature map is already normalised.
+        def bn(c, center):
+            gamma = 0.8 + 0.4 * torch.rand(c, generator=g)
+            beta = 0.2 * torch.rand(c, generator=g) - 0.1
+            mean = center * torch.rand(c, generator=g)
+            var = 0.5 + torch.rand(c, generator=g)
+            scale = gamma / torch.sqrt(var + 1e-5)
+            return scale.to(dev), (beta - mean * scale).to(dev)
+
+        self.bn = {"conv2": bn(96, 0.6), "conv3": bn(256, 0.5), "conv4": bn(384, 0.2),
+                   "conv5": bn(384, 0.2), "fc6": bn(256, 0.3), "fc7": bn(4096, 0.2)}
+        fused_out = {"conv3": "conv4", "conv4": "conv5", "fc6": "fc7"}  # BN of the next layer
         self.binary: dict[str, XnorConv2d] = {}
         for name, cin, cout, k, pad in BINARY_LAYERS:
-            self.binary[name] = XnorConv2d(rnd(cout, cin, k, k), pad=pad, variant=variant)
+            in_aff = None if name in fused_out.values() else self.bn[name]
+            out_aff = self.bn[fused_out[name]] if name in fused_out else None
+            self.binary[name] = XnorConv2d(rnd(cout, cin, k, k), pad=pad, variant=variant,
+                                           in_affine=in_aff, out_affine=out_aff)
         self.fc8_w = rnd(num_classes, 4096, scale=4096 ** -0.5)
         self.fc8_b = rnd(num_classes, scale=0.1)
 
@@ -96,11 +115,14 @@ class XnorNetAlexNet:
         with _tf32_full_precision_layers():
             return self._forward(x, return_features)
 
+    @torch.no_grad()
     def front_end(self, x: torch.Tensor) -> torch.Tensor:
         """conv1 (11x11, stride 4, pad 2; full precision, via space-to-depth) -> ReLU
-        -> max-pool 3/2: the input of the first binary layer."""
-        h = F.conv2d(F.pixel_unshuffle(F.pad(x, (2, 2, 2, 2)), 4), self.conv1_w_s2d, self.conv1_b)
-        return F.max_pool2d(F.relu_(h), 3, 2)
+        -> max-pool 3/2: the input of the first binary layer (the same cuDNN
+        settings as inside forward())."""
+        with _tf32_full_precision_layers():
+            h = F.conv2d(F.pixel_unshuffle(F.pad(x, (2, 2, 2, 2)), 4), self.conv1_w_s2d, self.conv1_b)
+            return F.max_pool2d(F.relu_(h), 3, 2)
 
     def _forward(self, x: torch.Tensor, return_features: bool):
         h = self.front_end(x)

@@ -42,14 +42,34 @@ def words(c: int) -> int:
     return (c + 31) // 32
 
 
-def pack_input(x: torch.Tensor, want_A: bool = True):
-    """K1: x f32 [N,C,H,W] -> (bits i32 [N,H,W,Cw] (u32 payload), A f32 [N,H,W])."""
+def _affine(aff, n: int, device, what: str):
+    """(scale, shift) f32 [n] device tensors, or (None, None)."""
+    if aff is None:
+        return None, None
+    sc, sh = aff
+    for t, nm in ((sc, "scale"), (sh, "shift")):
+        _need_cuda(t, f"{what} {nm}", torch.float32)
+        if t.numel() != n or not t.is_contiguous():
+            raise ValueError(f"{what} {nm} must be a contiguous f32 vector of {n}")
+    return sc, sh
+
+
+def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None):
+    """K1: x f32 [N,C,H,W] -> (bits i32 [N,H,W,Cw] (u32 payload), A f32 [N,H,W]).
+
+    in_affine = (scale, shift) f32 [C]: binarize and average x*scale + shift (one
+    rounding per op) instead of x -- a folded batch norm before the sign."""
     _need_cuda(x, "x", torch.float32)
     N, C, H, W = x.shape
     bits = torch.empty((N, H, W, words(C)), dtype=torch.int32, device=x.device)
     A = torch.empty((N, H, W), dtype=torch.float32, device=x.device) if want_A else None
-    check(lib().xnc_pack_input(x.data_ptr(), N, C, H, W, bits.data_ptr(), _ptr(A), _stream(x.device)),
-          "xnc_pack_input")
+    sc, sh = _affine(in_affine, C, x.device, "in_affine")
+    if sc is None:
+        check(lib().xnc_pack_input(x.data_ptr(), N, C, H, W, bits.data_ptr(), _ptr(A), _stream(x.device)),
+              "xnc_pack_input")
+    else:
+        check(lib().xnc_pack_input_affine(x.data_ptr(), N, C, H, W, sc.data_ptr(), sh.data_ptr(),
+                                          bits.data_ptr(), _ptr(A), _stream(x.device)), "xnc_pack_input_affine")
     return bits, A
 
 
@@ -141,7 +161,7 @@ VARIANTS = {"popc": 0, "b1mma": 1, "umma": 2}
 def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, pad: int,
               C: int | None = None, want_y: bool = True, want_acc: bool = False,
               variant: str = "popc", y: torch.Tensor | None = None,
-              acc: torch.Tensor | None = None, W: int | None = None):
+              acc: torch.Tensor | None = None, W: int | None = None, out_affine=None):
     """K3+K4: (y f32 [N,O,H',W'] or None, acc i32 [N,O,H',W'] or None).
 
     Every variant reads the packed bits `bits` (i32 [N,H,W,Cw], from pack_input)."""
@@ -165,14 +185,19 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
     if variant == "umma":
         if filt.wq is None:
             raise ValueError("umma variant needs attach_umma_weights() first")
-        check(lib().xnc_xnor_conv_umma(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), _ptr(K),
-                                       filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
-                                       _ptr(y), _ptr(acc), _stream(dev)), "xnc_xnor_conv_umma")
+        osc, osh = _affine(out_affine, filt.O, dev, "out_affine")
+        check(lib().xnc_xnor_conv_umma_affine(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), _ptr(K),
+                                              filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
+                                              _ptr(osc), _ptr(osh), _ptr(y), _ptr(acc), _stream(dev)),
+              "xnc_xnor_conv_umma")
     else:
         check(lib().xnc_xnor_conv_variant(VARIANTS[variant], bits.data_ptr(), filt.wbits.data_ptr(),
                                           _ptr(K), filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh,
                                           filt.kw, pad, _ptr(y), _ptr(acc), _stream(dev)),
               "xnc_xnor_conv")
+        if out_affine is not None and y is not None:  # same two roundings as the fused epilogue
+            osc, osh = _affine(out_affine, filt.O, dev, "out_affine")
+            y.mul_(osc.view(1, -1, 1, 1)).add_(osh.view(1, -1, 1, 1))
     return y, acc
 
 

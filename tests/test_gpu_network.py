@@ -35,10 +35,18 @@ def test_network_binary_layers_match_oracle():
             h = F.max_pool2d(h, 3, 2)
     for name, cin, cout, k, pad in BINARY_LAYERS:
         layer = net.binary[name]
-        xi = inputs[name][:2].contiguous().cpu().numpy()
+        xin = inputs[name][:2].contiguous()
+        if layer.in_affine is not None:  # the folded BN K1 applies: x*scale + shift, two roundings
+            sc, sh = layer.in_affine
+            xin = xin * sc.view(1, -1, 1, 1) + sh.view(1, -1, 1, 1)
+        xi = xin.cpu().numpy()
         o_idx = [0, cout // 2, cout - 1]
         wi = layer.weight[o_idx].cpu().numpy()
         want = O.conv_layer(xi, wi, pad)
+        if layer.out_affine is not None:  # the next layer's BN, fused into this epilogue
+            sc, sh = (t[o_idx].cpu().numpy() for t in layer.out_affine)
+            want = (want * sc.reshape(1, -1, 1, 1)).astype(np.float32)
+            want = (want + sh.reshape(1, -1, 1, 1)).astype(np.float32)
         got = feats[name][:2][:, o_idx].cpu().numpy()
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), name
 

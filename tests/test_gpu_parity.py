@@ -269,3 +269,31 @@ def test_pack_paths_large_and_small(N, C, H, W):
         s = (s + np.abs(x[:, c])).astype(np.float32)
     want = (s * np.float32(1.0 / C)).astype(np.float32)
     assert np.array_equal(A.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("variant", ["umma", "popc"])
+@pytest.mark.parametrize("shape", [(2, 64, 12, 12, 48, 3, 3, 1), (3, 200, 9, 9, 256, 3, 3, 1),
+                                   (2, 96, 13, 13, 384, 5, 5, 2)], ids=lambda s: "x".join(map(str, s)))
+def test_bn_affines_in_k1_and_epilogue(shape, variant):
+    """Folded batch norms: in_affine inside K1 (binarize / average x*s + b) and
+    out_affine in the conv epilogue (write y*s + b); parity against the oracle on
+    the materialised affine input, bit-exact floats."""
+    from paper_2007_14178_b200 import XnorConv2d, ops
+    N, C, H, W, Oc, kh, kw, pad = shape
+    if variant == "umma" and not ops.umma_supported(N, C, H, W, Oc, kh, kw, pad):
+        pytest.skip("shape outside the tcgen05 kernel's smem plan")
+    rng = np.random.default_rng(list(shape) + [7])
+    x = O.f32_exact(rng, (N, C, H, W))
+    w = O.f32_exact(rng, (Oc, C, kh, kw))
+    isc, ish = rng.uniform(0.5, 1.5, C).astype(np.float32), rng.uniform(-0.3, 0.3, C).astype(np.float32)
+    osc, osh = rng.uniform(0.5, 1.5, Oc).astype(np.float32), rng.uniform(-0.3, 0.3, Oc).astype(np.float32)
+    dev = _dev()
+    t = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+    layer = XnorConv2d(t(w), pad=pad, variant=variant, in_affine=(t(isc), t(ish)),
+                       out_affine=(t(osc), t(osh)))
+    y = layer.forward(t(x)).cpu().numpy()
+    xa = ((x * isc.reshape(1, -1, 1, 1)).astype(np.float32) + ish.reshape(1, -1, 1, 1)).astype(np.float32)
+    want = O.conv_layer(xa, w, pad)
+    want = ((want * osc.reshape(1, -1, 1, 1)).astype(np.float32) + osh.reshape(1, -1, 1, 1)).astype(np.float32)
+    assert np.array_equal(y.view(np.uint32), want.view(np.uint32))
+
