@@ -277,6 +277,8 @@ struct PairGeom {
   int P;             // extended pixel rows one K-block plane holds
   int plane_bytes;   // one K-block plane (1024-aligned)
   int NA;            // A plane ring slots (KBn, or 2*KBn: next tile's planes built during this tile)
+  int a_unit;        // 1: NA == 2*KBn and the A protocol runs per unit (one wait + one commit for
+                     // all KBn planes of a unit), 0: per plane through the ring
   int n_mt;          // pair tiles per image
   int n_nb;          // filter blocks
   int tiles;         // N * n_mt
@@ -322,7 +324,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   if (tid == 0) {
     for (int s = 0; s < kPStages; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
-    for (int k = 0; k < kPMaxA; ++k) { mbar_init(&a_full[k], 2 * kPAWarps); mbar_init(&a_empty[k], 1); }
+    for (int k = 0; k < kPMaxA; ++k) {
+      mbar_init(&a_full[k], 2 * kPAWarps * (g.a_unit ? g.KBn : 1));
+      mbar_init(&a_empty[k], 1);
+    }
     for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], 2 * kPEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -387,8 +392,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
       for (int kb = 0; kb < g.KBn; ++kb) {
         const uint32_t use = it * g.KBn + kb, sl = use % g.NA;  // ring slot of this plane
-        if (use >= (uint32_t)g.NA) {
-          if (lane == 0) mbar_wait_prof(&a_empty[sl], ((use / g.NA) - 1) & 1, prof, w_ae, XNC_PROD_HINT);
+        // barrier guarding the slot: per unit (group it & 1) or per plane
+        const uint32_t ab = g.a_unit ? (it & 1) : sl;
+        const bool wait_empty = g.a_unit ? (kb == 0 && it >= 2) : use >= (uint32_t)g.NA;
+        const uint32_t e_par = g.a_unit ? (((it >> 1) - 1) & 1) : (((use / g.NA) - 1) & 1);
+        if (wait_empty) {
+          if (lane == 0) mbar_wait_prof(&a_empty[ab], e_par, prof, w_ae, XNC_PROD_HINT);
           __syncwarp();
         }
         if (!((g.debug & 4) && use >= (uint32_t)g.NA)) {  // bit 2 (profiling): planes built once
@@ -431,7 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(full0 + sl * 8);
+        if (lane == 0) mbar_arrive_cluster(full0 + ab * 8);
       }
     }
     if (prof) g_umma_prof[blockIdx.x][8] = w_ae;
@@ -463,8 +472,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
           uint32_t acc = 0;
           for (int kb = 0; kb < g.KBn; ++kb) {
             const uint32_t use = item * g.KBn + kb, sl = use % g.NA;
-            mbar_wait_prof(&a_full[sl], (use / g.NA) & 1, prof, w_af);
-            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (!g.a_unit || kb == 0) {
+              mbar_wait_prof(&a_full[g.a_unit ? (item & 1) : sl],
+                             g.a_unit ? ((item >> 1) & 1) : ((use / g.NA) & 1), prof, w_af);
+              asm volatile("tcgen05.fence::after_thread_sync;");
+            }
             const uint64_t a_kb = a_desc0 + sl * plane16;
             for (int ky = 0; ky < g.kh; ++ky) {
               for (int kx = 0; kx < g.kw; ++kx, ++step) {
@@ -494,7 +506,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
                 if (b_proto && (j == kPCPS - 1 || step + 1 == total)) umma_commit_pair_elect(&b_empty[st]);
               }
             }
-            umma_commit_pair_elect(&a_empty[sl]);
+            if (!g.a_unit) umma_commit_pair_elect(&a_empty[sl]);
+            else if (kb == g.KBn - 1) umma_commit_pair_elect(&a_empty[item & 1]);
           }
           umma_commit_pair_elect(&t_full[buf]);
         }
@@ -736,6 +749,11 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   g.NA = 2 * g.KBn < kPMaxA ? 2 * g.KBn : kPMaxA;
   while (g.NA > 1 && (size_t)g.NA * g.plane_bytes + b_bytes > 225 * 1024) --g.NA;
   smem = (size_t)g.NA * g.plane_bytes + b_bytes;
+#ifdef XNC_A_PER_PLANE
+  g.a_unit = 0;
+#else
+  g.a_unit = g.NA == 2 * g.KBn;
+#endif
   return cols <= 512 && smem <= 225 * 1024 && (long)g.units < 0x7fffffffL &&
          (long)g.n_nb * g.NP * g.oh * g.ow < 0x7fffffffL;
 }
