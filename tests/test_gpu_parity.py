@@ -134,7 +134,15 @@ def test_b1mma_variant_vs_oracle(shape):
 
 UMMA_CASES = RANDOM_CASES + [(2, 256, 14, 14, 64, 3, 3, 1), (1, 128, 20, 20, 300, 3, 3, 1),
                              (2, 384, 13, 13, 40, 3, 3, 1), (1, 64, 27, 27, 16, 5, 5, 2),
-                             (1, 256, 9, 9, 256, 3, 3, 1)]
+                             (1, 256, 9, 9, 256, 3, 3, 1),
+                             # pair-kernel corners: 4 and 5 K blocks (C = 512 / 520, the ring
+                             # streams when the double-buffered planes do not fit), O = 512
+                             # (two 256-wide blocks), odd O / N, a single pixel row, 8x8 taps,
+                             # pad larger than the kernel reach, one image much smaller than a tile
+                             (2, 512, 10, 10, 96, 3, 3, 1), (1, 520, 7, 7, 20, 3, 3, 1),
+                             (3, 64, 9, 9, 512, 3, 3, 1), (5, 40, 11, 7, 77, 2, 3, 1),
+                             (4, 32, 1, 200, 24, 1, 5, 0), (1, 48, 12, 12, 16, 8, 8, 3),
+                             (2, 32, 5, 5, 32, 3, 3, 4), (7, 64, 3, 3, 192, 3, 3, 1)]
 
 
 @pytest.mark.parametrize("shape", UMMA_CASES, ids=lambda s: "x".join(map(str, s)))
