@@ -498,7 +498,8 @@ def run_network(args, cfg_name):
         res = {"metric": METRIC, "value": bops / (ms * 1e-3) / 1e9, "unit": "Gbinop/s", "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                "scaling": "strong" if cfg_name == "C5" else "weak", "vs_baseline": None,
-               "dtype": "1-bit signs (binary layers), f32 conv1/fc8", "data": "synthetic U(-1,1), random-init weights",
+               "dtype": "1-bit signs (binary layers); conv1 / fc8 full precision on cuDNN / cuBLAS with TF32",
+               "data": "synthetic U(-1,1), random-init weights",
                "config": {"workload": CONFIG_TEXT[cfg_name], "name": cfg_name, "global_batch": gb,
                           "batch_per_gpu": N, "variant": args.variant,
                           "binary_kernels": net.binary_kernels(N),
@@ -514,6 +515,30 @@ def run_network(args, cfg_name):
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return res
+
+
+def network_summary(variant="auto", batch=256, steps=5, warmup=3):
+    """A short XNOR-Net AlexNet forward timing (BASELINE config 4) for the default
+    bench line: images/s at batch 256 on this GPU, inputs resident."""
+    import torch
+    from paper_2007_14178_b200.network import BINARY_MACS_PER_IMAGE, XnorNetAlexNet
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator().manual_seed(11)
+    x = ((torch.rand((batch, 3, 224, 224), generator=g) * 2 - 1)).to(dev)
+    net = XnorNetAlexNet(dev, seed=7, variant=variant)
+    for _ in range(warmup):
+        net(x)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        net(x)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    return {"workload": CONFIG_TEXT["C4"], "ms_per_step": ms, "images_per_s": batch / (ms * 1e-3),
+            "Gbinop_s": 2.0 * BINARY_MACS_PER_IMAGE * batch / (ms * 1e-3) / 1e9,
+            "binary_kernels": net.binary_kernels(batch), "note": "full numbers: bench.py --config C4"}
 
 
 def cpu_baseline_fields(cfg_name, budget_s, ksweep=None):
@@ -590,6 +615,8 @@ def main():
     else:
         res = run_ours(args, args.config)
         ws, rank, _ = dist_env()
+        if res is not None and rank == 0 and ws == 1 and not args.no_ksweep:
+            res["network_C4"] = network_summary(args.variant)
         if res is not None and rank == 0 and ws == 1 and not args.no_cpu:
             try:
                 res["cpu_baseline"] = cpu_baseline_fields(args.config, args.cpu_budget, res.get("ksweep"))
