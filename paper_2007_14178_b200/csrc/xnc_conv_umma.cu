@@ -231,6 +231,39 @@ __device__ __forceinline__ void umma_i8_pair_elect(uint32_t tmem_d, uint64_t ade
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// One chunk (a 128-byte K row = four K=32 steps) of MMAs for MH row blocks,
+// issued by one elected lane of the converged issuer warp inside ONE asm block:
+// descriptors arrive as 32-bit low words (the start-address field; the high
+// word is shared), so per chunk the issuer runs a handful of uniform-datapath
+// instructions instead of ~100 (an elect, R2URs and 64-bit adds per MMA).  The
+// issuer shares its SM sub-partition with four busy epilogue warps; every
+// instruction it saves is issue latency the tensor pipe does not wait on.
+#define XNC_MMA1(D, AO, BO, P)                                                              \
+  "add.u32 al, %1, " #AO ";\n\tadd.u32 bl, %2, " #BO ";\n\tmov.b64 a, {al, %5};\n\t"   \
+  "mov.b64 b, {bl, %5};\n\t@e tcgen05.mma.cta_group::2.kind::i8 [" D "], a, b, %3, " P ";\n\t"
+template <int MH>
+__device__ __forceinline__ void umma_chunk_pair(uint32_t d0, int np, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
+                                                uint32_t idesc, uint32_t acc) {
+  if constexpr (MH == 1) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
+        XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%0", 2, 2, "t") XNC_MMA1("%0", 4, 4, "t") XNC_MMA1("%0", 6, 6, "t")
+        "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi));
+  } else {
+    const uint32_t d1 = d0 + (uint32_t)np;
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
+        XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%6", 1024, 0, "p")
+        XNC_MMA1("%0", 2, 2, "t") XNC_MMA1("%6", 1026, 2, "t")
+        XNC_MMA1("%0", 4, 4, "t") XNC_MMA1("%6", 1028, 4, "t")
+        XNC_MMA1("%0", 6, 6, "t") XNC_MMA1("%6", 1030, 6, "t")
+        "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(d1));
+  }
+}
+#undef XNC_MMA1
+
 __device__ __forceinline__ void umma_commit_pair_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -303,7 +336,7 @@ __device__ __forceinline__ uint4 d_bytes16(uint32_t bits16, uint32_t valid16) {
 
 // MH = M=128 row blocks per CTA (pair tile = 2*MH*128 extended pixels); the two
 // TMEM accumulators hold MH x NP columns each (MH * NP <= 256).
-template <int MH>
+template <int MH, bool PROF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv_umma_pair(
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
@@ -318,6 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
   __shared__ __align__(8) uint64_t t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base_s;
 
+  const int dbg = PROF ? g.debug : 0;  // profiling switches compile away in the production kernel
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -348,7 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     // ================= B producer: this CTA's NP/2 filter rows of every chunk,
     // kPCPS chunks per stage (one full barrier per stage)
     if (lane == 0) {
-      const bool prof = g.debug & 128;
+      const bool prof = dbg & 128;
       unsigned long long w_be = 0;
       const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
       const int my_units = (g.units - cluster + n_clusters - 1) / n_clusters;
@@ -362,8 +396,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
               if (j == 0) {
                 if (sidx >= kPStages) mbar_wait_prof(&b_empty[st], ((sidx / kPStages) - 1) & 1, prof, w_be, XNC_PROD_HINT);
                 const uint32_t n_in = min((uint32_t)kPCPS, total - step);
-                if ((g.debug & 256) && sidx >= kPStages) break;  // profiling: no B protocol after the fill
-                if ((g.debug & 2) && sidx >= kPStages) {  // profiling: reuse resident chunks, no traffic
+                if ((dbg & 256) && sidx >= kPStages) break;  // profiling: no B protocol after the fill
+                if ((dbg & 2) && sidx >= kPStages) {  // profiling: reuse resident chunks, no traffic
                   if (leader) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&b_full[st])) : "memory");
                   step += kPCPS - 1 - j;
                   tap += kPCPS - 1;
@@ -380,67 +414,103 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
   } else if (warp >= kPAWarp0 && warp < kPAWarp0 + kPAWarps) {
     // ================= A producers: packed bits -> swizzled d-bytes, per K block
     const int pt = tid - kPAWarp0 * 32, n_pt = kPAWarps * 32;
-    const bool prof = (g.debug & 128) && pt == 0;
+    const bool prof = (dbg & 128) && pt == 0;
     unsigned long long w_ae = 0;
     const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
     const bool vec4 = (g.Cw & 3) == 0 && (reinterpret_cast<uintptr_t>(bits) & 15) == 0;
+    // A planes are released in groups: all KBn planes of a unit at once (a_unit)
+    // or one plane at a time through the ring.  Within a group the loads of up to
+    // two planes x kAR rows per thread are all issued before any expansion, so a
+    // thread has up to 2*kAR 16-byte loads in flight instead of one: under the
+    // epilogue's store stream the L2 latency of the bit rows grows, and a
+    // one-load-at-a-time loop left the issuer waiting on a_full.
+    constexpr int kAR = 4;
+    const int grp = g.a_unit ? g.KBn : 1;
     uint32_t it = 0;  // units of this pair so far: every unit builds its KBn planes
     for (int u = cluster; u < g.units; u += n_clusters, ++it) {
       const int t = u / g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
       const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
-      for (int kb = 0; kb < g.KBn; ++kb) {
-        const uint32_t use = it * g.KBn + kb, sl = use % g.NA;  // ring slot of this plane
-        // barrier guarding the slot: per unit (group it & 1) or per plane
-        const uint32_t ab = g.a_unit ? (it & 1) : sl;
-        const bool wait_empty = g.a_unit ? (kb == 0 && it >= 2) : use >= (uint32_t)g.NA;
-        const uint32_t e_par = g.a_unit ? (((it >> 1) - 1) & 1) : (((use / g.NA) - 1) & 1);
+      for (int kb0 = 0; kb0 < g.KBn; kb0 += grp) {
+        const uint32_t use0 = it * g.KBn + kb0;
+        // barrier guarding the group's slots: per unit (group it & 1) or per plane
+        const uint32_t ab = g.a_unit ? (it & 1) : use0 % g.NA;
+        const bool wait_empty = g.a_unit ? it >= 2 : use0 >= (uint32_t)g.NA;
+        const uint32_t e_par = g.a_unit ? (((it >> 1) - 1) & 1) : (((use0 / g.NA) - 1) & 1);
         if (wait_empty) {
           if (lane == 0) mbar_wait_prof(&a_empty[ab], e_par, prof, w_ae, XNC_PROD_HINT);
           __syncwarp();
         }
-        if (!((g.debug & 4) && use >= (uint32_t)g.NA)) {  // bit 2 (profiling): planes built once
-          uint8_t* plane = a_s + (size_t)sl * g.plane_bytes;
-          // valid-channel masks of the block's four words
-          uint32_t vmask[4];
+        if (!((dbg & 4) && use0 >= (uint32_t)g.NA)) {  // bit 2 (profiling): planes built once
+          for (int kp = 0; kp < grp; kp += 2) {
+            const int kbA = kb0 + kp;
+            const bool two = kp + 1 < grp;
+            uint8_t* planes[2];
+            uint32_t vmask[2][4];  // valid-channel masks of each block's four words
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int rem = g.C - (kb * 128 + w * 32);
-            vmask[w] = rem >= 32 ? 0xFFFFFFFFu : rem <= 0 ? 0u : ((1u << rem) - 1u);
-          }
-          for (int p = pt; p < g.P; p += n_pt) {
-            const int e = m0 + p;
-            const int pr = e / g.IC, pc = e - pr * g.IC;
-            const int r = pr - g.pad, c = pc - g.pad;
-            uint32_t wd[4] = {0u, 0u, 0u, 0u};
-            uint32_t vm[4] = {0u, 0u, 0u, 0u};  // padding pixel: all d = 0
-            if (r >= 0 && r < g.H && c >= 0 && c < g.W) {
-              const uint32_t* src = img + ((size_t)r * g.W + c) * g.Cw + kb * 4;
-              if (vec4) {
-                const uint4 q = __ldg(reinterpret_cast<const uint4*>(src));
-                wd[0] = q.x; wd[1] = q.y; wd[2] = q.z; wd[3] = q.w;
-              } else {
+            for (int k = 0; k < 2; ++k) {
+              planes[k] = a_s + (size_t)((use0 + kp + k) % g.NA) * g.plane_bytes;
 #pragma unroll
-                for (int w = 0; w < 4; ++w)
-                  if (kb * 4 + w < g.Cw) wd[w] = __ldg(src + w);
+              for (int w = 0; w < 4; ++w) {
+                const int rem = g.C - ((kbA + k) * 128 + w * 32);
+                vmask[k][w] = rem >= 32 ? 0xFFFFFFFFu : rem <= 0 ? 0u : ((1u << rem) - 1u);
+              }
+            }
+            for (int r0 = 0; r0 < g.P; r0 += n_pt * kAR) {
+              uint4 q[2][kAR];
+              bool in_img[kAR];
+#pragma unroll
+              for (int i = 0; i < kAR; ++i) {
+                const int p = r0 + pt + i * n_pt;
+                const int e = m0 + p;
+                const int pr = e / g.IC, pc = e - pr * g.IC;
+                const int r = pr - g.pad, c = pc - g.pad;
+                in_img[i] = p < g.P && r >= 0 && r < g.H && c >= 0 && c < g.W;
+                const uint32_t* src = img + ((size_t)(in_img[i] ? r : 0) * g.W + (in_img[i] ? c : 0)) * g.Cw;
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                  q[k][i] = make_uint4(0u, 0u, 0u, 0u);
+                  if (in_img[i] && (k == 0 || two)) {
+                    const uint32_t* sk = src + (kbA + k) * 4;
+                    if (vec4) {
+                      q[k][i] = __ldg(reinterpret_cast<const uint4*>(sk));
+                    } else {
+                      const int wl = g.Cw - (kbA + k) * 4;  // words of this block present
+                      q[k][i].x = __ldg(sk);
+                      if (wl > 1) q[k][i].y = __ldg(sk + 1);
+                      if (wl > 2) q[k][i].z = __ldg(sk + 2);
+                      if (wl > 3) q[k][i].w = __ldg(sk + 3);
+                    }
+                  }
+                }
               }
 #pragma unroll
-              for (int w = 0; w < 4; ++w) vm[w] = vmask[w];
-            }
-            uint8_t* row = plane + (size_t)p * 128;
+              for (int i = 0; i < kAR; ++i) {
+                const int p = r0 + pt + i * n_pt;
+                if (p >= g.P) continue;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const uint32_t b16 = (wd[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu;
-              const uint32_t v16 = (vm[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu;
-              *reinterpret_cast<uint4*>(row + ((q ^ (p & 7)) << 4)) = d_bytes16(b16, v16);
+                for (int k = 0; k < 2; ++k) {
+                  if (k == 1 && !two) continue;
+                  const uint32_t wd[4] = {q[k][i].x, q[k][i].y, q[k][i].z, q[k][i].w};
+                  uint8_t* row = planes[k] + (size_t)p * 128;
+#pragma unroll
+                  for (int h = 0; h < 8; ++h) {
+                    const uint32_t b16 = (wd[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
+                    // padding pixel: all d = 0
+                    const uint32_t v16 = in_img[i] ? (vmask[k][h >> 1] >> ((h & 1) * 16)) & 0xFFFFu : 0u;
+                    *reinterpret_cast<uint4*>(row + ((h ^ (p & 7)) << 4)) = d_bytes16(b16, v16);
+                  }
+                }
+              }
             }
           }
           // generic-proxy smem writes -> visible to the tensor core (async proxy)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(full0 + ab * 8);
+        if (lane == 0)
+          for (int k = 0; k < grp; ++k) mbar_arrive_cluster(full0 + ab * 8);
       }
     }
     if (prof) g_umma_prof[blockIdx.x][8] = w_ae;
@@ -451,66 +521,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     if (leader) {  // the whole warp runs the loop; one elected lane issues
       const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(g.NP >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
+      // descriptors as (low word, high word): only the start-address field in the
+      // low word moves, so the loop runs on 32-bit values
       const uint64_t a_desc0 = umma_desc_sw128(smem_addr(a_s));
       const uint64_t b_desc0 = umma_desc_sw128(smem_addr(b_s));
+      const uint32_t a_lo0 = (uint32_t)a_desc0, hi = (uint32_t)(a_desc0 >> 32);
+      const uint32_t b_lo0 = (uint32_t)b_desc0;
       const uint32_t plane16 = (uint32_t)g.plane_bytes >> 4, b16 = g.b_half_bytes >> 4;
-      const bool prof = (g.debug & 128) && lane == 0;
-      const bool trace = (g.debug & 64) && blockIdx.x == 0 && lane == 0;
+      const uint32_t row_skip = (uint32_t)(g.IC - g.kw + 1) * 8u;  // next tap row, in descriptor units
+      const bool prof = PROF && (dbg & 128) && lane == 0;
+      const bool trace = PROF && (dbg & 64) && blockIdx.x == 0 && lane == 0;
       const int my_units = (g.units - cluster + n_clusters - 1) / n_clusters;
-      const uint32_t total = (uint32_t)my_units * g.KBn * g.taps;
+      uint32_t left = (uint32_t)my_units * g.KBn * g.taps;  // chunks still to issue
       unsigned long long w_te = 0, w_af = 0, w_bf = 0, n_mma = 0;
-      const unsigned long long t_start = clock64();
-      uint32_t step = 0, item = 0;
+      const unsigned long long t_start = PROF ? clock64() : 0ull;
+      uint32_t j = 0, st = 0, ph = 0, stages = 0, step = 0;  // chunk in stage, stage slot, parity, stages done
+      uint32_t item = 0;
       for (int u = cluster; u < g.units; u += n_clusters, ++item) {
-        {
-          const uint32_t buf = item & 1;
-          if (item >= 2) {
-            mbar_wait_prof(&t_empty[buf], ((item >> 1) - 1) & 1, prof, w_te);
+        const uint32_t buf = item & 1;
+        if (item >= 2) {
+          mbar_wait_prof(&t_empty[buf], ((item >> 1) - 1) & 1, prof, w_te);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        const uint32_t d0 = tmem + buf * (MH * g.NP);
+        uint32_t acc = 0;
+        for (int kb = 0; kb < g.KBn; ++kb) {
+          const uint32_t use = item * g.KBn + kb, sl = use % g.NA;
+          if (!g.a_unit || kb == 0) {
+            mbar_wait_prof(&a_full[g.a_unit ? (item & 1) : sl],
+                           g.a_unit ? ((item >> 1) & 1) : ((use / g.NA) & 1), prof, w_af);
             asm volatile("tcgen05.fence::after_thread_sync;");
           }
-          const uint32_t d0 = tmem + buf * (MH * g.NP);
-          uint32_t acc = 0;
-          for (int kb = 0; kb < g.KBn; ++kb) {
-            const uint32_t use = item * g.KBn + kb, sl = use % g.NA;
-            if (!g.a_unit || kb == 0) {
-              mbar_wait_prof(&a_full[g.a_unit ? (item & 1) : sl],
-                             g.a_unit ? ((item >> 1) & 1) : ((use / g.NA) & 1), prof, w_af);
+          uint32_t a_tap = a_lo0 + sl * plane16;
+          int kx = 0;
+          for (int tap = 0; tap < g.taps; ++tap, ++step) {
+            const unsigned long long tw0 = trace ? clock64() : 0ull;
+            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)kPStages);
+            if (j == 0 && b_proto) {
+              mbar_wait_prof(&b_full[st], ph, prof, w_bf);
               asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            const uint64_t a_kb = a_desc0 + sl * plane16;
-            for (int ky = 0; ky < g.kh; ++ky) {
-              for (int kx = 0; kx < g.kw; ++kx, ++step) {
-                const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
-                const unsigned long long tw0 = trace ? clock64() : 0ull;
-                const bool b_proto = !((g.debug & 256) && sidx >= kPStages);
-                if (j == 0 && b_proto) {
-                  mbar_wait_prof(&b_full[st], (sidx / kPStages) & 1, prof, w_bf);
-                  asm volatile("tcgen05.fence::after_thread_sync;");
-                }
-                if (trace && step < 4096) {  // profiling: chunk issue timeline of CTA pair 0
-                  const unsigned long long tw1 = clock64();
-                  g_umma_prof[512 + step / 8][2 * (step % 8)] = tw0 - t_start;
-                  g_umma_prof[512 + step / 8][2 * (step % 8) + 1] = tw1 - tw0;
-                }
-                const uint64_t a_tap = a_kb + (uint32_t)(ky * g.IC + kx) * 8u;
-                const uint64_t b_st = b_desc0 + (st * kPCPS + j) * b16;
-#pragma unroll
-                for (int s = 0; s < 4; ++s) {
-#pragma unroll
-                  for (int h = 0; h < MH; ++h)
-                    umma_i8_pair_elect(d0 + h * g.NP, a_tap + h * 1024 + 2 * s, b_st + 2 * s, idesc,
-                                 acc | (uint32_t)s);
-                }
-                acc = 1;
-                n_mma += 4 * MH;
-                if (b_proto && (j == kPCPS - 1 || step + 1 == total)) umma_commit_pair_elect(&b_empty[st]);
-              }
+            if (trace && step < 4096) {  // profiling: chunk issue timeline of CTA pair 0
+              const unsigned long long tw1 = clock64();
+              g_umma_prof[512 + step / 8][2 * (step % 8)] = tw0 - t_start;
+              g_umma_prof[512 + step / 8][2 * (step % 8) + 1] = tw1 - tw0;
             }
-            if (!g.a_unit) umma_commit_pair_elect(&a_empty[sl]);
-            else if (kb == g.KBn - 1) umma_commit_pair_elect(&a_empty[item & 1]);
+            umma_chunk_pair<MH>(d0, g.NP, a_tap, b_lo0 + (st * kPCPS + j) * b16, hi, idesc, acc);
+            acc = 1;
+            if (PROF) n_mma += 4 * MH;
+            if (++kx == g.kw) { kx = 0; a_tap += row_skip; } else { a_tap += 8u; }
+            --left;
+            if (++j == (uint32_t)kPCPS || left == 0) {
+              if (b_proto) umma_commit_pair_elect(&b_empty[st]);
+              j = 0;
+              ++stages;
+              if (++st == (uint32_t)kPStages) { st = 0; ph ^= 1u; }
+            }
           }
-          umma_commit_pair_elect(&t_full[buf]);
+          if (!g.a_unit) umma_commit_pair_elect(&a_empty[sl]);
+          else if (kb == g.KBn - 1) umma_commit_pair_elect(&a_empty[item & 1]);
         }
+        umma_commit_pair_elect(&t_full[buf]);
       }
       if (prof) {
         g_umma_prof[blockIdx.x][0] = clock64() - t_start;
@@ -534,7 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     const size_t plane_out = (size_t)g.oh * g.ow;
     const uint32_t t_empty0 = map_to_rank(smem_addr(&t_empty[0]), 0);
     uint32_t item = 0;
-    const bool prof = (g.debug & 128) && warp == kPEpiWarp0 && lane == 0;
+    const bool prof = (dbg & 128) && warp == kPEpiWarp0 && lane == 0;
     unsigned long long w_tf = 0, w_ld = 0, w_st = 0;
     const unsigned long long t_start = clock64();
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
@@ -561,7 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         const uint32_t buf = item & 1;
         mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        for (int ch = (g.debug & 32) ? n_chunks : cg; ch < n_chunks; ch += kPEpiWarps / 4) {
+        for (int ch = (dbg & 32) ? n_chunks : cg; ch < n_chunks; ch += kPEpiWarps / 4) {
           const int c = ch * 16;
           const int obase = nb * g.NP + c;
           const unsigned long long tc0 = prof ? clock64() : 0ull;
@@ -591,10 +662,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
           tmem_wait_ld();
           const unsigned long long tc1 = prof ? clock64() : 0ull;
           if (prof) w_ld += tc1 - tc0;
-          if (g.debug & 1) continue;
+          if (dbg & 1) continue;
           if (fast && obase + 16 <= g.O) {
             // hot path: float output only, all 16 filters valid -- about six
             // instructions per output (IADD3, I2F, 2 FMUL, IMAD.WIDE, predicated STG)
+            if (dbg & (32768 | 65536)) {  // profiling: math without stores / stores without math
+#pragma unroll
+              for (int h = 0; h < MH; ++h) {
+                const float* yp = y + pix[h] + (size_t)obase * plane_out;
+                float sum = 0.0f;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  if (dbg & 32768) {
+                    const int accv = swv[j] - 2 * (int)v[h][j];
+                    sum += __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
+                  } else {
+                    st_cs_pred(yp + j * plane_out32, __int_as_float(v[h][j]), ok[h]);
+                  }
+                }
+                if (dbg & 32768) st_cs_pred(yp, sum, ok[h]);
+              }
+              continue;
+            }
+            if (dbg & (8192 | 16384)) {  // profiling: instruction-count experiments (wrong values)
+#pragma unroll
+              for (int h = 0; h < MH; ++h) {
+                const float* yp = y + pix[h] + (size_t)obase * plane_out;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  const int accv = (dbg & 8192) ? (int)v[h][j] : swv[j] - 2 * (int)v[h][j];
+                  const float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
+                  st_cs_pred((dbg & 16384) ? yp + j * 3136 : yp + j * plane_out32, val, ok[h]);
+                }
+              }
+              continue;
+            }
+            if (dbg & (512 | 1024 | 2048)) {  // profiling: store-shape experiments (wrong layout)
+#pragma unroll
+              for (int h = 0; h < MH; ++h) {
+                const size_t y_end = (size_t)(g.tiles / g.n_mt) * g.O * plane_out;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float f[4];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i)
+                    f[i] = __fmul_rn(__fmul_rn((float)(swv[4 * q + i] - 2 * (int)v[h][4 * q + i]), kv[h]), av[4 * q + i]);
+                  if (dbg & 512) {  // v4: 4 pixels x 1 filter per lane, same bytes, 1/4 the STGs
+                    const size_t idx = ((pix[h] - lane + (size_t)(obase + 4 * q) * plane_out) & ~(size_t)3) + 4 * lane;
+                    if (ok[h] && idx + 4 <= y_end)
+                      asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(y + idx), "f"(f[0]), "f"(f[1]),
+                                   "f"(f[2]), "f"(f[3]) : "memory");
+                  } else if (dbg & 2048) {  // all the math, 16 predicated-off stores
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                      st_cs_pred(y + pix[h] + (size_t)(obase + 4 * q + i) * plane_out, f[i], ok[h] && (dbg & 4096));
+                  } else {  // 1024: a quarter of the scalar stores (1/4 bytes, 1/4 STGs)
+                    st_cs_pred(y + pix[h] + (size_t)(obase + 4 * q) * plane_out, f[0] + f[1] + f[2] + f[3], ok[h]);
+                  }
+                }
+              }
+              continue;
+            }
 #pragma unroll
             for (int h = 0; h < MH; ++h) {
               const float* yp = y + pix[h] + (size_t)obase * plane_out;
@@ -824,9 +952,10 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int pairs = g.units < sms / 2 ? g.units : sms / 2;
-  static size_t attr_smem[2] = {0, 0};  // one-time (per size increase) shared-memory opt-in
-  auto kern = g.MH == 2 ? k_conv_umma_pair<2> : k_conv_umma_pair<1>;
-  size_t& attr = attr_smem[g.MH == 2 ? 1 : 0];
+  static size_t attr_smem[4] = {0, 0, 0, 0};  // one-time (per size increase) shared-memory opt-in
+  auto kern = g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true> : k_conv_umma_pair<2, false>)
+                        : (g.debug ? k_conv_umma_pair<1, true> : k_conv_umma_pair<1, false>);
+  size_t& attr = attr_smem[(g.MH == 2 ? 1 : 0) + (g.debug ? 2 : 0)];
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
