@@ -43,7 +43,7 @@
 // This replaces an 8x larger d-byte tensor in HBM (205 MB written by K1 and
 // re-read by TMA at C3).
 //
-// Persistent, warp-specialised pipeline (one CTA per SM, 640 threads per CTA):
+// Persistent, warp-specialised pipeline (one CTA per SM, 384 threads per CTA):
 //   warp 0      B producer (both CTAs): TMA of this CTA's NP/2 filter rows of one
 //               (tap, K block) chunk, completing on the leader's b_full
 //   warp 1      MMA issuer (leader CTA, one thread): per unit, MH x 4 K=32
@@ -51,8 +51,11 @@
 //   warps 2-3   A producers (both CTAs): per 128-channel K block, packed bits ->
 //               swizzled d-bytes in shared memory, arrive on the leader's a_full;
 //               warp 3 also allocates TMEM (cta_group::2)
-//   warps 4-19  epilogue (both CTAs): TMEM -> registers -> S_w - 2*acc ->
-//               (f32 * K) * alpha -> y, four warps per TMEM lane quadrant
+//   warps 4-11  epilogue (both CTAs): TMEM -> registers -> S_w - 2*acc ->
+//               (f32 * K) * alpha -> y, two warps per TMEM lane quadrant
+//               (16 were slower: the issuer's sub-partition then hosts four busy
+//               epilogue warps, and every issue slot the issuer waits for stalls
+//               the tensor pipe; 4 cannot drain a unit within its MMA time)
 // Work unit = (pair tile of 2*MH*128 extended pixels of one image, filter block
 // of NP).  TMEM holds two accumulators (MH x NP columns each): the epilogue of
 // one unit overlaps the MMAs of the next.
@@ -67,15 +70,15 @@
 namespace xnc {
 
 #ifndef XNC_EPI_WARPS
-#define XNC_EPI_WARPS 16
+#define XNC_EPI_WARPS 8
 #endif
 constexpr int kPEpiWarps = XNC_EPI_WARPS;  // multiple of 4 (one group per TMEM lane quadrant)
 constexpr int kPThreads = 128 + 32 * kPEpiWarps;
 #ifndef XNC_PSTAGES
-#define XNC_PSTAGES 2
+#define XNC_PSTAGES 4
 #endif
 #ifndef XNC_PCPS
-#define XNC_PCPS 3
+#define XNC_PCPS 1
 #endif
 constexpr int kPStages = XNC_PSTAGES;  // B pipeline depth (stages)
 constexpr int kPCPS = XNC_PCPS;        // (tap, K block) chunks per B stage: one wait + one commit each
@@ -593,8 +596,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     }
   } else if (warp >= kPEpiWarp0 && warp < kPEpiWarp0 + kPEpiWarps) {
     // ================= epilogue (both CTAs)
-    // 16 warps: warp w reads TMEM lane quadrant (w & 3) and the 16-column chunks
-    // cg, cg+4, ... (cg = (w-4) >> 2) of every accumulator row block.  Each
+    // warp w reads TMEM lane quadrant (w & 3) and the 16-column chunks cg,
+    // cg + kPEpiWarps/4, ... (cg = (w-4) >> 2) of every accumulator row block.  Each
     // thread owns one extended pixel per row block; for a chunk it issues the
     // TMEM loads of all row blocks before one wait, then writes 16 filters x MH
     // pixels (for a fixed filter the 32 lanes store 32 consecutive pixels).
