@@ -308,6 +308,17 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// wait for this thread's TMEM loads with the destination registers as operands, so
+// the compiler cannot hoist their uses above the wait
+#define XNC_R16(v) "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), \
+    "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+__device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : XNC_R16(v)::"memory");
+}
+// orders later uses of v after the preceding (volatile) wait
+__device__ __forceinline__ void reg_dep16(uint32_t (&v)[16]) { asm volatile("" : XNC_R16(v)); }
+#undef XNC_R16
+
 struct PairGeom {
   int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NP, MH, taps, Cw;
   int P;             // extended pixel rows one K-block plane holds
@@ -598,19 +609,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     // ================= epilogue (both CTAs)
     // warp w reads TMEM lane quadrant (w & 3) and the 16-column chunks cg,
     // cg + kPEpiWarps/4, ... (cg = (w-4) >> 2) of every accumulator row block.  Each
-    // thread owns one extended pixel per row block; for a chunk it issues the
-    // TMEM loads of all row blocks before one wait, then writes 16 filters x MH
-    // pixels (for a fixed filter the 32 lanes store 32 consecutive pixels).
+    // thread owns one extended pixel per row block and writes 16 filters x MH
+    // pixels per chunk (for a fixed filter the 32 lanes store 32 consecutive
+    // pixels).  (Software-pipelining the TMEM loads across chunks measured no
+    // faster at C3 and 10% slower at C2: the loads are not the critical path.)
     const int e_w = warp - kPEpiWarp0;
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int cg = e_w >> 2;
+    constexpr int cstep = kPEpiWarps / 4;
     const int n_chunks = g.NP / 16;
     const size_t plane_out = (size_t)g.oh * g.ow;
     const uint32_t t_empty0 = map_to_rank(smem_addr(&t_empty[0]), 0);
     uint32_t item = 0;
     const bool prof = (dbg & 128) && warp == kPEpiWarp0 && lane == 0;
     unsigned long long w_tf = 0, w_ld = 0, w_st = 0;
-    const unsigned long long t_start = clock64();
+    const unsigned long long t_start = PROF ? clock64() : 0ull;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
                         ((reinterpret_cast<uintptr_t>(alpha) & 15) == 0);
     // 32-bit filter-plane stride for the hot path (host guarantees O*oh*ow < 2^31)
@@ -631,140 +644,97 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         pix[h] = (size_t)n * g.O * plane_out + (size_t)rr * g.ow + cc;
         kv[h] = (ok[h] && y) ? __ldg(Kmap + (size_t)n * plane_out + (size_t)rr * g.ow + cc) : 0.0f;
       }
-      {
-        const uint32_t buf = item & 1;
-        mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        for (int ch = (dbg & 32) ? n_chunks : cg; ch < n_chunks; ch += kPEpiWarps / 4) {
-          const int c = ch * 16;
-          const int obase = nb * g.NP + c;
-          const unsigned long long tc0 = prof ? clock64() : 0ull;
-          uint32_t v[MH][16];
+      const uint32_t buf = item & 1;
+      mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NP);
+      for (int ch = (PROF && (dbg & 32)) ? n_chunks : cg; ch < n_chunks; ch += cstep) {
+        const int obase = nb * g.NP + ch * 16;
+        const unsigned long long tc0 = prof ? clock64() : 0ull;
+        uint32_t v[MH][16];
 #pragma unroll
-          for (int h = 0; h < MH; ++h)
-            tmem_ld16_async(tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NP) + h * g.NP + c, v[h]);
-          // per-filter constants for these 16 columns (uniform across lanes)
-          int swv[16];
-          float av[16];
-          if (vec_ok && obase + 16 <= g.O) {
+        for (int h = 0; h < MH; ++h) tmem_ld16_async(tbase + h * g.NP + ch * 16, v[h]);
+        // per-filter constants for these 16 columns (uniform across lanes), loaded
+        // while the TMEM loads are in flight
+        int swv[16];
+        float av[16];
+        if (vec_ok && obase + 16 <= g.O) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int4 si = __ldg(reinterpret_cast<const int4*>(sw + obase) + q);
-              const float4 ai = __ldg(reinterpret_cast<const float4*>(alpha + obase) + q);
-              swv[4 * q] = si.x; swv[4 * q + 1] = si.y; swv[4 * q + 2] = si.z; swv[4 * q + 3] = si.w;
-              av[4 * q] = ai.x; av[4 * q + 1] = ai.y; av[4 * q + 2] = ai.z; av[4 * q + 3] = ai.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const bool in = obase + j < g.O;
-              swv[j] = in ? __ldg(sw + obase + j) : 0;
-              av[j] = in ? __ldg(alpha + obase + j) : 0.0f;
-            }
+          for (int q = 0; q < 4; ++q) {
+            const int4 si = __ldg(reinterpret_cast<const int4*>(sw + obase) + q);
+            const float4 ai = __ldg(reinterpret_cast<const float4*>(alpha + obase) + q);
+            swv[4 * q] = si.x; swv[4 * q + 1] = si.y; swv[4 * q + 2] = si.z; swv[4 * q + 3] = si.w;
+            av[4 * q] = ai.x; av[4 * q + 1] = ai.y; av[4 * q + 2] = ai.z; av[4 * q + 3] = ai.w;
           }
-          tmem_wait_ld();
-          const unsigned long long tc1 = prof ? clock64() : 0ull;
-          if (prof) w_ld += tc1 - tc0;
-          if (dbg & 1) continue;
-          if (fast && obase + 16 <= g.O) {
-            // hot path: float output only, all 16 filters valid -- about six
-            // instructions per output (IADD3, I2F, 2 FMUL, IMAD.WIDE, predicated STG)
-            if (dbg & (32768 | 65536)) {  // profiling: math without stores / stores without math
+        } else {
 #pragma unroll
-              for (int h = 0; h < MH; ++h) {
-                const float* yp = y + pix[h] + (size_t)obase * plane_out;
-                float sum = 0.0f;
+          for (int j = 0; j < 16; ++j) {
+            const bool in = obase + j < g.O;
+            swv[j] = in ? __ldg(sw + obase + j) : 0;
+            av[j] = in ? __ldg(alpha + obase + j) : 0.0f;
+          }
+        }
+        tmem_wait_ld_regs(v[0]);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                  if (dbg & 32768) {
-                    const int accv = swv[j] - 2 * (int)v[h][j];
-                    sum += __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
-                  } else {
-                    st_cs_pred(yp + j * plane_out32, __int_as_float(v[h][j]), ok[h]);
-                  }
-                }
-                if (dbg & 32768) st_cs_pred(yp, sum, ok[h]);
-              }
-              continue;
-            }
-            if (dbg & (8192 | 16384)) {  // profiling: instruction-count experiments (wrong values)
-#pragma unroll
-              for (int h = 0; h < MH; ++h) {
-                const float* yp = y + pix[h] + (size_t)obase * plane_out;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                  const int accv = (dbg & 8192) ? (int)v[h][j] : swv[j] - 2 * (int)v[h][j];
-                  const float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
-                  st_cs_pred((dbg & 16384) ? yp + j * 3136 : yp + j * plane_out32, val, ok[h]);
-                }
-              }
-              continue;
-            }
-            if (dbg & (512 | 1024 | 2048)) {  // profiling: store-shape experiments (wrong layout)
-#pragma unroll
-              for (int h = 0; h < MH; ++h) {
-                const size_t y_end = (size_t)(g.tiles / g.n_mt) * g.O * plane_out;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  float f[4];
-#pragma unroll
-                  for (int i = 0; i < 4; ++i)
-                    f[i] = __fmul_rn(__fmul_rn((float)(swv[4 * q + i] - 2 * (int)v[h][4 * q + i]), kv[h]), av[4 * q + i]);
-                  if (dbg & 512) {  // v4: 4 pixels x 1 filter per lane, same bytes, 1/4 the STGs
-                    const size_t idx = ((pix[h] - lane + (size_t)(obase + 4 * q) * plane_out) & ~(size_t)3) + 4 * lane;
-                    if (ok[h] && idx + 4 <= y_end)
-                      asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(y + idx), "f"(f[0]), "f"(f[1]),
-                                   "f"(f[2]), "f"(f[3]) : "memory");
-                  } else if (dbg & 2048) {  // all the math, 16 predicated-off stores
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                      st_cs_pred(y + pix[h] + (size_t)(obase + 4 * q + i) * plane_out, f[i], ok[h] && (dbg & 4096));
-                  } else {  // 1024: a quarter of the scalar stores (1/4 bytes, 1/4 STGs)
-                    st_cs_pred(y + pix[h] + (size_t)(obase + 4 * q) * plane_out, f[0] + f[1] + f[2] + f[3], ok[h]);
-                  }
-                }
-              }
-              continue;
-            }
+        for (int h = 1; h < MH; ++h) reg_dep16(v[h]);
+        const unsigned long long tc1 = prof ? clock64() : 0ull;
+        if (prof) w_ld += tc1 - tc0;
+        if (PROF && (dbg & 1)) continue;
+        if (fast && obase + 16 <= g.O) {
+          // hot path: float output only, all 16 filters valid (IADD3, I2F, 2 FMUL,
+          // address, predicated STG per output); the optional per-filter affine
+          // (bias / folded BN of the next layer) is a separate loop so the plain
+          // path carries none of its loads
+          if (out_scale == nullptr) {
 #pragma unroll
             for (int h = 0; h < MH; ++h) {
               const float* yp = y + pix[h] + (size_t)obase * plane_out;
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const int accv = swv[j] - 2 * (int)v[h][j];
-                float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
-                if (out_scale != nullptr)  // optional per-filter affine (bias / folded BN of the next layer)
-                  val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + obase + j)), __ldg(out_shift + obase + j));
-                st_cs_pred(yp + j * plane_out32, val, ok[h]);
+                st_cs_pred(yp + j * plane_out32, __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]), ok[h]);
               }
             }
-            if (prof) w_st += clock64() - tc1;
-            continue;
-          }
+          } else {
 #pragma unroll
-          for (int h = 0; h < MH; ++h) {
-            if (!ok[h]) continue;
+            for (int h = 0; h < MH; ++h) {
+              const float* yp = y + pix[h] + (size_t)obase * plane_out;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int o = obase + j;
-              if (o < g.O) {
+              for (int j = 0; j < 16; ++j) {
                 const int accv = swv[j] - 2 * (int)v[h][j];
-                const size_t idx = pix[h] + (size_t)o * plane_out;
-                if (y) {
-                  float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
-                  if (out_scale != nullptr)
-                    val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
-                  __stcs(y + idx, val);
-                }
-                if (acc_out) acc_out[idx] = accv;
+                const float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
+                st_cs_pred(yp + j * plane_out32,
+                           __fadd_rn(__fmul_rn(val, __ldg(out_scale + obase + j)), __ldg(out_shift + obase + j)),
+                           ok[h]);
               }
+            }
+          }
+          if (prof) w_st += clock64() - tc1;
+          continue;
+        }
+#pragma unroll
+        for (int h = 0; h < MH; ++h) {
+          if (!ok[h]) continue;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int o = obase + j;
+            if (o < g.O) {
+              const int accv = swv[j] - 2 * (int)v[h][j];
+              const size_t idx = pix[h] + (size_t)o * plane_out;
+              if (y) {
+                float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
+                if (out_scale != nullptr)
+                  val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
+                __stcs(y + idx, val);
+              }
+              if (acc_out) acc_out[idx] = accv;
             }
           }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(t_empty0 + buf * 8);
       }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(t_empty0 + buf * 8);
     }
     if (prof) {
       g_umma_prof[blockIdx.x][5] = clock64() - t_start;
