@@ -13,6 +13,8 @@
 // channels with 16-byte loads; a warp's load is 512 contiguous bytes per
 // channel (fully coalesced), and x is read exactly once.  The bits for 32
 // channels are built in registers and written as one word per pixel.
+#include <type_traits>
+
 #include "xnc_common.cuh"
 
 namespace xnc {
@@ -27,7 +29,7 @@ namespace xnc {
 // kernel (popc, b1 mma.sync and the tcgen05 pair kernel, which expands the
 // bits to its byte operand in shared memory) reads this one format.
 #ifndef XNC_PACK_THREADS
-#define XNC_PACK_THREADS 512  // sweep (tools/pack_sweep.py): 512 x unroll 8 = 6.4 TB/s at C3, 256 = 5.0
+#define XNC_PACK_THREADS 128  // sweep (tools/pack_sweep.py, explicit 8-deep loads): 128 = 6.6 TB/s at C3, 256 = 6.5, 512 = 5.7
 #endif
 #ifndef XNC_PACK_UNROLL
 #define XNC_PACK_UNROLL 8
@@ -35,7 +37,7 @@ namespace xnc {
 constexpr int kPackThreads = XNC_PACK_THREADS;  // preferred block size (smaller if smem is short)
 constexpr int kPackUnroll = XNC_PACK_UNROLL;  // channel loads in flight per thread
 
-template <int VEC, int THREADS>
+template <int VEC, int THREADS, bool AFF>
 __global__ void __launch_bounds__(THREADS) k_pack_input(const float* __restrict__ x, int C, int HW,
                                                              int Cw, float inv, long groups_per_img,
                                                              long total_groups,
@@ -63,26 +65,39 @@ __global__ void __launch_bounds__(THREADS) k_pack_input(const float* __restrict_
 #pragma unroll
       for (int i = 0; i < VEC; ++i) word[i] = 0u;
       const int cend = min(32, C - 32 * j);
-#pragma unroll kPackUnroll
-      for (int cc = 0; cc < cend; ++cc) {
-        const float* src = xp + (long)(32 * j + cc) * HW;
-        float v[VEC];
-        if constexpr (VEC == 4) {
-          float4 t = __ldcs(reinterpret_cast<const float4*>(src));  // streamed once
-          v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-        } else {
+      // kPackUnroll channel loads are issued before any is consumed (written out
+      // explicitly: left to the compiler, the streaming loads were issued one at a
+      // time, each right before its use, and K1 ran at ~80% of the HBM read rate)
+      for (int c0 = 0; c0 < cend; c0 += kPackUnroll) {
+        float v[kPackUnroll][VEC];
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) v[i] = __ldcs(src + i);
+        for (int u = 0; u < kPackUnroll; ++u) {
+          const float* src = xp + (long)(32 * j + c0 + u) * HW;
+          if (c0 + u < cend) {
+            if constexpr (VEC == 4) {
+              const float4 t = __ldcs(reinterpret_cast<const float4*>(src));  // streamed once
+              v[u][0] = t.x; v[u][1] = t.y; v[u][2] = t.z; v[u][3] = t.w;
+            } else {
+#pragma unroll
+              for (int i = 0; i < VEC; ++i) v[u][i] = __ldcs(src + i);
+            }
+          }
         }
-        if (in_scale != nullptr) {  // optional per-channel affine (folded BN) before sign and |.|
-          const float sc = __ldg(in_scale + 32 * j + cc), sh = __ldg(in_shift + 32 * j + cc);
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) v[i] = __fadd_rn(__fmul_rn(v[i], sc), sh);
-        }
+        for (int u = 0; u < kPackUnroll; ++u) {
+          if (c0 + u < cend) {
+            const int cc = c0 + u;
+            if constexpr (AFF) {  // per-channel affine (folded BN) before sign and |.|
+              const float sc = __ldg(in_scale + 32 * j + cc), sh = __ldg(in_shift + 32 * j + cc);
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) {
-          s[i] = __fadd_rn(s[i], fabsf(v[i]));
-          word[i] |= (v[i] >= 0.0f ? 1u : 0u) << cc;
+              for (int i = 0; i < VEC; ++i) v[u][i] = __fadd_rn(__fmul_rn(v[u][i], sc), sh);
+            }
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) {
+              s[i] = __fadd_rn(s[i], fabsf(v[u][i]));
+              word[i] |= (v[u][i] >= 0.0f ? 1u : 0u) << cc;
+            }
+          }
         }
       }
       if constexpr (VEC == 4) {
@@ -195,24 +210,30 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   const size_t smem = (size_t)Cw * (threads * vec + 4) * 4;
   if (smem > 200 * 1024) return XNC_ENOTSUP;  // C > ~12k channels
   const unsigned blocks = (unsigned)cdivl(total, threads);
-  static size_t opted[2][3] = {{0, 0, 0}, {0, 0, 0}};  // one-time smem opt-in per instantiation
+  static size_t opted[2][2][3] = {};  // one-time smem opt-in per instantiation
+  const bool aff = in_scale != nullptr;
   auto go = [&](auto kern, int t) {
-    size_t& o = opted[vec4 ? 1 : 0][t == 512 ? 2 : t == 256 ? 1 : 0];
+    size_t& o = opted[vec4 ? 1 : 0][aff ? 1 : 0][t == 512 ? 2 : t == 256 ? 1 : 0];
     if (smem > 48 * 1024 && smem > o) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       o = smem;
     }
     kern<<<blocks, t, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, in_scale, in_shift);
   };
-  if (vec4) {
-    if (threads == 512) go(k_pack_input<4, 512>, 512);
-    else if (threads == 256) go(k_pack_input<4, 256>, 256);
-    else go(k_pack_input<4, 128>, 128);
-  } else {
-    if (threads == 512) go(k_pack_input<1, 512>, 512);
-    else if (threads == 256) go(k_pack_input<1, 256>, 256);
-    else go(k_pack_input<1, 128>, 128);
-  }
+  auto pick = [&](auto aff_tag) {
+    constexpr bool AF = decltype(aff_tag)::value;
+    if (vec4) {
+      if (threads == 512) go(k_pack_input<4, 512, AF>, 512);
+      else if (threads == 256) go(k_pack_input<4, 256, AF>, 256);
+      else go(k_pack_input<4, 128, AF>, 128);
+    } else {
+      if (threads == 512) go(k_pack_input<1, 512, AF>, 512);
+      else if (threads == 256) go(k_pack_input<1, 256, AF>, 256);
+      else go(k_pack_input<1, 128, AF>, 128);
+    }
+  };
+  if (aff) pick(std::true_type{});
+  else pick(std::false_type{});
   return launch_status();
 }
 
