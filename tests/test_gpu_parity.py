@@ -142,7 +142,12 @@ UMMA_CASES = RANDOM_CASES + [(2, 256, 14, 14, 64, 3, 3, 1), (1, 128, 20, 20, 300
                              (2, 512, 10, 10, 96, 3, 3, 1), (1, 520, 7, 7, 20, 3, 3, 1),
                              (3, 64, 9, 9, 512, 3, 3, 1), (5, 40, 11, 7, 77, 2, 3, 1),
                              (4, 32, 1, 200, 24, 1, 5, 0), (1, 48, 12, 12, 16, 8, 8, 3),
-                             (2, 32, 5, 5, 32, 3, 3, 4), (7, 64, 3, 3, 192, 3, 3, 1)]
+                             (2, 32, 5, 5, 32, 3, 3, 4), (7, 64, 3, 3, 192, 3, 3, 1),
+                             # 256-filter blocks: tiles starting mid-row, odd widths, tail filters,
+                             # two blocks with a tail, 7x7 taps, rows wider than a quarter tile
+                             (1, 64, 56, 56, 256, 3, 3, 1), (2, 32, 23, 17, 250, 3, 3, 1),
+                             (1, 48, 15, 30, 500, 5, 5, 2), (1, 32, 20, 20, 256, 7, 7, 3),
+                             (2, 128, 8, 64, 256, 3, 3, 1), (3, 16, 2, 3, 256, 2, 2, 1)]
 
 
 @pytest.mark.parametrize("shape", UMMA_CASES, ids=lambda s: "x".join(map(str, s)))
