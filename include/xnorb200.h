@@ -116,6 +116,20 @@ int xnc_xnor_conv_umma_affine(const uint32_t* bits, const uint8_t* wq, const int
                               const float* K, const float* alpha, int N, int C, int H, int W,
                               int O, int kh, int kw, int pad, const float* out_scale,
                               const float* out_shift, float* y, int32_t* acc, void* stream);
+/* K split for shapes with fewer (pixel tile, 256-filter block) work units than CTA
+ * pairs -- fully connected layers viewed as one 1 x N image.  Units of one output
+ * tile take disjoint K ranges and add their raw partial sums into split_ws
+ * (s32, xnc_umma_split_ws_bytes() bytes, ZEROED by the caller; left zeroed on
+ * return); a finalize kernel then writes y / acc with the same arithmetic as the
+ * unsplit epilogue (integer sums: exact in any order).  xnc_umma_split_ws_bytes()
+ * == 0: no split for this shape, split_ws is ignored (may be NULL).  Otherwise
+ * the same contract as xnc_xnor_conv_umma_affine (which never splits). */
+size_t xnc_umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad);
+int xnc_xnor_conv_umma_ws(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
+                          const float* K, const float* alpha, int N, int C, int H, int W,
+                          int O, int kh, int kw, int pad, const float* out_scale,
+                          const float* out_shift, int32_t* split_ws, float* y, int32_t* acc,
+                          void* stream);
 /* Profiling only: per-CTA cycle counters of the last tcgen05 conv launched with
  * XNC_UMMA_DEBUG bit 7 set (16 u64 slots per CTA, host memory; blocking copy). */
 int xnc_umma_profile(unsigned long long* host_out, int n_ctas);

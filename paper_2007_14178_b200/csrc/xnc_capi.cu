@@ -133,6 +133,23 @@ int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* s
                           as_stream(stream));
 }
 
+size_t xnc_umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
+  if (O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return 0;
+  return umma_split_ws_bytes(N, C, H, W, O, kh, kw, pad);
+}
+
+int xnc_xnor_conv_umma_ws(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
+                          const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
+                          const float* out_scale, const float* out_shift, int32_t* split_ws, float* y,
+                          int32_t* acc, void* stream) {
+  if (!bits || !wq || !sw || O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return XNC_EINVAL;
+  if (!y && !acc) return XNC_EINVAL;
+  if (y && (!K || !alpha)) return XNC_EINVAL;
+  if (!out_scale != !out_shift) return XNC_EINVAL;
+  return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, acc, as_stream(stream),
+                          out_scale, out_shift, split_ws);
+}
+
 int xnc_umma_profile(unsigned long long* host_out, int n_ctas) {
   if (!host_out || n_ctas < 1) return XNC_EINVAL;
   return umma_profile_read(host_out, n_ctas);

@@ -62,6 +62,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -329,7 +330,10 @@ struct PairGeom {
   int n_mt;          // pair tiles per image
   int n_nb;          // filter blocks
   int tiles;         // N * n_mt
-  int units;         // tiles * n_nb work units (pair tile, filter block), strided over the pairs
+  int units;         // tiles * n_nb * S work units (pair tile, filter block, K split), strided over the pairs
+  int S, KBu;        // K splits per (tile, filter block) and K blocks per unit (KBn = S * KBu); S > 1
+                     // for shapes with fewer (tile, block) pairs than CTA pairs (fully connected
+                     // layers): the units add raw partial sums into a zeroed s32 buffer
   uint32_t b_half_bytes, tmem_cols;
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
              // (kPCPS == 1 only), bit 8 = no B protocol at all after the first fill, bit 2 = build the
@@ -355,7 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
     const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out,
-    const float* __restrict__ out_scale, const float* __restrict__ out_shift) {
+    const float* __restrict__ out_scale, const float* __restrict__ out_shift, int32_t* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
@@ -373,7 +377,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
   if (tid == 0) {
     for (int s = 0; s < kPStages; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
     for (int k = 0; k < kPMaxA; ++k) {
-      mbar_init(&a_full[k], 2 * kPAWarps * (g.a_unit ? g.KBn : 1));
+      mbar_init(&a_full[k], 2 * kPAWarps * (g.a_unit ? g.KBu : 1));
       mbar_init(&a_empty[k], 1);
     }
     for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], 2 * kPEpiWarps); }
@@ -400,11 +404,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       unsigned long long w_be = 0;
       const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
       const int my_units = (g.units - cluster + n_clusters - 1) / n_clusters;
-      const uint32_t total = (uint32_t)my_units * g.KBn * g.taps;
+      const uint32_t total = (uint32_t)my_units * g.KBu * g.taps;
       uint32_t step = 0;
       for (int u = cluster; u < g.units; u += n_clusters) {
-        const int nb = u % g.n_nb;
-          for (int kb = 0; kb < g.KBn; ++kb)
+        const int nb = (u / g.S) % g.n_nb, kbu0 = (u % g.S) * g.KBu;
+          for (int kb = kbu0; kb < kbu0 + g.KBu; ++kb)
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
               const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
               if (j == 0) {
@@ -439,15 +443,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     // epilogue's store stream the L2 latency of the bit rows grows, and a
     // one-load-at-a-time loop left the issuer waiting on a_full.
     constexpr int kAR = 4;
-    const int grp = g.a_unit ? g.KBn : 1;
-    uint32_t it = 0;  // units of this pair so far: every unit builds its KBn planes
+    const int grp = g.a_unit ? g.KBu : 1;
+    uint32_t it = 0;  // units of this pair so far: every unit builds its KBu planes
     for (int u = cluster; u < g.units; u += n_clusters, ++it) {
-      const int t = u / g.n_nb;
+      const int t = u / (g.n_nb * g.S), kbu0 = (u % g.S) * g.KBu;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
       const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
-      for (int kb0 = 0; kb0 < g.KBn; kb0 += grp) {
-        const uint32_t use0 = it * g.KBn + kb0;
+      for (int kb0 = 0; kb0 < g.KBu; kb0 += grp) {
+        const uint32_t use0 = it * g.KBu + kb0;
         // barrier guarding the group's slots: per unit (group it & 1) or per plane
         const uint32_t ab = g.a_unit ? (it & 1) : use0 % g.NA;
         const bool wait_empty = g.a_unit ? it >= 2 : use0 >= (uint32_t)g.NA;
@@ -458,7 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         }
         if (!((dbg & 4) && use0 >= (uint32_t)g.NA)) {  // bit 2 (profiling): planes built once
           for (int kp = 0; kp < grp; kp += 2) {
-            const int kbA = kb0 + kp;
+            const int kbA = kbu0 + kb0 + kp;  // global K block of the first plane
             const bool two = kp + 1 < grp;
             uint8_t* planes[2];
             uint32_t vmask[2][4];  // valid-channel masks of each block's four words
@@ -546,7 +550,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       const bool prof = PROF && (dbg & 128) && lane == 0;
       const bool trace = PROF && (dbg & 64) && blockIdx.x == 0 && lane == 0;
       const int my_units = (g.units - cluster + n_clusters - 1) / n_clusters;
-      uint32_t left = (uint32_t)my_units * g.KBn * g.taps;  // chunks still to issue
+      uint32_t left = (uint32_t)my_units * g.KBu * g.taps;  // chunks still to issue
       unsigned long long w_te = 0, w_af = 0, w_bf = 0, n_mma = 0;
       const unsigned long long t_start = PROF ? clock64() : 0ull;
       uint32_t j = 0, st = 0, ph = 0, stages = 0, step = 0;  // chunk in stage, stage slot, parity, stages done
@@ -559,8 +563,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         }
         const uint32_t d0 = tmem + buf * (MH * g.NP);
         uint32_t acc = 0;
-        for (int kb = 0; kb < g.KBn; ++kb) {
-          const uint32_t use = item * g.KBn + kb, sl = use % g.NA;
+        for (int kb = 0; kb < g.KBu; ++kb) {
+          const uint32_t use = item * g.KBu + kb, sl = use % g.NA;
           if (!g.a_unit || kb == 0) {
             mbar_wait_prof(&a_full[g.a_unit ? (item & 1) : sl],
                            g.a_unit ? ((item >> 1) & 1) : ((use / g.NA) & 1), prof, w_af);
@@ -593,7 +597,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
             }
           }
           if (!g.a_unit) umma_commit_pair_elect(&a_empty[sl]);
-          else if (kb == g.KBn - 1) umma_commit_pair_elect(&a_empty[item & 1]);
+          else if (kb == g.KBu - 1) umma_commit_pair_elect(&a_empty[item & 1]);
         }
         umma_commit_pair_elect(&t_full[buf]);
       }
@@ -630,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     const int plane_out32 = g.oh * g.ow;
     const bool fast = y != nullptr && acc_out == nullptr;
     for (int u = cluster; u < g.units; u += n_clusters, ++item) {
-      const int t = u / g.n_nb, nb = u - t * g.n_nb;
+      const int t = u / (g.n_nb * g.S), nb = (u / g.S) % g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);
       size_t pix[MH];
@@ -680,6 +684,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         const unsigned long long tc1 = prof ? clock64() : 0ull;
         if (prof) w_ld += tc1 - tc0;
         if (PROF && (dbg & 1)) continue;
+        if (part != nullptr) {  // K split: add this unit's raw partial sums (exact, any order)
+#pragma unroll
+          for (int h = 0; h < MH; ++h) {
+            if (!ok[h]) continue;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (obase + j < g.O) atomicAdd(part + pix[h] + (size_t)(obase + j) * plane_out, (int)v[h][j]);
+          }
+          continue;
+        }
         if (fast && obase + 16 <= g.O) {
           // hot path: float output only, all 16 filters valid (IADD3, I2F, 2 FMUL,
           // address, predicated STG per output); the optional per-filter affine
@@ -824,7 +838,7 @@ int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int
 }
 
 static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int pad, int MH, PairGeom& g,
-                         size_t& smem) {
+                         size_t& smem, int S = 1) {
   g.C = C; g.H = H; g.W = W; g.O = O; g.kh = kh; g.kw = kw; g.pad = pad; g.MH = MH;
   g.oh = H + 2 * pad - kh + 1; g.ow = W + 2 * pad - kw + 1;
   g.IC = W + 2 * pad;
@@ -839,7 +853,9 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   g.n_mt = cdiv(g.oh * g.IC, 2 * MT);
   g.n_nb = cdiv(O, g.NP);
   g.tiles = N * g.n_mt;
-  g.units = g.tiles * g.n_nb;
+  g.S = g.KBn % S == 0 ? S : 1;
+  g.KBu = g.KBn / g.S;
+  g.units = g.tiles * g.n_nb * g.S;
   g.b_half_bytes = (uint32_t)(g.NP / 2) * 128u;
   const int cols = 2 * MH * g.NP;  // two accumulators x MH row blocks
   g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
@@ -847,13 +863,13 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   // A plane ring: two units' planes when they fit (the next unit's planes are
   // built during this unit's MMAs), else fewer; long K (fully connected layers
   // viewed as 1 x N images) streams through the ring.
-  g.NA = 2 * g.KBn < kPMaxA ? 2 * g.KBn : kPMaxA;
+  g.NA = 2 * g.KBu < kPMaxA ? 2 * g.KBu : kPMaxA;
   while (g.NA > 1 && (size_t)g.NA * g.plane_bytes + b_bytes > 225 * 1024) --g.NA;
   smem = (size_t)g.NA * g.plane_bytes + b_bytes;
 #ifdef XNC_A_PER_PLANE
   g.a_unit = 0;
 #else
-  g.a_unit = g.NA == 2 * g.KBn;
+  g.a_unit = g.NA == 2 * g.KBu;
 #endif
   return cols <= 512 && smem <= 225 * 1024 && (long)g.units < 0x7fffffffL &&
          (long)g.n_nb * g.NP * g.oh * g.ow < 0x7fffffffL;
@@ -862,13 +878,66 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
 // MH = 2 row blocks per CTA for narrow filter blocks (NP <= 128: two MMAs per
 // K step), 1 for wider ones; fall back to MH = 1 when the rows do not fit shared
 // memory.  XNC_UMMA_MH overrides (tuning knob).
-static bool pair_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, PairGeom& g, size_t& smem) {
+static bool pair_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, PairGeom& g, size_t& smem,
+                      int S = 1) {
   static const int mh_env = getenv("XNC_UMMA_MH") ? atoi(getenv("XNC_UMMA_MH")) : 0;
   int mh = pair_np(O) > 128 ? 1 : 2;
   if (mh_env == 1 || (mh_env == 2 && pair_np(O) <= 128)) mh = mh_env;
   for (; mh >= 1; mh /= 2)
-    if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem)) return true;
+    if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem, S)) return true;
   return false;
+}
+
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 2) sms = 148;
+  }
+  return sms;
+}
+
+// K splits for a shape: the largest divisor S of KBn with (tile, block) units * S
+// <= CTA pairs, when the unsplit shape leaves more than half of the pairs idle
+// (fully connected layers: one 256-image tile, O / 256 blocks, K up to 36 K blocks
+// of 128 channels per split unit).  1 = no split.
+static int split_factor(const PairGeom& g) {
+  const int pairs = sm_count() / 2;
+  if (2 * g.units > pairs || g.KBn < 2) return 1;
+  int best = 1;
+  for (int d = 2; d <= g.KBn; ++d)
+    if (g.KBn % d == 0 && (long)g.units * d <= pairs) best = d;
+  return best;
+}
+
+size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
+  PairGeom g;
+  size_t smem;
+  if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem) || split_factor(g) == 1) return 0;
+  return (size_t)N * O * g.oh * g.ow * sizeof(int32_t);
+}
+
+// K-split epilogue: part (the units' summed raw d.s_w sums) -> y / acc exactly as
+// the conv epilogue would, and part back to zero for the next call.
+__global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __restrict__ sw,
+                                 const float* __restrict__ Kmap, const float* __restrict__ alpha,
+                                 const float* __restrict__ out_scale, const float* __restrict__ out_shift,
+                                 long total, int O, long plane, float* __restrict__ y, int32_t* __restrict__ acc) {
+  // 32-bit index math (the host guarantees total < 2^31): 64-bit divisions made
+  // this kernel 10x slower than its 12 bytes per output
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)total; i += gridDim.x * blockDim.x) {
+    const int np = i / (int)plane, p = i - np * (int)plane;
+    const int n = np / O, o = np - n * O;
+    const int accv = __ldg(sw + o) - 2 * part[i];
+    part[i] = 0;
+    if (acc) acc[i] = accv;
+    if (y) {
+      float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + (long)n * plane + p)), __ldg(alpha + o));
+      if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
+      y[i] = val;
+    }
+  }
 }
 
 bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
@@ -898,10 +967,13 @@ int umma_profile_read(unsigned long long* host, int n_ctas) {
 int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s, const float* out_scale,
-                     const float* out_shift) {
+                     const float* out_shift, int32_t* split_ws) {
   PairGeom g;
   size_t smem;
   if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
+  // split K across CTA pairs when the caller passed the (zeroed) partial-sum buffer
+  const int S = split_ws != nullptr ? split_factor(g) : 1;
+  if (S > 1 && !pair_plan(N, C, H, W, O, kh, kw, pad, g, smem, S)) return XNC_ENOTSUP;
   auto encode = tensor_map_encoder();
   if (!encode) return XNC_ENOTSUP;
   // B: weight rows [n_nb * taps * KBn * NP][128 B]; box = NP/2 rows
@@ -921,9 +993,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     static const int dbg = getenv("XNC_UMMA_DEBUG") ? atoi(getenv("XNC_UMMA_DEBUG")) : 0;
     g.debug = dbg;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   const int pairs = g.units < sms / 2 ? g.units : sms / 2;
   static size_t attr_smem[4] = {0, 0, 0, 0};  // one-time (per size increase) shared-memory opt-in
   auto kern = g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true> : k_conv_umma_pair<2, false>)
@@ -934,7 +1004,17 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
     attr = smem;
   }
-  kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift);
+  int32_t* part = g.S > 1 && (long)N * O * g.oh * g.ow < 0x7fffffffL ? split_ws : nullptr;
+  if (g.S > 1 && part == nullptr) {  // no buffer usable: run unsplit
+    if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
+  }
+  kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part);
+  if (part != nullptr) {
+    const long total = (long)N * O * g.oh * g.ow;
+    const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
+    k_split_finalize<<<blocks, 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift, total, O,
+                                            (long)g.oh * g.ow, y, acc);
+  }
   return launch_status();
 }
 

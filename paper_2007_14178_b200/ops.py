@@ -186,9 +186,13 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
         if filt.wq is None:
             raise ValueError("umma variant needs attach_umma_weights() first")
         osc, osh = _affine(out_affine, filt.O, dev, "out_affine")
-        check(lib().xnc_xnor_conv_umma_affine(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), _ptr(K),
-                                              filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
-                                              _ptr(osc), _ptr(osh), _ptr(y), _ptr(acc), _stream(dev)),
+        # a K split (fully connected shapes) needs a zeroed s32 partial-sum buffer
+        ws_bytes = lib().xnc_umma_split_ws_bytes(N, C, H, W, filt.O, filt.kh, filt.kw, pad)
+        split_ws = torch.zeros(ws_bytes // 4, dtype=torch.int32, device=dev) if ws_bytes else None
+        check(lib().xnc_xnor_conv_umma_ws(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), _ptr(K),
+                                          filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
+                                          _ptr(osc), _ptr(osh), _ptr(split_ws), _ptr(y), _ptr(acc),
+                                          _stream(dev)),
               "xnc_xnor_conv_umma")
     else:
         check(lib().xnc_xnor_conv_variant(VARIANTS[variant], bits.data_ptr(), filt.wbits.data_ptr(),

@@ -147,7 +147,10 @@ UMMA_CASES = RANDOM_CASES + [(2, 256, 14, 14, 64, 3, 3, 1), (1, 128, 20, 20, 300
                              # two blocks with a tail, 7x7 taps, rows wider than a quarter tile
                              (1, 64, 56, 56, 256, 3, 3, 1), (2, 32, 23, 17, 250, 3, 3, 1),
                              (1, 48, 15, 30, 500, 5, 5, 2), (1, 32, 20, 20, 256, 7, 7, 3),
-                             (2, 128, 8, 64, 256, 3, 3, 1), (3, 16, 2, 3, 256, 2, 2, 1)]
+                             (2, 128, 8, 64, 256, 3, 3, 1), (3, 16, 2, 3, 256, 2, 2, 1),
+                             # fewer work units than CTA pairs: K split over the pairs (4 and 3 K
+                             # blocks), partial sums added in any order, then the finalize kernel
+                             (1, 512, 8, 8, 256, 3, 3, 1), (1, 384, 5, 5, 64, 3, 3, 1)]
 
 
 @pytest.mark.parametrize("shape", UMMA_CASES, ids=lambda s: "x".join(map(str, s)))
