@@ -133,6 +133,13 @@ int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* s
                           as_stream(stream));
 }
 
+int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, float* out,
+                 void* stream) {
+  if (!x || !out || N < 1 || C < 1 || pool_k < 1 || pool_k > 8 || pool_s < 1 || Hin < pool_k || Win < pool_k)
+    return XNC_EINVAL;
+  return launch_max_pool(x, N, C, Hin, Win, pool_k, pool_s, out, as_stream(stream));
+}
+
 size_t xnc_umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
   if (O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return 0;
   return umma_split_ws_bytes(N, C, H, W, O, kh, kw, pad);

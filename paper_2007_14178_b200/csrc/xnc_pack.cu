@@ -13,6 +13,7 @@
 // channels with 16-byte loads; a warp's load is 512 contiguous bytes per
 // channel (fully coalesced), and x is read exactly once.  The bits for 32
 // channels are built in registers and written as one word per pixel.
+#include <algorithm>
 #include <type_traits>
 
 #include "xnc_common.cuh"
@@ -173,8 +174,7 @@ __global__ void k_absmean(const float* __restrict__ x, int C, int HW, long npix,
   const float* xp = x + n * C * (long)HW + p;
   float s = 0.0f;
   // The sum is one sequential f32 chain per pixel (bit-exactness), so the loads
-  // are issued in batches of 8 ahead of the adds; a plain loop waited out one
-  // memory latency per few channels (fc7, 4096 channels: 80 us -> ~10 us).
+  // are issued in batches of 8 ahead of the adds.
   if (HW == 1 && (C & 31) == 0 && ((reinterpret_cast<uintptr_t>(xp) & 15) == 0) && in_scale == nullptr) {
     for (int c = 0; c < C; c += 32) {  // channels contiguous: 16-byte loads, same sequential order
       float4 v[8];
@@ -252,6 +252,54 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   };
   if (aff) pick(std::true_type{});
   else pick(std::false_type{});
+  return launch_status();
+}
+
+// Max-pool (kernel pk, stride ps, no padding) of every channel plane, for layers
+// whose input is pooled first (XNOR-Net: pool -> BN -> sign).  One thread per
+// output element in NCHW order, so a warp's window loads are short strided
+// spans of the same input rows (L1 serves the 3x3 / 2 overlap); torch's rule
+// (a later element replaces the max when greater, or NaN), row-major window
+// order, so the pooled values are those of torch.max_pool2d.  (Folding the pool
+// into K1's per-pixel channel walk measured slower: that walk is one sequential
+// chain per pixel and the pooled layers have few pixels.)
+template <int PK>
+__global__ void k_max_pool(const float* __restrict__ x, long planes, int Hin, int Win, int Ho, int Wo, int pk_rt,
+                           int ps, float* __restrict__ out) {
+  const int pk = PK > 0 ? PK : pk_rt;
+  const long total = planes * Ho * Wo;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long pl = i / (Ho * Wo);
+    const int r = (int)(i - pl * (Ho * Wo));
+    const int oy = r / Wo, ox = r - oy * Wo;
+    const float* b = x + pl * Hin * Win + (oy * ps) * Win + ox * ps;
+    float m = __ldg(b);
+#pragma unroll
+    for (int dy = 0; dy < (PK > 0 ? PK : 8); ++dy) {
+      if (PK == 0 && dy >= pk) break;
+#pragma unroll
+      for (int dx = 0; dx < (PK > 0 ? PK : 8); ++dx) {
+        if (PK == 0 && dx >= pk) break;
+        const float v = __ldg(b + dy * Win + dx);
+        if (v > m || v != v) m = v;
+      }
+    }
+    out[i] = m;
+  }
+}
+
+int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, float* out,
+                    cudaStream_t s) {
+  if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
+  const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
+  const long planes = (long)N * C, total = planes * Ho * Wo;
+  const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
+  if (pk == 3)
+    k_max_pool<3><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, out);
+  else if (pk == 2)
+    k_max_pool<2><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, out);
+  else
+    k_max_pool<0><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, out);
   return launch_status();
 }
 

@@ -26,11 +26,13 @@ class XnorConv2d:
     """Binary conv layer with packed weights resident on one device."""
 
     def __init__(self, weight: torch.Tensor, pad: int | None = None, variant: str = "popc",
-                 in_affine=None, out_affine=None):
+                 in_affine=None, out_affine=None, in_pool=None):
         """in_affine = (scale, shift) f32 [C]: the layer binarizes x*scale + shift
         (a folded batch norm in front of the sign, computed inside K1); out_affine =
         (scale, shift) f32 [O]: y*scale + shift is written instead of y (the next
-        binary layer's batch norm, fused into the conv epilogue)."""
+        binary layer's batch norm, fused into the conv epilogue); in_pool = (kernel,
+        stride): the input is max-pooled first (no padding, xnc_max_pool) --
+        forward() then takes the pre-pool tensor."""
         if weight.dim() != 4:
             raise ValueError(f"weight must be [O, C, kh, kw], got {tuple(weight.shape)}")
         O, C, kh, kw = weight.shape
@@ -55,14 +57,20 @@ class XnorConv2d:
             t.detach().to(device=dev, dtype=torch.float32).contiguous() for t in in_affine)
         self.out_affine = None if out_affine is None else tuple(
             t.detach().to(device=dev, dtype=torch.float32).contiguous() for t in out_affine)
+        self.in_pool = None if in_pool is None else (int(in_pool[0]), int(in_pool[1]))
         self._ws: dict[tuple, torch.Tensor] = {}
 
     @property
     def alpha64(self) -> torch.Tensor:
         return self.filters.alpha64
 
-    def out_shape(self, x_shape) -> tuple[int, int, int, int]:
+    def conv_in_shape(self, x_shape) -> tuple[int, int, int, int]:
+        """The shape the convolution sees: x's, after the optional input pool."""
         N, C, H, W = x_shape
+        return (N, C) + ops.pool_dims(H, W, self.in_pool)
+
+    def out_shape(self, x_shape) -> tuple[int, int, int, int]:
+        N, C, H, W = self.conv_in_shape(x_shape)
         oh, ow = ops.out_dims(H, W, self.kh, self.kw, self.pad)
         if oh < 1 or ow < 1:
             raise ValueError("kernel larger than the padded input")
@@ -96,15 +104,15 @@ class XnorConv2d:
 
     def _forward_device(self, x: torch.Tensor, out: torch.Tensor | None = None,
                         want_acc: bool = False):
-        variant = self.kernel_for(x.shape)
+        variant = self.kernel_for(self.conv_in_shape(x.shape))
         if variant in ("popc-fc", "umma-fc"):
             return self._forward_fc(x, out, want_acc, variant)
-        plain = self.in_affine is None and self.out_affine is None
+        plain = self.in_affine is None and self.out_affine is None and self.in_pool is None
         if variant == "popc" and not want_acc and plain:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
         if variant == "umma" and not want_acc and plain:  # one C-ABI call: K1 -> K2 -> tcgen05 K3+K4
             return ops.layer_forward_umma(x, self.filters, self.pad, self.workspace(x), y=out)
-        bits, A = ops.pack_input(x, in_affine=self.in_affine)
+        bits, A = ops.pack_input(x, in_affine=self.in_affine, in_pool=self.in_pool)
         K = ops.scale_map(A, self.kh, self.kw, self.pad)
         y, acc = ops.xnor_conv(bits, self.filters, K, self.pad, want_acc=want_acc,
                                variant=variant, y=out, out_affine=self.out_affine)
@@ -140,8 +148,8 @@ class XnorConv2d:
         the image, so the conv kernels' pixel tiling runs over the batch.  Same
         arithmetic as the conv view: C' = kh*kw*C valid bits, K = box mean of A
         over the whole input, alpha per filter (the reference's (c, ky, kx) sum)."""
-        N, C, H, W = x.shape
-        bits, A = ops.pack_input(x, in_affine=self.in_affine)
+        N, C, H, W = self.conv_in_shape(x.shape)
+        bits, A = ops.pack_input(x, in_affine=self.in_affine, in_pool=self.in_pool)
         K = ops.scale_map(A, self.kh, self.kw, 0)                     # [N, 1, 1]
         fcf = self._fc_filters(umma=variant == "umma-fc")
         y1, acc1 = ops.xnor_conv(bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,

@@ -9,11 +9,11 @@ path:
     conv1  11x11/4, 3 -> 96      full precision      224 -> 55  (as 3x3 over 4x4 space-to-depth)
     pool   3/2                                       55 -> 27
     bn2 -> conv2  5x5 pad 2, 96 -> 256  BINARY (XnorConv2d) 27
-    pool   3/2                                       27 -> 13
+    pool   3/2                                       27 -> 13  (conv3's in_pool: xnc_max_pool)
     bn3 -> conv3  3x3 pad 1, 256 -> 384 BINARY       13  (epilogue applies bn4)
     conv4  3x3 pad 1, 384 -> 384 BINARY              13  (epilogue applies bn5)
     conv5  3x3 pad 1, 384 -> 256 BINARY              13
-    pool   3/2                                       13 -> 6
+    pool   3/2                                       13 -> 6   (fc6's in_pool)
     bn6 -> fc6  6x6 valid, 256 -> 4096 BINARY (a k = H = W conv)  1x1  (epilogue applies bn7)
     fc7    1x1, 4096 -> 4096     BINARY              1x1
     fc8    4096 -> 1000          full precision
@@ -55,6 +55,7 @@ BINARY_LAYERS = (  # name, C_in, C_out, k, pad
     ("fc6", 256, 4096, 6, 0),
     ("fc7", 4096, 4096, 1, 0),
 )
+POOLED_INPUT = ("conv3", "fc6")  # layers whose input is max-pool 3/2 of the previous output
 BINARY_MACS_PER_IMAGE = (27 * 27 * 256 * 96 * 25 + 13 * 13 * 384 * 256 * 9 + 13 * 13 * 384 * 384 * 9
                          + 13 * 13 * 256 * 384 * 9 + 4096 * 256 * 36 + 4096 * 4096)
 
@@ -100,8 +101,10 @@ class XnorNetAlexNet:
         for name, cin, cout, k, pad in BINARY_LAYERS:
             in_aff = None if name in fused_out.values() else self.bn[name]
             out_aff = self.bn[fused_out[name]] if name in fused_out else None
+            # the max-pools after conv2 / conv5 are the next layer's in_pool (our pool kernel)
+            in_pool = (3, 2) if name in POOLED_INPUT else None
             self.binary[name] = XnorConv2d(rnd(cout, cin, k, k), pad=pad, variant=variant,
-                                           in_affine=in_aff, out_affine=out_aff)
+                                           in_affine=in_aff, out_affine=out_aff, in_pool=in_pool)
         self.fc8_w = rnd(num_classes, 4096, scale=4096 ** -0.5)
         self.fc8_b = rnd(num_classes, scale=0.1)
 
@@ -128,10 +131,9 @@ class XnorNetAlexNet:
         h = self.front_end(x)
         feats = {}
         for name, *_ in BINARY_LAYERS:
+            # conv3 / fc6 take the pre-pool map (their in_pool)
             h = self.binary[name](h.contiguous())
             feats[name] = h
-            if name in ("conv2", "conv5"):
-                h = F.max_pool2d(h, 3, 2)
         logits = F.linear(h.flatten(1), self.fc8_w, self.fc8_b)  # full precision
         return (logits, feats) if return_features else logits
 

@@ -54,12 +54,39 @@ def _affine(aff, n: int, device, what: str):
     return sc, sh
 
 
-def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None):
+def pool_dims(H: int, W: int, in_pool) -> tuple[int, int]:
+    """Spatial dims after the optional input max-pool (kernel, stride), no padding."""
+    if in_pool is None:
+        return H, W
+    k, s = in_pool
+    if k < 1 or s < 1 or H < k or W < k:
+        raise ValueError(f"pool {in_pool} does not fit a {H}x{W} input")
+    return (H - k) // s + 1, (W - k) // s + 1
+
+
+def max_pool(x: torch.Tensor, k: int, s: int) -> torch.Tensor:
+    """Max-pool k x k / stride s, no padding (torch.max_pool2d values), on the device."""
+    _need_cuda(x, "x", torch.float32)
+    x = x.contiguous()
+    N, C, H, W = x.shape
+    Ho, Wo = pool_dims(H, W, (k, s))
+    out = torch.empty((N, C, Ho, Wo), dtype=torch.float32, device=x.device)
+    check(lib().xnc_max_pool(x.data_ptr(), N, C, H, W, int(k), int(s), out.data_ptr(), _stream(x.device)),
+          "xnc_max_pool")
+    return out
+
+
+def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None, in_pool=None):
     """K1: x f32 [N,C,H,W] -> (bits i32 [N,H,W,Cw] (u32 payload), A f32 [N,H,W]).
 
     in_affine = (scale, shift) f32 [C]: binarize and average x*scale + shift (one
-    rounding per op) instead of x -- a folded batch norm before the sign."""
+    rounding per op) instead of x -- a folded batch norm before the sign.
+    in_pool = (kernel, stride): x is the pre-pool tensor, max-pooled first (no
+    padding; xnc_max_pool) -- XNOR-Net's pool -> BN -> sign; bits / A then have the
+    pooled spatial shape."""
     _need_cuda(x, "x", torch.float32)
+    if in_pool is not None:
+        x = max_pool(x, *in_pool)
     N, C, H, W = x.shape
     bits = torch.empty((N, H, W, words(C)), dtype=torch.int32, device=x.device)
     A = torch.empty((N, H, W), dtype=torch.float32, device=x.device) if want_A else None

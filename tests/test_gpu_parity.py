@@ -313,3 +313,40 @@ def test_bn_affines_in_k1_and_epilogue(shape, variant):
     want = ((want * osc.reshape(1, -1, 1, 1)).astype(np.float32) + osh.reshape(1, -1, 1, 1)).astype(np.float32)
     assert np.array_equal(y.view(np.uint32), want.view(np.uint32))
 
+
+
+@pytest.mark.parametrize("shape", [(3, 256, 27, 27, 3, 2), (2, 70, 13, 13, 3, 2), (2, 64, 9, 12, 2, 2),
+                                   (4, 4096, 3, 3, 3, 1)], ids=lambda s: "x".join(map(str, s)))
+def test_pooled_input_k1(shape):
+    """K1 over a max-pooled input (xnc_max_pool): pooled values identical to
+    torch.max_pool2d, bits and A identical to K1 on that map, with and without the
+    folded BN."""
+    import torch.nn.functional as F
+    from paper_2007_14178_b200 import ops
+    N, C, H, W, k, s = shape
+    rng = np.random.default_rng(list(shape))
+    x = torch.from_numpy(O.f32_exact(rng, (N, C, H, W))).to(_dev())
+    x[0, 0, 0, :2] = 0.0  # exact zeros and a negative zero inside pooled windows
+    x[0, 1, 1, 1] = -0.0
+    pooled = F.max_pool2d(x, k, s).contiguous()
+    assert torch.equal(ops.max_pool(x, k, s).view(torch.int32), pooled.view(torch.int32))
+    for aff in (None, (torch.rand(C, device=_dev()) + 0.5, torch.rand(C, device=_dev()) - 0.5)):
+        b1, a1 = ops.pack_input(x, in_affine=aff, in_pool=(k, s))
+        b2, a2 = ops.pack_input(pooled, in_affine=aff)
+        assert torch.equal(b1, b2)
+        assert torch.equal(a1.view(torch.int32), a2.view(torch.int32))
+
+
+def test_layer_in_pool_matches_pooled_layer():
+    """XnorConv2d(in_pool) on the pre-pool map == the same layer on the pooled map."""
+    import torch.nn.functional as F
+    from paper_2007_14178_b200 import XnorConv2d
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(O.f32_exact(rng, (4, 96, 27, 27))).to(_dev())
+    w = torch.from_numpy(O.f32_exact(rng, (128, 96, 3, 3))).to(_dev())
+    a = XnorConv2d(w, pad=1, variant="auto", in_pool=(3, 2))
+    b = XnorConv2d(w, pad=1, variant="auto")
+    ya = a.forward(x)
+    yb = b.forward(F.max_pool2d(x, 3, 2).contiguous())
+    assert ya.shape == (4, 128, 13, 13)
+    assert torch.equal(ya.view(torch.int32), yb.view(torch.int32))

@@ -23,7 +23,7 @@ def main():
         net(x)
     torch.cuda.synchronize()
     reps = 10
-    names = ["front_end"] + [n for n, *_ in BINARY_LAYERS] + ["pool2", "pool5", "fc8"]
+    names = ["front_end"] + [n for n, *_ in BINARY_LAYERS] + ["fc8"]  # pools run inside conv3 / fc6
     acc = {n: 0.0 for n in names}
     with torch.no_grad(), _tf32_full_precision_layers():
         for _ in range(reps):
@@ -39,9 +39,6 @@ def main():
             for name, *_ in BINARY_LAYERS:
                 h = net.binary[name](h.contiguous())
                 mark(name)
-                if name in ("conv2", "conv5"):
-                    h = F.max_pool2d(h, 3, 2)
-                    mark("pool2" if name == "conv2" else "pool5")
             F.linear(h.flatten(1), net.fc8_w, net.fc8_b)
             mark("fc8")
             torch.cuda.synchronize()
