@@ -116,12 +116,18 @@ int xnc_xnor_conv_umma_affine(const uint32_t* bits, const uint8_t* wq, const int
                               const float* K, const float* alpha, int N, int C, int H, int W,
                               int O, int kh, int kw, int pad, const float* out_scale,
                               const float* out_shift, float* y, int32_t* acc, void* stream);
-/* Max-pool in front of a binary layer (XNOR-Net: pool -> BN -> sign): out f32
+/* ---- network data movement (XNOR-Net AlexNet forward, network.py) ----------
+ * Max-pool in front of a binary layer (XNOR-Net: pool -> BN -> sign): out f32
  * [N][C][H][W] = max over pool_k x pool_k windows (stride pool_s, no padding) of
  * x [N][C][Hin][Win], H = (Hin - pool_k) / pool_s + 1; the values of
- * torch.max_pool2d (NaN propagates).  pool_k <= 8. */
-int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, float* out,
-                 void* stream);
+ * torch.max_pool2d (NaN propagates); relu != 0: torch.relu before the pool, in
+ * the same pass.  pool_k <= 8. */
+int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu,
+                 float* out, void* stream);
+/* F.pixel_unshuffle(F.pad(x, pad on all sides), r) in one pass: out f32
+ * [N][C*r*r][(H+2pad)/r][(W+2pad)/r] (conv1 11x11/4 as a 3x3 conv, network.py). */
+int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, int r, float* out,
+                           void* stream);
 /* K split for shapes with fewer (pixel tile, 256-filter block) work units than CTA
  * pairs -- fully connected layers viewed as one 1 x N image.  Units of one output
  * tile take disjoint K ranges and add their raw partial sums into split_ws

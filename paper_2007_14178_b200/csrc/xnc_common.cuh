@@ -56,6 +56,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
                      float* y, int32_t* acc, cudaStream_t s, const float* out_scale = nullptr,
                      const float* out_shift = nullptr, int32_t* split_ws = nullptr);
 size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad);
-int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, float* out,
+int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
                     cudaStream_t s);
+int launch_pad_s2d(const float* x, int N, int C, int H, int W, int p, int r, float* out, cudaStream_t s);
 }  // namespace xnc

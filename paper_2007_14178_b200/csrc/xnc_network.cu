@@ -1,0 +1,93 @@
+// Data-movement kernels around the binary layers of the XNOR-Net AlexNet forward
+// (network.py): the max-pools (fused with the ReLU in front of them where the
+// network has one) and conv1's pad + space-to-depth.  Pure data movement and
+// max selection: the values are exactly those of the torch ops they replace.
+#include <algorithm>
+
+#include "xnc_common.cuh"
+
+namespace xnc {
+
+// Max-pool (kernel pk, stride ps, no padding) of every channel plane.  One thread
+// per output element in NCHW order, so a warp's window loads are short strided
+// spans of the same input rows (L1 serves the 3x3 / 2 overlap).  torch's rule (a
+// later element replaces the max when greater, or NaN) in row-major window order,
+// so the values are torch.max_pool2d's; relu != 0 applies torch's relu after the
+// max (relu(max(w)) == max(relu(w)): the ReLU + pool of conv1 in one pass).
+template <int PK>
+__global__ void k_max_pool(const float* __restrict__ x, long planes, int Hin, int Win, int Ho, int Wo, int pk_rt,
+                           int ps, int relu, float* __restrict__ out) {
+  const int pk = PK > 0 ? PK : pk_rt;
+  const long total = planes * Ho * Wo;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long pl = i / (Ho * Wo);
+    const int r = (int)(i - pl * (Ho * Wo));
+    const int oy = r / Wo, ox = r - oy * Wo;
+    const float* b = x + pl * Hin * Win + (oy * ps) * Win + ox * ps;
+    float m = __ldg(b);
+#pragma unroll
+    for (int dy = 0; dy < (PK > 0 ? PK : 8); ++dy) {
+      if (PK == 0 && dy >= pk) break;
+#pragma unroll
+      for (int dx = 0; dx < (PK > 0 ? PK : 8); ++dx) {
+        if (PK == 0 && dx >= pk) break;
+        const float v = __ldg(b + dy * Win + dx);
+        if (v > m || v != v) m = v;
+      }
+    }
+    if (relu && m < 0.0f) m = 0.0f;  // clamp_min(0): NaN and -0.0 pass through
+    out[i] = m;
+  }
+}
+
+int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
+                    cudaStream_t s) {
+  if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
+  const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
+  const long planes = (long)N * C, total = planes * Ho * Wo;
+  const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
+  if (pk == 3)
+    k_max_pool<3><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, relu, out);
+  else if (pk == 2)
+    k_max_pool<2><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, relu, out);
+  else
+    k_max_pool<0><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, relu, out);
+  return launch_status();
+}
+
+// Zero pad by p on every side, then space-to-depth by r (torch's F.pad followed by
+// F.pixel_unshuffle(., r)): out[n][(c*r + i)*r + j][y][x] = x_pad[n][c][y*r + i][x*r + j],
+// out spatial (H + 2p) / r x (W + 2p) / r.  One pass instead of two copies.  A
+// thread takes r consecutive elements of one padded input row (read together) and
+// writes one element to each of the r output planes j: for a fixed j, consecutive
+// threads write consecutive floats.  32-bit index math (host-checked sizes).
+__global__ void k_pad_s2d(const float* __restrict__ x, int C, int H, int W, int p, int r, int Hp, int Ho,
+                          int Wo, int total, float* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int xo = i % Wo;
+    int t = i / Wo;
+    const int Y = t % Hp;
+    t /= Hp;
+    const int c = t % C, n = t / C;
+    const int yi = Y - p, ii = Y % r, yo = Y / r;
+    const bool row_in = yi >= 0 && yi < H;
+    const float* src = x + ((long)(n * C + c) * H + (row_in ? yi : 0)) * W;
+    float* dst = out + ((long)(n * C + c) * r * r + ii * r) * Ho * Wo + (long)yo * Wo + xo;
+    for (int j = 0; j < r; ++j) {
+      const int xi = xo * r + j - p;
+      dst[(long)j * Ho * Wo] = (row_in && xi >= 0 && xi < W) ? __ldg(src + xi) : 0.0f;
+    }
+  }
+}
+
+int launch_pad_s2d(const float* x, int N, int C, int H, int W, int p, int r, float* out, cudaStream_t s) {
+  if (r < 1 || p < 0 || (H + 2 * p) % r || (W + 2 * p) % r) return XNC_EINVAL;
+  const int Hp = H + 2 * p, Ho = Hp / r, Wo = (W + 2 * p) / r;
+  const long total = (long)N * C * Hp * Wo;
+  if (total >= 0x7fffffffL || (long)N * C * r * r * Ho * Wo >= 0x7fffffffL) return XNC_ENOTSUP;
+  const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
+  k_pad_s2d<<<blocks, 256, 0, s>>>(x, C, H, W, p, r, Hp, Ho, Wo, (int)total, out);
+  return launch_status();
+}
+
+}  // namespace xnc

@@ -198,6 +198,44 @@ __global__ void k_absmean(const float* __restrict__ x, int C, int HW, long npix,
   A[q] = __fmul_rn(s, inv);
 }
 
+// A for 1x1 images with long channel vectors (the fc7 input, 4096 channels): the
+// sum is one sequential chain per pixel, so one thread per pixel left all but a
+// couple of SMs idle and waited out a memory latency per few channels.  Here a
+// warp per pixel streams 1024-channel chunks into shared memory (the next chunk's
+// loads in flight while lane 0 runs the chain over the current one, in channel
+// order; the folded BN, if any, is applied by the loading lanes, the same two
+// roundings).
+constexpr int kAbsChunk = 1024;
+__global__ void __launch_bounds__(128) k_absmean_wide(const float* __restrict__ x, int C, long npix, float inv,
+                                                      float* __restrict__ A, const float* __restrict__ in_scale,
+                                                      const float* __restrict__ in_shift) {
+  __shared__ float buf[4][kAbsChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long q = (long)blockIdx.x * 4 + warp;
+  if (q >= npix) return;
+  const float* xp = x + q * C;
+  float* b = buf[warp];
+  float s = 0.0f;
+  for (int c0 = 0; c0 < C; c0 += kAbsChunk) {
+    const int n = min(kAbsChunk, C - c0);
+    float v[kAbsChunk / 32];
+#pragma unroll
+    for (int u = 0; u < kAbsChunk / 32; ++u) {
+      const int c = u * 32 + lane;
+      v[u] = c < n ? fabsf(affine_in(__ldg(xp + c0 + c), in_scale, in_shift, c0 + c)) : 0.0f;
+    }
+    __syncwarp();  // lane 0 is done with the previous chunk
+#pragma unroll
+    for (int u = 0; u < kAbsChunk / 32; ++u) b[u * 32 + lane] = v[u];
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll 16
+      for (int i = 0; i < n; ++i) s = __fadd_rn(s, b[i]);
+    }
+  }
+  if (lane == 0) A[q] = __fmul_rn(s, inv);
+}
+
 int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
                       cudaStream_t s, const float* in_scale, const float* in_shift) {
   {
@@ -209,7 +247,10 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
       const long words = npix * Cw;
       k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, in_scale,
                                                               in_shift);
-      if (A)
+      if (A && H * W == 1 && C >= 1024)
+        k_absmean_wide<<<(unsigned)cdivl(npix, 4), 128, 0, s>>>(x, C, npix, (float)(1.0 / (double)C), A, in_scale,
+                                                                in_shift);
+      else if (A)
         k_absmean<<<(unsigned)cdivl(npix, 128), 128, 0, s>>>(x, C, H * W, npix, (float)(1.0 / (double)C), A,
                                                              in_scale, in_shift);
       return launch_status();
@@ -252,54 +293,6 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   };
   if (aff) pick(std::true_type{});
   else pick(std::false_type{});
-  return launch_status();
-}
-
-// Max-pool (kernel pk, stride ps, no padding) of every channel plane, for layers
-// whose input is pooled first (XNOR-Net: pool -> BN -> sign).  One thread per
-// output element in NCHW order, so a warp's window loads are short strided
-// spans of the same input rows (L1 serves the 3x3 / 2 overlap); torch's rule
-// (a later element replaces the max when greater, or NaN), row-major window
-// order, so the pooled values are those of torch.max_pool2d.  (Folding the pool
-// into K1's per-pixel channel walk measured slower: that walk is one sequential
-// chain per pixel and the pooled layers have few pixels.)
-template <int PK>
-__global__ void k_max_pool(const float* __restrict__ x, long planes, int Hin, int Win, int Ho, int Wo, int pk_rt,
-                           int ps, float* __restrict__ out) {
-  const int pk = PK > 0 ? PK : pk_rt;
-  const long total = planes * Ho * Wo;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const long pl = i / (Ho * Wo);
-    const int r = (int)(i - pl * (Ho * Wo));
-    const int oy = r / Wo, ox = r - oy * Wo;
-    const float* b = x + pl * Hin * Win + (oy * ps) * Win + ox * ps;
-    float m = __ldg(b);
-#pragma unroll
-    for (int dy = 0; dy < (PK > 0 ? PK : 8); ++dy) {
-      if (PK == 0 && dy >= pk) break;
-#pragma unroll
-      for (int dx = 0; dx < (PK > 0 ? PK : 8); ++dx) {
-        if (PK == 0 && dx >= pk) break;
-        const float v = __ldg(b + dy * Win + dx);
-        if (v > m || v != v) m = v;
-      }
-    }
-    out[i] = m;
-  }
-}
-
-int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, float* out,
-                    cudaStream_t s) {
-  if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
-  const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
-  const long planes = (long)N * C, total = planes * Ho * Wo;
-  const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
-  if (pk == 3)
-    k_max_pool<3><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, out);
-  else if (pk == 2)
-    k_max_pool<2><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, out);
-  else
-    k_max_pool<0><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, out);
   return launch_status();
 }
 

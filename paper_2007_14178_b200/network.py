@@ -30,6 +30,7 @@ import contextlib
 import torch
 import torch.nn.functional as F
 
+from . import ops
 from .layer import XnorConv2d
 
 
@@ -124,8 +125,10 @@ class XnorNetAlexNet:
         -> max-pool 3/2: the input of the first binary layer (the same cuDNN
         settings as inside forward())."""
         with _tf32_full_precision_layers():
-            h = F.conv2d(F.pixel_unshuffle(F.pad(x, (2, 2, 2, 2)), 4), self.conv1_w_s2d, self.conv1_b)
-            return F.max_pool2d(F.relu_(h), 3, 2)
+            # pad + space-to-depth and ReLU + pool are one pass each (our data-movement
+            # kernels, same values as F.pad / F.pixel_unshuffle and F.relu / F.max_pool2d)
+            h = F.conv2d(ops.pad_space_to_depth(x, 2, 4), self.conv1_w_s2d, self.conv1_b)
+            return ops.max_pool(h, 3, 2, relu=True)
 
     def _forward(self, x: torch.Tensor, return_features: bool):
         h = self.front_end(x)

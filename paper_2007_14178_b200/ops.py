@@ -64,15 +64,30 @@ def pool_dims(H: int, W: int, in_pool) -> tuple[int, int]:
     return (H - k) // s + 1, (W - k) // s + 1
 
 
-def max_pool(x: torch.Tensor, k: int, s: int) -> torch.Tensor:
-    """Max-pool k x k / stride s, no padding (torch.max_pool2d values), on the device."""
+def max_pool(x: torch.Tensor, k: int, s: int, relu: bool = False) -> torch.Tensor:
+    """Max-pool k x k / stride s, no padding (torch.max_pool2d values), on the
+    device; relu=True: torch.relu first, in the same pass."""
     _need_cuda(x, "x", torch.float32)
     x = x.contiguous()
     N, C, H, W = x.shape
     Ho, Wo = pool_dims(H, W, (k, s))
     out = torch.empty((N, C, Ho, Wo), dtype=torch.float32, device=x.device)
-    check(lib().xnc_max_pool(x.data_ptr(), N, C, H, W, int(k), int(s), out.data_ptr(), _stream(x.device)),
-          "xnc_max_pool")
+    check(lib().xnc_max_pool(x.data_ptr(), N, C, H, W, int(k), int(s), int(bool(relu)), out.data_ptr(),
+                             _stream(x.device)), "xnc_max_pool")
+    return out
+
+
+def pad_space_to_depth(x: torch.Tensor, pad: int, r: int) -> torch.Tensor:
+    """F.pixel_unshuffle(F.pad(x, (pad,) * 4), r) in one device pass."""
+    _need_cuda(x, "x", torch.float32)
+    x = x.contiguous()
+    N, C, H, W = x.shape
+    if (H + 2 * pad) % r or (W + 2 * pad) % r:
+        raise ValueError(f"padded {H}x{W} input is not a multiple of {r}")
+    out = torch.empty((N, C * r * r, (H + 2 * pad) // r, (W + 2 * pad) // r), dtype=torch.float32,
+                      device=x.device)
+    check(lib().xnc_pad_space_to_depth(x.data_ptr(), N, C, H, W, int(pad), int(r), out.data_ptr(),
+                                       _stream(x.device)), "xnc_pad_space_to_depth")
     return out
 
 

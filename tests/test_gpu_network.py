@@ -57,3 +57,21 @@ def test_network_kernel_selection():
     ks = net.binary_kernels(256)
     assert ks["fc7"] in ("popc-fc", "umma-fc") and ks["fc6"] in ("popc-fc", "umma-fc")
     assert all(v in ("umma", "popc", "popc-fc", "umma-fc") for v in ks.values())
+
+
+@pytest.mark.parametrize("shape,pad,r", [((2, 3, 224, 224), 2, 4), ((3, 5, 10, 14), 1, 4), ((1, 2, 6, 6), 0, 2)])
+def test_pad_space_to_depth_matches_torch(shape, pad, r):
+    from paper_2007_14178_b200 import ops
+    x = torch.randn(shape, device="cuda")
+    want = F.pixel_unshuffle(F.pad(x, (pad,) * 4), r)
+    assert torch.equal(ops.pad_space_to_depth(x, pad, r), want)
+
+
+@pytest.mark.parametrize("shape,k,s", [((2, 96, 55, 55), 3, 2), ((3, 7, 9, 12), 2, 2), ((1, 4, 11, 11), 5, 3)])
+def test_relu_max_pool_matches_torch(shape, k, s):
+    from paper_2007_14178_b200 import ops
+    x = torch.randn(shape, device="cuda")
+    x[0, 0, :3, :3] = -1.0  # an all-negative window: relu -> 0
+    want = F.max_pool2d(F.relu(x), k, s)
+    assert torch.equal(ops.max_pool(x, k, s, relu=True), want)
+    assert torch.equal(ops.max_pool(x, k, s), F.max_pool2d(x, k, s))

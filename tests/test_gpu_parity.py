@@ -73,6 +73,20 @@ def test_pack_input_bits_and_absmean(C, HW):
         assert np.array_equal(A[n].cpu().numpy().view(np.uint32), A_ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("C", [1024, 2500, 4096])
+def test_pack_input_long_channel_vectors(C):
+    """1x1 images with long channel vectors (the fc7 input): A from the warp-per-pixel
+    kernel is the oracle's sequential f32 sum, bit for bit; bits exact."""
+    from paper_2007_14178_b200 import ops
+    rng = np.random.default_rng([C, 11])
+    x = O.f32_exact(rng, (5, C, 1, 1))
+    bits, A = ops.pack_input(torch.from_numpy(x).to(_dev()))
+    assert np.array_equal(_unpack_bits(bits.cpu().numpy(), C), O.signs(x))
+    for n in range(5):
+        A_ref, _ = O.scale_map_f32(x[n], 1, 1, 0)
+        assert np.array_equal(A[n].cpu().numpy().view(np.uint32), A_ref.view(np.uint32))
+
+
 @pytest.mark.parametrize("k,pad", [((1, 1), 0), ((3, 3), 1), ((3, 3), 0), ((5, 5), 2), ((7, 7), 3),
                                    ((3, 5), 2), ((8, 8), 3), ((2, 2), 1)])
 def test_scale_map_bit_exact(k, pad):
