@@ -123,11 +123,16 @@ int xnc_xnor_conv_umma_affine(const uint32_t* bits, const uint8_t* wq, const int
  * torch.max_pool2d (NaN propagates); relu != 0: torch.relu before the pool, in
  * the same pass.  pool_k <= 8. */
 int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu,
-                 float* out, void* stream);
+                 int nhwc, float* out, void* stream);
 /* F.pixel_unshuffle(F.pad(x, pad on all sides), r) in one pass: out f32
- * [N][C*r*r][(H+2pad)/r][(W+2pad)/r] (conv1 11x11/4 as a 3x3 conv, network.py). */
-int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, int r, float* out,
-                           void* stream);
+ * [N][C*r*r][(H+2pad)/r][(W+2pad)/r] (conv1 11x11/4 as a 3x3 conv, network.py).
+ * nhwc != 0 (xnc_max_pool too): the map is stored channels-last, [N][H][W][C]. */
+int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, int r, int nhwc,
+                           float* out, void* stream);
+/* K1 (xnc_pack_input_affine) for a channels-last input x f32 [N][H][W][C]: same
+ * bits / A, a thread per pixel walking its contiguous channels. */
+int xnc_pack_input_nhwc(const float* x, int N, int C, int H, int W, const float* in_scale,
+                        const float* in_shift, uint32_t* bits, float* A, void* stream);
 /* K split for shapes with fewer (pixel tile, 256-filter block) work units than CTA
  * pairs -- fully connected layers viewed as one 1 x N image.  Units of one output
  * tile take disjoint K ranges and add their raw partial sums into split_ws

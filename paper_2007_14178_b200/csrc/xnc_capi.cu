@@ -133,18 +133,26 @@ int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* s
                           as_stream(stream));
 }
 
-int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu, float* out,
-                 void* stream) {
+int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu, int nhwc,
+                 float* out, void* stream) {
   if (!x || !out || N < 1 || C < 1 || pool_k < 1 || pool_k > 8 || pool_s < 1 || Hin < pool_k || Win < pool_k)
     return XNC_EINVAL;
-  return launch_max_pool(x, N, C, Hin, Win, pool_k, pool_s, relu, out, as_stream(stream));
+  return nhwc ? launch_max_pool_nhwc(x, N, C, Hin, Win, pool_k, pool_s, relu, out, as_stream(stream))
+              : launch_max_pool(x, N, C, Hin, Win, pool_k, pool_s, relu, out, as_stream(stream));
 }
 
-int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, int r, float* out, void* stream) {
+int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, int r, int nhwc, float* out,
+                           void* stream) {
   if (!x || !out || N < 1 || C < 1 || H < 1 || W < 1 || pad < 0 || r < 1 || (H + 2 * pad) % r ||
       (W + 2 * pad) % r)
     return XNC_EINVAL;
-  return launch_pad_s2d(x, N, C, H, W, pad, r, out, as_stream(stream));
+  return launch_pad_s2d(x, N, C, H, W, pad, r, nhwc, out, as_stream(stream));
+}
+
+int xnc_pack_input_nhwc(const float* x, int N, int C, int H, int W, const float* in_scale, const float* in_shift,
+                        uint32_t* bits, float* A, void* stream) {
+  if (!x || !bits || N < 1 || C < 1 || H < 1 || W < 1 || (!in_scale != !in_shift)) return XNC_EINVAL;
+  return launch_pack_input_nhwc(x, N, C, H, W, bits, A, as_stream(stream), in_scale, in_shift);
 }
 
 size_t xnc_umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {

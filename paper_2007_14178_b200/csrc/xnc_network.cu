@@ -40,6 +40,41 @@ __global__ void k_max_pool(const float* __restrict__ x, long planes, int Hin, in
   }
 }
 
+// The same pool on channels-last (NHWC) maps, output NHWC: one thread per output
+// element with the channel fastest, so window loads and stores are coalesced.
+__global__ void k_max_pool_nhwc(const float* __restrict__ x, int C, int Hin, int Win, int Ho, int Wo, int pk,
+                                int ps, int relu, int total, float* __restrict__ out) {
+  // 32-bit index math (host-checked): 64-bit div/mod made this pass 3x slower
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c = i % C;
+    int t = i / C;
+    const int ox = t % Wo;
+    t /= Wo;
+    const int oy = t % Ho;
+    const int n = t / Ho;
+    const float* b = x + ((long)(n * Hin + oy * ps) * Win + ox * ps) * C + c;
+    float m = __ldg(b);
+    for (int dy = 0; dy < pk; ++dy)
+      for (int dx = 0; dx < pk; ++dx) {
+        const float v = __ldg(b + ((long)dy * Win + dx) * C);
+        if (v > m || v != v) m = v;
+      }
+    if (relu && m < 0.0f) m = 0.0f;
+    out[i] = m;
+  }
+}
+
+int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
+                         cudaStream_t s) {
+  if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
+  const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
+  const long total = (long)N * Ho * Wo * C;
+  if (total >= 0x7fffffffL || (long)N * Hin * Win * C >= 0x7fffffffL) return XNC_ENOTSUP;
+  const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
+  k_max_pool_nhwc<<<blocks, 256, 0, s>>>(x, C, Hin, Win, Ho, Wo, pk, ps, relu, (int)total, out);
+  return launch_status();
+}
+
 int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
                     cudaStream_t s) {
   if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
@@ -57,12 +92,15 @@ int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int 
 
 // Zero pad by p on every side, then space-to-depth by r (torch's F.pad followed by
 // F.pixel_unshuffle(., r)): out[n][(c*r + i)*r + j][y][x] = x_pad[n][c][y*r + i][x*r + j],
-// out spatial (H + 2p) / r x (W + 2p) / r.  One pass instead of two copies.  A
-// thread takes r consecutive elements of one padded input row (read together) and
-// writes one element to each of the r output planes j: for a fixed j, consecutive
-// threads write consecutive floats.  32-bit index math (host-checked sizes).
+// out spatial (H + 2p) / r x (W + 2p) / r, stored NCHW or, nhwc != 0, channels-last
+// (what cuDNN's fastest conv kernels read).  One pass instead of two copies.  A
+// thread takes r consecutive elements of one padded input row and writes one
+// element to each of the r output channels j (NCHW: for a fixed j consecutive
+// threads write consecutive floats; NHWC: the thread's r outputs are adjacent).
+// 32-bit index math (host-checked sizes).
 __global__ void k_pad_s2d(const float* __restrict__ x, int C, int H, int W, int p, int r, int Hp, int Ho,
-                          int Wo, int total, float* __restrict__ out) {
+                          int Wo, int total, int nhwc, float* __restrict__ out) {
+  const int Co = C * r * r;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int xo = i % Wo;
     int t = i / Wo;
@@ -72,21 +110,54 @@ __global__ void k_pad_s2d(const float* __restrict__ x, int C, int H, int W, int 
     const int yi = Y - p, ii = Y % r, yo = Y / r;
     const bool row_in = yi >= 0 && yi < H;
     const float* src = x + ((long)(n * C + c) * H + (row_in ? yi : 0)) * W;
-    float* dst = out + ((long)(n * C + c) * r * r + ii * r) * Ho * Wo + (long)yo * Wo + xo;
+    const int co0 = (c * r + ii) * r;
+    float* dst;
+    long jstride;
+    if (nhwc) {
+      dst = out + (((long)n * Ho + yo) * Wo + xo) * Co + co0;
+      jstride = 1;
+    } else {
+      dst = out + ((long)n * Co + co0) * Ho * Wo + (long)yo * Wo + xo;
+      jstride = (long)Ho * Wo;
+    }
     for (int j = 0; j < r; ++j) {
       const int xi = xo * r + j - p;
-      dst[(long)j * Ho * Wo] = (row_in && xi >= 0 && xi < W) ? __ldg(src + xi) : 0.0f;
+      dst[j * jstride] = (row_in && xi >= 0 && xi < W) ? __ldg(src + xi) : 0.0f;
     }
   }
 }
 
-int launch_pad_s2d(const float* x, int N, int C, int H, int W, int p, int r, float* out, cudaStream_t s) {
+// Channels-last output: one thread per output element in memory order (channel
+// fastest), so the stores are fully coalesced; a warp's reads are r-float runs of a
+// few input rows that neighbouring pixels share through L1.
+__global__ void k_pad_s2d_nhwc(const float* __restrict__ x, int C, int H, int W, int p, int r, int Ho, int Wo,
+                               int total, float* __restrict__ out) {
+  const int Co = C * r * r;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int co = i % Co;
+    int t = i / Co;
+    const int xo = t % Wo;
+    t /= Wo;
+    const int yo = t % Ho, n = t / Ho;
+    const int c = co / (r * r), ij = co - c * r * r, ii = ij / r, jj = ij - ii * r;
+    const int yi = yo * r + ii - p, xi = xo * r + jj - p;
+    out[i] = (yi >= 0 && yi < H && xi >= 0 && xi < W) ? __ldg(x + ((long)(n * C + c) * H + yi) * W + xi) : 0.0f;
+  }
+}
+
+int launch_pad_s2d(const float* x, int N, int C, int H, int W, int p, int r, int nhwc, float* out,
+                   cudaStream_t s) {
   if (r < 1 || p < 0 || (H + 2 * p) % r || (W + 2 * p) % r) return XNC_EINVAL;
   const int Hp = H + 2 * p, Ho = Hp / r, Wo = (W + 2 * p) / r;
-  const long total = (long)N * C * Hp * Wo;
-  if (total >= 0x7fffffffL || (long)N * C * r * r * Ho * Wo >= 0x7fffffffL) return XNC_ENOTSUP;
-  const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
-  k_pad_s2d<<<blocks, 256, 0, s>>>(x, C, H, W, p, r, Hp, Ho, Wo, (int)total, out);
+  const long total = (long)N * C * Hp * Wo, out_total = (long)N * C * r * r * Ho * Wo;
+  if (total >= 0x7fffffffL || out_total >= 0x7fffffffL) return XNC_ENOTSUP;
+  if (nhwc) {
+    const unsigned blocks = (unsigned)std::min<long>(cdivl(out_total, 256), 148L * 16);
+    k_pad_s2d_nhwc<<<blocks, 256, 0, s>>>(x, C, H, W, p, r, Ho, Wo, (int)out_total, out);
+  } else {
+    const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
+    k_pad_s2d<<<blocks, 256, 0, s>>>(x, C, H, W, p, r, Hp, Ho, Wo, (int)total, 0, out);
+  }
   return launch_status();
 }
 

@@ -296,6 +296,61 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   return launch_status();
 }
 
+// K1 for a channels-last input [N][H][W][C]: one thread per pixel walks its C
+// contiguous channels in order (16-byte loads when C % 4 == 0), building the words
+// and the sequential |.| sum exactly as k_pack_input does for NCHW.
+template <bool AFF>
+__global__ void __launch_bounds__(128) k_pack_input_nhwc(const float* __restrict__ x, int C, int Cw, long npix,
+                                                         float inv, uint32_t* __restrict__ bits,
+                                                         float* __restrict__ A,
+                                                         const float* __restrict__ in_scale,
+                                                         const float* __restrict__ in_shift) {
+  const long q = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= npix) return;
+  const float* xp = x + q * C;
+  const bool v4 = (C & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  float s = 0.0f;
+  for (int j = 0; j < Cw; ++j) {
+    const int c0 = 32 * j, cend = min(32, C - c0);
+    float v[32];
+    if (v4 && cend == 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(xp + c0) + u);
+        v[4 * u] = t.x; v[4 * u + 1] = t.y; v[4 * u + 2] = t.z; v[4 * u + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) v[u] = u < cend ? __ldg(xp + c0 + u) : 0.0f;
+    }
+    uint32_t word = 0u;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      if (u < cend) {
+        float t = v[u];
+        if (AFF) t = __fadd_rn(__fmul_rn(t, __ldg(in_scale + c0 + u)), __ldg(in_shift + c0 + u));
+        s = __fadd_rn(s, fabsf(t));
+        word |= (t >= 0.0f ? 1u : 0u) << u;
+      }
+    }
+    bits[q * Cw + j] = word;
+  }
+  if (A) A[q] = __fmul_rn(s, inv);
+}
+
+int launch_pack_input_nhwc(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A, cudaStream_t s,
+                           const float* in_scale, const float* in_shift) {
+  const long npix = (long)N * H * W;
+  const int Cw = cdiv(C, 32);
+  const float inv = (float)(1.0 / (double)C);
+  const unsigned blocks = (unsigned)cdivl(npix, 128);
+  if (in_scale)
+    k_pack_input_nhwc<true><<<blocks, 128, 0, s>>>(x, C, Cw, npix, inv, bits, A, in_scale, in_shift);
+  else
+    k_pack_input_nhwc<false><<<blocks, 128, 0, s>>>(x, C, Cw, npix, inv, bits, A, in_scale, in_shift);
+  return launch_status();
+}
+
 // One thread per filter.  wbits layout [Cw][kh][kw][O] (filters contiguous) so
 // the conv kernel stages a filter block with coalesced row copies.  Templated
 // on the weight dtype: the drop-in API passes the reference's float64 Tensor3

@@ -98,7 +98,8 @@ class XnorConv2d:
             if want_acc:
                 raise ValueError("want_acc is only supported for device inputs")
             return self.forward_host(x, out=out)
-        x = x.contiguous()
+        if not (x.is_contiguous() or x.is_contiguous(memory_format=torch.channels_last)):
+            x = x.contiguous()  # NCHW or channels-last maps are taken as they are
         self.out_shape(x.shape)
         return self._forward_device(x, out, want_acc)
 
@@ -107,7 +108,8 @@ class XnorConv2d:
         variant = self.kernel_for(self.conv_in_shape(x.shape))
         if variant in ("popc-fc", "umma-fc"):
             return self._forward_fc(x, out, want_acc, variant)
-        plain = self.in_affine is None and self.out_affine is None and self.in_pool is None
+        plain = (self.in_affine is None and self.out_affine is None and self.in_pool is None
+                 and x.is_contiguous())
         if variant == "popc" and not want_acc and plain:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
         if variant == "umma" and not want_acc and plain:  # one C-ABI call: K1 -> K2 -> tcgen05 K3+K4

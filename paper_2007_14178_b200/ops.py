@@ -24,12 +24,12 @@ def _stream(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def _need_cuda(t: torch.Tensor, name: str, dtype: torch.dtype) -> None:
+def _need_cuda(t: torch.Tensor, name: str, dtype: torch.dtype, channels_last_ok: bool = False) -> None:
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (the B200 path has no CPU fallback)")
     if t.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
-    if not t.is_contiguous():
+    if not (t.is_contiguous() or (channels_last_ok and t.is_contiguous(memory_format=torch.channels_last))):
         raise ValueError(f"{name} must be contiguous")
 
 
@@ -64,30 +64,40 @@ def pool_dims(H: int, W: int, in_pool) -> tuple[int, int]:
     return (H - k) // s + 1, (W - k) // s + 1
 
 
+def _channels_last(x: torch.Tensor) -> bool:
+    return not x.is_contiguous() and x.is_contiguous(memory_format=torch.channels_last)
+
+
 def max_pool(x: torch.Tensor, k: int, s: int, relu: bool = False) -> torch.Tensor:
     """Max-pool k x k / stride s, no padding (torch.max_pool2d values), on the
-    device; relu=True: torch.relu first, in the same pass."""
-    _need_cuda(x, "x", torch.float32)
-    x = x.contiguous()
+    device; relu=True: torch.relu first, in the same pass.  A channels-last x gives
+    a channels-last result."""
+    _need_cuda(x, "x", torch.float32, channels_last_ok=True)
+    nhwc = _channels_last(x)
+    if not nhwc:
+        x = x.contiguous()
     N, C, H, W = x.shape
     Ho, Wo = pool_dims(H, W, (k, s))
-    out = torch.empty((N, C, Ho, Wo), dtype=torch.float32, device=x.device)
-    check(lib().xnc_max_pool(x.data_ptr(), N, C, H, W, int(k), int(s), int(bool(relu)), out.data_ptr(),
-                             _stream(x.device)), "xnc_max_pool")
+    fmt = torch.channels_last if nhwc else torch.contiguous_format
+    out = torch.empty((N, C, Ho, Wo), dtype=torch.float32, device=x.device, memory_format=fmt)
+    check(lib().xnc_max_pool(x.data_ptr(), N, C, H, W, int(k), int(s), int(bool(relu)), int(nhwc),
+                             out.data_ptr(), _stream(x.device)), "xnc_max_pool")
     return out
 
 
-def pad_space_to_depth(x: torch.Tensor, pad: int, r: int) -> torch.Tensor:
-    """F.pixel_unshuffle(F.pad(x, (pad,) * 4), r) in one device pass."""
+def pad_space_to_depth(x: torch.Tensor, pad: int, r: int, channels_last: bool = False) -> torch.Tensor:
+    """F.pixel_unshuffle(F.pad(x, (pad,) * 4), r) in one device pass (x NCHW);
+    channels_last=True stores the result channels-last."""
     _need_cuda(x, "x", torch.float32)
     x = x.contiguous()
     N, C, H, W = x.shape
     if (H + 2 * pad) % r or (W + 2 * pad) % r:
         raise ValueError(f"padded {H}x{W} input is not a multiple of {r}")
+    fmt = torch.channels_last if channels_last else torch.contiguous_format
     out = torch.empty((N, C * r * r, (H + 2 * pad) // r, (W + 2 * pad) // r), dtype=torch.float32,
-                      device=x.device)
-    check(lib().xnc_pad_space_to_depth(x.data_ptr(), N, C, H, W, int(pad), int(r), out.data_ptr(),
-                                       _stream(x.device)), "xnc_pad_space_to_depth")
+                      device=x.device, memory_format=fmt)
+    check(lib().xnc_pad_space_to_depth(x.data_ptr(), N, C, H, W, int(pad), int(r), int(bool(channels_last)),
+                                       out.data_ptr(), _stream(x.device)), "xnc_pad_space_to_depth")
     return out
 
 
@@ -99,14 +109,17 @@ def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None, in_pool=Non
     in_pool = (kernel, stride): x is the pre-pool tensor, max-pooled first (no
     padding; xnc_max_pool) -- XNOR-Net's pool -> BN -> sign; bits / A then have the
     pooled spatial shape."""
-    _need_cuda(x, "x", torch.float32)
+    _need_cuda(x, "x", torch.float32, channels_last_ok=True)
     if in_pool is not None:
         x = max_pool(x, *in_pool)
     N, C, H, W = x.shape
     bits = torch.empty((N, H, W, words(C)), dtype=torch.int32, device=x.device)
     A = torch.empty((N, H, W), dtype=torch.float32, device=x.device) if want_A else None
     sc, sh = _affine(in_affine, C, x.device, "in_affine")
-    if sc is None:
+    if _channels_last(x):  # channels-last maps (the network's front end) are packed in place
+        check(lib().xnc_pack_input_nhwc(x.data_ptr(), N, C, H, W, _ptr(sc), _ptr(sh), bits.data_ptr(), _ptr(A),
+                                        _stream(x.device)), "xnc_pack_input_nhwc")
+    elif sc is None:
         check(lib().xnc_pack_input(x.data_ptr(), N, C, H, W, bits.data_ptr(), _ptr(A), _stream(x.device)),
               "xnc_pack_input")
     else:

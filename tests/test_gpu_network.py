@@ -65,6 +65,8 @@ def test_pad_space_to_depth_matches_torch(shape, pad, r):
     x = torch.randn(shape, device="cuda")
     want = F.pixel_unshuffle(F.pad(x, (pad,) * 4), r)
     assert torch.equal(ops.pad_space_to_depth(x, pad, r), want)
+    cl = ops.pad_space_to_depth(x, pad, r, channels_last=True)
+    assert cl.is_contiguous(memory_format=torch.channels_last) and torch.equal(cl, want)
 
 
 @pytest.mark.parametrize("shape,k,s", [((2, 96, 55, 55), 3, 2), ((3, 7, 9, 12), 2, 2), ((1, 4, 11, 11), 5, 3)])
@@ -75,3 +77,23 @@ def test_relu_max_pool_matches_torch(shape, k, s):
     want = F.max_pool2d(F.relu(x), k, s)
     assert torch.equal(ops.max_pool(x, k, s, relu=True), want)
     assert torch.equal(ops.max_pool(x, k, s), F.max_pool2d(x, k, s))
+    xl = x.contiguous(memory_format=torch.channels_last)  # channels-last in, channels-last out
+    got = ops.max_pool(xl, k, s, relu=True)
+    assert got.is_contiguous(memory_format=torch.channels_last) and torch.equal(got, want)
+
+
+@pytest.mark.parametrize("shape", [(3, 96, 27, 27), (2, 70, 5, 7), (2, 33, 4, 4)])
+def test_pack_input_channels_last_matches_nchw(shape):
+    """K1 on a channels-last map (the front end's output) == K1 on the NCHW copy:
+    bits and A identical, with and without the folded BN."""
+    from paper_2007_14178_b200 import ops
+    x = torch.randn(shape, device="cuda")
+    x[0, 0, 0, 0] = 0.0
+    x[0, 1, 0, 0] = -0.0
+    xl = x.contiguous(memory_format=torch.channels_last)
+    C = shape[1]
+    for aff in (None, (torch.rand(C, device="cuda") + 0.5, torch.rand(C, device="cuda") - 0.5)):
+        b1, a1 = ops.pack_input(xl, in_affine=aff)
+        b2, a2 = ops.pack_input(x, in_affine=aff)
+        assert torch.equal(b1, b2)
+        assert torch.equal(a1.view(torch.int32), a2.view(torch.int32))

@@ -1,5 +1,6 @@
 """Split the C4 front end (conv1 as space-to-depth 3x3 on cuDNN TF32, ReLU, max-pool
-3/2) into its pieces at batch 256.  Profiling aid; prints one JSON line."""
+3/2, then conv2's K1) into its pieces at batch 256, NCHW vs channels-last.
+Profiling aid; prints one JSON line."""
 import json
 import os
 import sys
@@ -28,16 +29,19 @@ def t(fn, reps=10):
 net = XnorNetAlexNet("cuda", seed=7)
 x = torch.rand((256, 3, 224, 224), device="cuda") * 2 - 1
 r = {}
+bn2 = net.bn["conv2"]
 with torch.no_grad(), _tf32_full_precision_layers():
-    xs = F.pixel_unshuffle(F.pad(x, (2, 2, 2, 2)), 4)
+    for fmt in ("nchw", "nhwc"):
+        cl = fmt == "nhwc"
+        w = net.conv1_w_s2d.contiguous(memory_format=torch.channels_last) if cl else net.conv1_w_s2d
+        r[f"{fmt}_s2d"] = t(lambda: ops.pad_space_to_depth(x, 2, 4, channels_last=cl))
+        xs = ops.pad_space_to_depth(x, 2, 4, channels_last=cl)
+        r[f"{fmt}_conv"] = t(lambda: F.conv2d(xs, w, net.conv1_b))
+        h = F.conv2d(xs, w, net.conv1_b)
+        r[f"{fmt}_conv_out_cl"] = h.is_contiguous(memory_format=torch.channels_last) and not h.is_contiguous()
+        r[f"{fmt}_relu_pool"] = t(lambda: ops.max_pool(h, 3, 2, relu=True))
+        p = ops.max_pool(h, 3, 2, relu=True)
+        r[f"{fmt}_conv2_k1"] = t(lambda: ops.pack_input(p, in_affine=bn2))
     r["torch_pad_s2d"] = t(lambda: F.pixel_unshuffle(F.pad(x, (2, 2, 2, 2)), 4))
-    r["our_pad_s2d"] = t(lambda: ops.pad_space_to_depth(x, 2, 4))
-    r["conv"] = t(lambda: F.conv2d(xs, net.conv1_w_s2d, net.conv1_b))
-    h = F.conv2d(xs, net.conv1_w_s2d, net.conv1_b)
-    r["relu"] = t(lambda: F.relu(h))
-    hr = F.relu(h)
-    r["torch_pool"] = t(lambda: F.max_pool2d(hr, 3, 2))
-    r["our_pool"] = t(lambda: ops.max_pool(hr, 3, 2))
-    r["our_relu_pool"] = t(lambda: ops.max_pool(h, 3, 2, relu=True))
     r["front_end"] = t(lambda: net.front_end(x))
-print(json.dumps({"bench": "front_probe", "ms": r, "conv_out": list(h.shape)}))
+print(json.dumps({"bench": "front_probe", "ms": r}))
