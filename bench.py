@@ -493,6 +493,7 @@ def run_network(args, cfg_name):
     torch.cuda.synchronize(dev)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / max(2, min(args.steps, 5)), ws, dev)
     bops = 2.0 * BINARY_MACS_PER_IMAGE * gb
+    per_step = count_own_kernels(lambda: net(x)) if rank == 0 else None
     res = None
     if rank == 0:
         res = {"metric": METRIC, "value": bops / (ms * 1e-3) / 1e9, "unit": "Gbinop/s", "n_gpus": ws,
@@ -506,7 +507,10 @@ def run_network(args, cfg_name):
                           "parallelism": f"batch-sharded x{ws}, per-rank weight replicas, no collective"},
                "images_per_s": gb / (ms * 1e-3),
                "binops_per_image": 2.0 * BINARY_MACS_PER_IMAGE,
-               "gpu_launches": None,
+               "gpu_launches": None if per_step is None else per_step * args.steps,
+               "gpu_launches_note": "our (xnc::) kernels per forward, counted with torch.profiler on one extra "
+                                    "forward outside the timed region, x steps; cuDNN / cuBLAS / torch kernels "
+                                    "(conv1, fc8, zero-fill) not counted",
                "e2e": {"value": bops / (e2e_ms * 1e-3) / 1e9, "unit": "Gbinop/s",
                        "h2d_bytes_per_step": x_host.numel() * 4 * ws, "d2h_bytes_per_step": logits_host.numel() * 4 * ws,
                        "ms_per_step": e2e_ms, "api": "XnorNetAlexNet.forward"},
@@ -515,6 +519,23 @@ def run_network(args, cfg_name):
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return res
+
+
+def count_own_kernels(fn) -> int | None:
+    """Number of this library's kernels (names in namespace xnc::) one call of fn
+    launches, from a torch.profiler trace of one extra call (None if CUPTI is not
+    available)."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+        return sum(1 for n in names if "xnc::" in n)
+    except Exception:
+        return None
 
 
 def network_summary(variant="auto", batch=256, steps=5, warmup=3):
