@@ -75,6 +75,9 @@ namespace xnc {
 #endif
 constexpr int kPEpiWarps = XNC_EPI_WARPS;  // multiple of 4 (one group per TMEM lane quadrant)
 constexpr int kPThreads = 128 + 32 * kPEpiWarps;
+#ifndef XNC_A_ROWS
+#define XNC_A_ROWS 4  // A producer: bit rows per thread per batch (x 2 planes) loaded before expanding
+#endif
 #ifndef XNC_PSTAGES
 #define XNC_PSTAGES 4
 #endif
@@ -442,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     // thread has up to 2*kAR 16-byte loads in flight instead of one: under the
     // epilogue's store stream the L2 latency of the bit rows grows, and a
     // one-load-at-a-time loop left the issuer waiting on a_full.
-    constexpr int kAR = 4;
+    constexpr int kAR = XNC_A_ROWS;
     const int grp = g.a_unit ? g.KBu : 1;
     uint32_t it = 0;  // units of this pair so far: every unit builds its KBu planes
     for (int u = cluster; u < g.units; u += n_clusters, ++it) {
