@@ -471,8 +471,11 @@ def run_network(args, cfg_name):
     x = x_host.to(dev)
     net = XnorNetAlexNet(dev, seed=7, variant=args.variant)
     stream = torch.cuda.current_stream(dev)
+    # the forward as one CUDA graph (same kernels; removes the per-layer host launches)
+    graph, logits = net.capture(x) if not args.no_graph else (None, None)
+    step = graph.replay if graph is not None else (lambda: net(x))
     for _ in range(args.warmup):
-        net(x)
+        step()
     torch.cuda.synchronize(dev)
     if ws > 1:
         torch.distributed.barrier()
@@ -480,20 +483,27 @@ def run_network(args, cfg_name):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            logits = net(x)
+            out = step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
+    if graph is None:
+        logits = out
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws, dev)
-    # e2e: host images in, host logits out, copies timed
+    # e2e: host images in (pinned -> the graph's input buffer), host logits out, copies timed
     logits_host = torch.empty(tuple(logits.shape), dtype=torch.float32).pin_memory()
     e0.record(stream)
     for _ in range(max(2, min(args.steps, 5))):
-        logits_host.copy_(net(x_host.to(dev, non_blocking=True)), non_blocking=True)
+        if graph is not None:
+            x.copy_(x_host, non_blocking=True)
+            graph.replay()
+            logits_host.copy_(logits, non_blocking=True)
+        else:
+            logits_host.copy_(net(x_host.to(dev, non_blocking=True)), non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / max(2, min(args.steps, 5)), ws, dev)
     bops = 2.0 * BINARY_MACS_PER_IMAGE * gb
-    per_step = count_own_kernels(lambda: net(x)) if rank == 0 else None
+    per_step = count_own_kernels(lambda: net(x)) if rank == 0 else None  # eager: same kernels as the graph
     res = None
     if rank == 0:
         res = {"metric": METRIC, "value": bops / (ms * 1e-3) / 1e9, "unit": "Gbinop/s", "n_gpus": ws,
@@ -504,6 +514,7 @@ def run_network(args, cfg_name):
                "config": {"workload": CONFIG_TEXT[cfg_name], "name": cfg_name, "global_batch": gb,
                           "batch_per_gpu": N, "variant": args.variant,
                           "binary_kernels": net.binary_kernels(N),
+                          "execution": "CUDA graph of the forward" if graph is not None else "eager",
                           "parallelism": f"batch-sharded x{ws}, per-rank weight replicas, no collective"},
                "images_per_s": gb / (ms * 1e-3),
                "binops_per_image": 2.0 * BINARY_MACS_PER_IMAGE,
@@ -547,13 +558,14 @@ def network_summary(variant="auto", batch=256, steps=5, warmup=3):
     g = torch.Generator().manual_seed(11)
     x = ((torch.rand((batch, 3, 224, 224), generator=g) * 2 - 1)).to(dev)
     net = XnorNetAlexNet(dev, seed=7, variant=variant)
+    graph, _ = net.capture(x)
     for _ in range(warmup):
-        net(x)
+        graph.replay()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
-        net(x)
+        graph.replay()
     e1.record()
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / steps
@@ -625,6 +637,7 @@ def main():
     ap.add_argument("--variant", choices=["popc", "b1mma", "umma", "auto"], default="auto")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-ksweep", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="C4/C5: eager forward instead of the CUDA graph")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU reference work")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -145,6 +145,24 @@ class XnorNetAlexNet:
 
     __call__ = forward
 
+    def capture(self, x_static: torch.Tensor):
+        """Record one forward of the fixed input buffer x_static as a CUDA graph.
+
+        Returns (graph, logits): after copying new images into x_static,
+        graph.replay() recomputes logits in place.  Same kernels and results as
+        forward() (the graph only removes the ~40 per-layer launches from the host
+        path: 1.65 vs 1.71 ms at batch 256)."""
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):  # warm up: one-time smem opt-ins, cuDNN plans
+            for _ in range(2):
+                self.forward(x_static)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            logits = self.forward(x_static)
+        return graph, logits
+
     def binary_kernels(self, batch: int) -> dict[str, str]:
         """Which conv kernel (umma / popc) each binary layer runs at this batch."""
         shapes = {"conv2": (96, 27), "conv3": (256, 13), "conv4": (384, 13), "conv5": (384, 13),

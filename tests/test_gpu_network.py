@@ -97,3 +97,17 @@ def test_pack_input_channels_last_matches_nchw(shape):
         b2, a2 = ops.pack_input(x, in_affine=aff)
         assert torch.equal(b1, b2)
         assert torch.equal(a1.view(torch.int32), a2.view(torch.int32))
+
+
+def test_network_cuda_graph_matches_eager():
+    """The captured forward (bench.py's C4 step) recomputes the eager logits exactly,
+    also after new images are copied into its input buffer."""
+    from paper_2007_14178_b200.network import XnorNetAlexNet
+    net = XnorNetAlexNet("cuda", seed=2)
+    x = torch.rand((4, 3, 224, 224), device="cuda") * 2 - 1
+    graph, logits = net.capture(x)
+    for _ in range(2):
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(logits, net.forward(x))
+        x.copy_(torch.rand_like(x) * 2 - 1)
