@@ -133,6 +133,20 @@ int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, 
  * bits / A, a thread per pixel walking its contiguous channels. */
 int xnc_pack_input_nhwc(const float* x, int N, int C, int H, int W, const float* in_scale,
                         const float* in_shift, uint32_t* bits, float* A, void* stream);
+/* Binary -> binary: the conv epilogue writes the NEXT binary layer's K1 output
+ * instead of y (north star item 4, "sign for the next binary layer"): with
+ * y' = ((f32(acc) * K) * alpha) [* out_scale + out_shift], next_bits u32
+ * [N][H'][W'][ceil(O/32)] = sign words of y' (bit c = y'_c >= 0, tail bits 0) and
+ * next_A f32 [N][H'][W'] = (sequential f32 sum over c of |y'_c|) * f32(1/O) (NULL
+ * = not written), bit-identical to xnc_pack_input_affine run on the materialised
+ * y'.  The 822 MB float map of a C3 layer is never written nor re-read.  Needs all
+ * O filters in one 256-wide block: xnc_umma_emit_supported() (O <= 256). */
+int xnc_umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
+int xnc_xnor_conv_umma_emit(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
+                            const float* K, const float* alpha, int N, int C, int H, int W,
+                            int O, int kh, int kw, int pad, const float* out_scale,
+                            const float* out_shift, uint32_t* next_bits, float* next_A,
+                            void* stream);
 /* K split for shapes with fewer (pixel tile, 256-filter block) work units than CTA
  * pairs -- fully connected layers viewed as one 1 x N image.  Units of one output
  * tile take disjoint K ranges and add their raw partial sums into split_ws

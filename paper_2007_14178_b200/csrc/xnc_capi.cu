@@ -155,6 +155,22 @@ int xnc_pack_input_nhwc(const float* x, int N, int C, int H, int W, const float*
   return launch_pack_input_nhwc(x, N, C, H, W, bits, A, as_stream(stream), in_scale, in_shift);
 }
 
+int xnc_umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
+  if (O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return 0;
+  return umma_emit_supported(N, C, H, W, O, kh, kw, pad) ? 1 : 0;
+}
+
+int xnc_xnor_conv_umma_emit(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
+                            const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
+                            const float* out_scale, const float* out_shift, uint32_t* next_bits, float* next_A,
+                            void* stream) {
+  if (!bits || !wq || !sw || !K || !alpha || !next_bits || O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad))
+    return XNC_EINVAL;
+  if (!out_scale != !out_shift) return XNC_EINVAL;
+  return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, nullptr, nullptr, as_stream(stream),
+                          out_scale, out_shift, nullptr, next_bits, next_A);
+}
+
 size_t xnc_umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
   if (O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad)) return 0;
   return umma_split_ws_bytes(N, C, H, W, O, kh, kw, pad);

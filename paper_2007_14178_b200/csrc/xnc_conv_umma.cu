@@ -338,6 +338,7 @@ struct PairGeom {
                      // for shapes with fewer (tile, block) pairs than CTA pairs (fully connected
                      // layers): the units add raw partial sums into a zeroed s32 buffer
   uint32_t b_half_bytes, tmem_cols;
+  float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
              // (kPCPS == 1 only), bit 8 = no B protocol at all after the first fill, bit 2 = build the
              // input planes once, bit 5 = epilogue does only the TMEM handshake, bit 6 = chunk
@@ -362,7 +363,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
     const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out,
-    const float* __restrict__ out_scale, const float* __restrict__ out_shift, int32_t* __restrict__ part) {
+    const float* __restrict__ out_scale, const float* __restrict__ out_shift, int32_t* __restrict__ part,
+    uint32_t* __restrict__ next_bits, float* __restrict__ next_A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
@@ -640,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       const int t = u / (g.n_nb * g.S), nb = (u / g.S) % g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);
-      size_t pix[MH];
+      size_t pix[MH], qix[MH];
       bool ok[MH];
       float kv[MH];
 #pragma unroll
@@ -648,13 +650,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         const int e = m0 + h * 128 + quad * 32 + lane;
         const int rr = e / g.IC, cc = e - (e / g.IC) * g.IC;
         ok[h] = rr < g.oh && cc < g.ow;
+        qix[h] = (size_t)n * plane_out + (size_t)rr * g.ow + cc;  // output pixel (n, rr, cc)
         pix[h] = (size_t)n * g.O * plane_out + (size_t)rr * g.ow + cc;
-        kv[h] = (ok[h] && y) ? __ldg(Kmap + (size_t)n * plane_out + (size_t)rr * g.ow + cc) : 0.0f;
+        kv[h] = (ok[h] && (y || next_bits)) ? __ldg(Kmap + qix[h]) : 0.0f;
       }
       const uint32_t buf = item & 1;
       mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + buf * (MH * g.NP);
+      if (next_bits != nullptr) {
+        // Binary -> binary: emit the NEXT layer's K1 output instead of y (north star
+        // item 4, "sign for the next binary layer").  One filter
+        // block holds all O channels of a pixel (host-checked), and warp group 0
+        // walks them in channel order, so the sign words and the sequential f32
+        // |.| sum are exactly K1's on the (affine) output map: bits [q][O/32 words],
+        // A[q] = (sum_c |y'_c|) * f32(1/O).  Group 1 only releases the buffer.
+        if (cg == 0) {
+          const int Cw_next = (g.O + 31) >> 5;
+          float sA[MH];
+          uint32_t word[MH];
+#pragma unroll
+          for (int h = 0; h < MH; ++h) { sA[h] = 0.0f; word[h] = 0u; }
+          for (int ch = 0; ch < n_chunks; ++ch) {
+            const int obase = ch * 16;
+            uint32_t v[MH][16];
+#pragma unroll
+            for (int h = 0; h < MH; ++h) tmem_ld16_async(tbase + h * g.NP + ch * 16, v[h]);
+            float av[16], osc[16], osh[16];
+            int swv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const bool in = obase + j < g.O;
+              swv[j] = in ? __ldg(sw + obase + j) : 0;
+              av[j] = in ? __ldg(alpha + obase + j) : 0.0f;
+              osc[j] = (in && out_scale) ? __ldg(out_scale + obase + j) : 1.0f;
+              osh[j] = (in && out_scale) ? __ldg(out_shift + obase + j) : 0.0f;
+            }
+            tmem_wait_ld_regs(v[0]);
+#pragma unroll
+            for (int h = 1; h < MH; ++h) reg_dep16(v[h]);
+#pragma unroll
+            for (int h = 0; h < MH; ++h) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (obase + j < g.O) {
+                  float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
+                  if (out_scale != nullptr) val = __fadd_rn(__fmul_rn(val, osc[j]), osh[j]);
+                  sA[h] = __fadd_rn(sA[h], fabsf(val));
+                  word[h] |= (val >= 0.0f ? 1u : 0u) << ((ch & 1) * 16 + j);
+                }
+              }
+              if ((ch & 1) || ch == n_chunks - 1) {
+                if (ok[h]) next_bits[qix[h] * Cw_next + (ch >> 1)] = word[h];
+                word[h] = 0u;
+              }
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < MH; ++h)
+            if (ok[h] && next_A != nullptr) next_A[qix[h]] = __fmul_rn(sA[h], g.inv_O);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(t_empty0 + buf * 8);
+        continue;
+      }
       for (int ch = (PROF && (dbg & 32)) ? n_chunks : cg; ch < n_chunks; ch += cstep) {
         const int obase = nb * g.NP + ch * 16;
         const unsigned long long tc0 = prof ? clock64() : 0ull;
@@ -914,6 +974,12 @@ static int split_factor(const PairGeom& g) {
   return best;
 }
 
+bool umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
+  PairGeom g;
+  size_t smem;
+  return pair_plan(N, C, H, W, O, kh, kw, pad, g, smem) && g.n_nb == 1;
+}
+
 size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
   PairGeom g;
   size_t smem;
@@ -970,10 +1036,12 @@ int umma_profile_read(unsigned long long* host, int n_ctas) {
 int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s, const float* out_scale,
-                     const float* out_shift, int32_t* split_ws) {
+                     const float* out_shift, int32_t* split_ws, uint32_t* next_bits, float* next_A) {
   PairGeom g;
   size_t smem;
   if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
+  if (next_bits != nullptr && g.n_nb != 1) return XNC_ENOTSUP;  // all channels of a pixel in one block
+  if (next_bits != nullptr) split_ws = nullptr;
   // split K across CTA pairs when the caller passed the (zeroed) partial-sum buffer
   const int S = split_ws != nullptr ? split_factor(g) : 1;
   if (S > 1 && !pair_plan(N, C, H, W, O, kh, kw, pad, g, smem, S)) return XNC_ENOTSUP;
@@ -1011,7 +1079,9 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   if (g.S > 1 && part == nullptr) {  // no buffer usable: run unsplit
     if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
   }
-  kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part);
+  g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
+  kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
+                                          next_bits, next_A);
   if (part != nullptr) {
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);

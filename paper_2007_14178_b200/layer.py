@@ -86,37 +86,62 @@ class XnorConv2d:
             self._ws[key] = ws
         return ws
 
-    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None,
-                want_acc: bool = False):
+    def forward(self, x, out: torch.Tensor | None = None, want_acc: bool = False,
+                emit_signs: bool = False):
         """x f32 [N, C, H, W] -> y f32 [N, O, H', W'] (and acc i32 if asked).
 
         A CUDA x runs on the device and returns a device y.  A host (CPU) x runs
-        the pipelined host path (`forward_host`) and returns a host y."""
+        the pipelined host path (`forward_host`) and returns a host y.  x may also
+        be an ops.PackedInput (a previous layer's emitted signs): K1 is skipped.
+        emit_signs=True returns the NEXT binary layer's input as an
+        ops.PackedInput (sign words + A of y [* out_affine]) instead of y, written
+        by the conv epilogue itself (tcgen05 kernel, O <= 256): the float map never
+        reaches HBM."""
+        if isinstance(x, ops.PackedInput):
+            return self._forward_packed(x, out, want_acc, emit_signs)
         if x.dim() != 4 or x.shape[1] != self.C:
             raise ValueError(f"input {tuple(x.shape)} does not match {self.C} filter channels")
         if not x.is_cuda:
-            if want_acc:
-                raise ValueError("want_acc is only supported for device inputs")
+            if want_acc or emit_signs:
+                raise ValueError("want_acc / emit_signs are only supported for device inputs")
             return self.forward_host(x, out=out)
         if not (x.is_contiguous() or x.is_contiguous(memory_format=torch.channels_last)):
             x = x.contiguous()  # NCHW or channels-last maps are taken as they are
         self.out_shape(x.shape)
-        return self._forward_device(x, out, want_acc)
+        return self._forward_device(x, out, want_acc, emit_signs)
 
     def _forward_device(self, x: torch.Tensor, out: torch.Tensor | None = None,
-                        want_acc: bool = False):
+                        want_acc: bool = False, emit_signs: bool = False):
         variant = self.kernel_for(self.conv_in_shape(x.shape))
-        if variant in ("popc-fc", "umma-fc"):
-            return self._forward_fc(x, out, want_acc, variant)
         plain = (self.in_affine is None and self.out_affine is None and self.in_pool is None
-                 and x.is_contiguous())
-        if variant == "popc" and not want_acc and plain:
+                 and x.is_contiguous() and not want_acc and not emit_signs)
+        if variant == "popc" and plain:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
-        if variant == "umma" and not want_acc and plain:  # one C-ABI call: K1 -> K2 -> tcgen05 K3+K4
+        if variant == "umma" and plain:  # one C-ABI call: K1 -> K2 -> tcgen05 K3+K4
             return ops.layer_forward_umma(x, self.filters, self.pad, self.workspace(x), y=out)
         bits, A = ops.pack_input(x, in_affine=self.in_affine, in_pool=self.in_pool)
-        K = ops.scale_map(A, self.kh, self.kw, self.pad)
-        y, acc = ops.xnor_conv(bits, self.filters, K, self.pad, want_acc=want_acc,
+        return self._conv_packed(ops.PackedInput(bits, A, self.C), variant, out, want_acc, emit_signs)
+
+    def _forward_packed(self, p: "ops.PackedInput", out, want_acc: bool, emit_signs: bool):
+        if p.C != self.C:
+            raise ValueError(f"packed input has {p.C} channels, the filters {self.C}")
+        if self.in_affine is not None or self.in_pool is not None:
+            raise ValueError("a packed input is already normalised / pooled: in_affine / in_pool do not apply")
+        self.out_shape(p.shape)
+        return self._conv_packed(p, self.kernel_for(p.shape), out, want_acc, emit_signs)
+
+    def _conv_packed(self, p: "ops.PackedInput", variant: str, out, want_acc: bool, emit_signs: bool):
+        """K2 -> K3+K4 on a K1-form input."""
+        if variant in ("popc-fc", "umma-fc"):
+            if emit_signs:
+                raise ValueError("emit_signs is not available for fully connected layers")
+            return self._fc_packed(p, out, want_acc, variant)
+        K = ops.scale_map(p.A, self.kh, self.kw, self.pad)
+        if emit_signs:
+            if variant != "umma":
+                raise ValueError("emit_signs needs the tcgen05 kernel (variant 'umma' or 'auto')")
+            return ops.xnor_conv_emit(p.bits, self.filters, K, self.pad, out_affine=self.out_affine)
+        y, acc = ops.xnor_conv(p.bits, self.filters, K, self.pad, want_acc=want_acc,
                                variant=variant, y=out, out_affine=self.out_affine)
         return (y, acc) if want_acc else y
 
@@ -143,15 +168,14 @@ class XnorConv2d:
         N, C, H, W = x_shape
         return self.pad == 0 and self.kh == H and self.kw == W and C % 32 == 0 and N > 1
 
-    def _forward_fc(self, x: torch.Tensor, out: torch.Tensor | None, want_acc: bool,
-                    variant: str = "popc-fc"):
+    def _fc_packed(self, p: "ops.PackedInput", out, want_acc: bool, variant: str):
         """Fully connected binary layer (kernel covers the whole input): every image
         is one 'pixel' of a 1-row image whose channels are the (y, x, c) words of
         the image, so the conv kernels' pixel tiling runs over the batch.  Same
         arithmetic as the conv view: C' = kh*kw*C valid bits, K = box mean of A
         over the whole input, alpha per filter (the reference's (c, ky, kx) sum)."""
-        N, C, H, W = self.conv_in_shape(x.shape)
-        bits, A = ops.pack_input(x, in_affine=self.in_affine, in_pool=self.in_pool)
+        N, C, H, W = p.shape
+        bits, A = p.bits, p.A
         K = ops.scale_map(A, self.kh, self.kw, 0)                     # [N, 1, 1]
         fcf = self._fc_filters(umma=variant == "umma-fc")
         y1, acc1 = ops.xnor_conv(bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,

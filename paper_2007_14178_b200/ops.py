@@ -213,6 +213,53 @@ def scale_map(A: torch.Tensor, kh: int, kw: int, pad: int) -> torch.Tensor:
 VARIANTS = {"popc": 0, "b1mma": 1, "umma": 2}
 
 
+@dataclass
+class PackedInput:
+    """A binary layer's input in K1 form: bits i32 [N,H,W,Cw] (u32 payload) and
+    A f32 [N,H,W] for C channels -- what pack_input returns, or what a previous
+    layer's sign-emitting epilogue wrote (xnor_conv_emit)."""
+
+    bits: torch.Tensor
+    A: torch.Tensor
+    C: int
+
+    @property
+    def shape(self) -> tuple[int, int, int, int]:
+        N, H, W, _ = self.bits.shape
+        return N, self.C, H, W
+
+
+def umma_emit_supported(N: int, C: int, H: int, W: int, O: int, kh: int, kw: int, pad: int) -> bool:
+    return bool(lib().xnc_umma_emit_supported(N, C, H, W, O, kh, kw, pad))
+
+
+def xnor_conv_emit(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor, pad: int,
+                   out_affine=None) -> PackedInput:
+    """tcgen05 conv whose epilogue writes the NEXT binary layer's K1 output (sign words
+    and A of y' = alpha*K*acc [*scale + shift]) instead of y: bit-identical to
+    pack_input(y', ...) without the float map ever reaching HBM."""
+    _need_cuda(bits, "bits", torch.int32)
+    _need_cuda(K, "K", torch.float32)
+    if filt.wq is None:
+        raise ValueError("the sign-emitting epilogue runs on the tcgen05 kernel: attach_umma_weights() first")
+    N, H, W, Cw = bits.shape
+    C = filt.C
+    if words(C) != Cw:
+        raise ValueError(f"bits hold {Cw} words per pixel; filters have {C} channels")
+    if not umma_emit_supported(N, C, H, W, filt.O, filt.kh, filt.kw, pad):
+        raise ValueError(f"sign emission needs all {filt.O} filters in one 256-wide block (O <= 256)")
+    oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    dev = bits.device
+    nbits = torch.empty((N, oh, ow, words(filt.O)), dtype=torch.int32, device=dev)
+    nA = torch.empty((N, oh, ow), dtype=torch.float32, device=dev)
+    osc, osh = _affine(out_affine, filt.O, dev, "out_affine")
+    check(lib().xnc_xnor_conv_umma_emit(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), K.data_ptr(),
+                                        filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
+                                        _ptr(osc), _ptr(osh), nbits.data_ptr(), nA.data_ptr(), _stream(dev)),
+          "xnc_xnor_conv_umma_emit")
+    return PackedInput(nbits, nA, filt.O)
+
+
 def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, pad: int,
               C: int | None = None, want_y: bool = True, want_acc: bool = False,
               variant: str = "popc", y: torch.Tensor | None = None,

@@ -364,3 +364,51 @@ def test_layer_in_pool_matches_pooled_layer():
     yb = b.forward(F.max_pool2d(x, 3, 2).contiguous())
     assert ya.shape == (4, 128, 13, 13)
     assert torch.equal(ya.view(torch.int32), yb.view(torch.int32))
+
+
+@pytest.mark.parametrize("shape", [(2, 64, 20, 20, 256, 3, 3, 1), (1, 96, 14, 14, 250, 3, 3, 1),
+                                   (3, 32, 13, 13, 96, 5, 5, 2), (2, 200, 9, 9, 33, 3, 3, 1)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("affine", [False, True])
+def test_sign_emitting_epilogue(shape, affine):
+    """Binary -> binary epilogue: the conv writes the next layer's K1 output (sign
+    words + A of y [* out_affine]) -- bit-identical to K1 run on the float output."""
+    from paper_2007_14178_b200 import ops
+    N, C, H, W, Oc, kh, kw, pad = shape
+    if not ops.umma_emit_supported(N, C, H, W, Oc, kh, kw, pad):
+        pytest.skip("shape outside the tcgen05 plan")
+    rng = np.random.default_rng(list(shape) + [int(affine)])
+    dev = _dev()
+    x = torch.from_numpy(O.f32_exact(rng, (N, C, H, W))).to(dev)
+    w = torch.from_numpy(O.f32_exact(rng, (Oc, C, kh, kw))).to(dev)
+    filt = ops.pack_weights(w)
+    ops.attach_umma_weights(filt, w)
+    aff = None
+    if affine:
+        aff = (torch.from_numpy(rng.uniform(0.5, 1.5, Oc).astype(np.float32)).to(dev),
+               torch.from_numpy(rng.uniform(-0.3, 0.3, Oc).astype(np.float32)).to(dev))
+    bits, A = ops.pack_input(x)
+    K = ops.scale_map(A, kh, kw, pad)
+    y, _ = ops.xnor_conv(bits, filt, K, pad, variant="umma", out_affine=aff)
+    want_bits, want_A = ops.pack_input(y.contiguous())
+    got = ops.xnor_conv_emit(bits, filt, K, pad, out_affine=aff)
+    assert torch.equal(got.bits, want_bits)
+    assert torch.equal(got.A.view(torch.int32), want_A.view(torch.int32))
+
+
+def test_layer_chain_with_emitted_signs():
+    """XnorConv2d(emit_signs=True) feeding the next layer == the float chain, exactly
+    (a C3-style pair of binary layers with the second layer's BN folded in between)."""
+    from paper_2007_14178_b200 import XnorConv2d
+    rng = np.random.default_rng(9)
+    dev = _dev()
+    x = torch.from_numpy(O.f32_exact(rng, (2, 128, 24, 24))).to(dev)
+    w1 = torch.from_numpy(O.f32_exact(rng, (256, 128, 3, 3))).to(dev)
+    w2 = torch.from_numpy(O.f32_exact(rng, (64, 256, 3, 3))).to(dev)
+    bn = (torch.rand(256, device=dev) + 0.5, torch.rand(256, device=dev) - 0.5)
+    l1 = XnorConv2d(w1, pad=1, variant="auto", out_affine=bn)
+    l2 = XnorConv2d(w2, pad=1, variant="auto")
+    want = l2.forward(l1.forward(x))
+    packed = l1.forward(x, emit_signs=True)
+    got = l2.forward(packed)
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
