@@ -310,6 +310,18 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // wait for this thread's TMEM loads with the destination registers as operands, so
@@ -661,23 +673,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       if (next_bits != nullptr) {
         // Binary -> binary: emit the NEXT layer's K1 output instead of y (north star
         // item 4, "sign for the next binary layer").  One filter
-        // block holds all O channels of a pixel (host-checked), and warp group 0
-        // walks them in channel order, so the sign words and the sequential f32
-        // |.| sum are exactly K1's on the (affine) output map: bits [q][O/32 words],
-        // A[q] = (sum_c |y'_c|) * f32(1/O).  Group 1 only releases the buffer.
-        if (cg == 0) {
-          const int Cw_next = (g.O + 31) >> 5;
-          float sA[MH];
-          uint32_t word[MH];
+        // block holds all O channels of a pixel (host-checked): bits [q][O/32 words],
+        // A[q] = (sum_c |y'_c|) * f32(1/O), the sum sequential in channel order.
+        // Group 1 takes the upper chunks: their sign words, and |y'| written back
+        // over their TMEM columns; group 0 takes the lower chunks, then (after a
+        // two-warp barrier per lane quadrant) continues its running sum over the
+        // upper chunks' |y'| from TMEM -- the same order as K1, half the work each.
+        const int Cw_next = (g.O + 31) >> 5;
+        const int half = (n_chunks / 4) * 2;  // group 0: chunks [0, half); even: words never split
+        const int c_lo = cg == 0 ? 0 : half, c_hi = cg == 0 ? half : n_chunks;
+        const bool vec_c = vec_ok && ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
+                           (out_scale == nullptr || (((reinterpret_cast<uintptr_t>(out_scale) |
+                                                       reinterpret_cast<uintptr_t>(out_shift)) & 15) == 0));
+        float sA[MH];
+        uint32_t word[MH];
 #pragma unroll
-          for (int h = 0; h < MH; ++h) { sA[h] = 0.0f; word[h] = 0u; }
-          for (int ch = 0; ch < n_chunks; ++ch) {
-            const int obase = ch * 16;
-            uint32_t v[MH][16];
+        for (int h = 0; h < MH; ++h) { sA[h] = 0.0f; word[h] = 0u; }
+        for (int ch = c_lo; ch < c_hi; ++ch) {
+          const int obase = ch * 16;
+          uint32_t v[MH][16];
 #pragma unroll
-            for (int h = 0; h < MH; ++h) tmem_ld16_async(tbase + h * g.NP + ch * 16, v[h]);
-            float av[16], osc[16], osh[16];
-            int swv[16];
+          for (int h = 0; h < MH; ++h) tmem_ld16_async(tbase + h * g.NP + ch * 16, v[h]);
+          float av[16], osc[16], osh[16];
+          int swv[16];
+          if (vec_c && obase + 16 <= g.O) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int4 si = __ldg(reinterpret_cast<const int4*>(sw + obase) + q);
+              const float4 ai = __ldg(reinterpret_cast<const float4*>(alpha + obase) + q);
+              swv[4 * q] = si.x; swv[4 * q + 1] = si.y; swv[4 * q + 2] = si.z; swv[4 * q + 3] = si.w;
+              av[4 * q] = ai.x; av[4 * q + 1] = ai.y; av[4 * q + 2] = ai.z; av[4 * q + 3] = ai.w;
+              if (out_scale != nullptr) {
+                const float4 sc = __ldg(reinterpret_cast<const float4*>(out_scale + obase) + q);
+                const float4 sh = __ldg(reinterpret_cast<const float4*>(out_shift + obase) + q);
+                osc[4 * q] = sc.x; osc[4 * q + 1] = sc.y; osc[4 * q + 2] = sc.z; osc[4 * q + 3] = sc.w;
+                osh[4 * q] = sh.x; osh[4 * q + 1] = sh.y; osh[4 * q + 2] = sh.z; osh[4 * q + 3] = sh.w;
+              }
+            }
+          } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const bool in = obase + j < g.O;
@@ -686,25 +719,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
               osc[j] = (in && out_scale) ? __ldg(out_scale + obase + j) : 1.0f;
               osh[j] = (in && out_scale) ? __ldg(out_shift + obase + j) : 0.0f;
             }
+          }
+          tmem_wait_ld_regs(v[0]);
+#pragma unroll
+          for (int h = 1; h < MH; ++h) reg_dep16(v[h]);
+#pragma unroll
+          for (int h = 0; h < MH; ++h) {
+            uint32_t absv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
+              if (out_scale != nullptr) val = __fadd_rn(__fmul_rn(val, osc[j]), osh[j]);
+              const bool in = obase + j < g.O;
+              absv[j] = in ? __float_as_uint(fabsf(val)) : 0u;
+              if (cg == 0 && in) sA[h] = __fadd_rn(sA[h], fabsf(val));
+              word[h] |= (in && val >= 0.0f ? 1u : 0u) << ((ch & 1) * 16 + j);
+            }
+            if (cg == 1) tmem_st16(tbase + h * g.NP + ch * 16, absv);
+            if ((ch & 1) || ch == n_chunks - 1) {
+              if (ok[h]) next_bits[qix[h] * Cw_next + (ch >> 1)] = word[h];
+              word[h] = 0u;
+            }
+          }
+        }
+        if (cg == 1) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        named_bar_sync(1 + quad, 64);  // the two warps of this lane quadrant
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (cg == 0) {
+          for (int ch = half; ch < n_chunks; ++ch) {  // the running sum over the upper chunks
+            uint32_t v[MH][16];
+#pragma unroll
+            for (int h = 0; h < MH; ++h) tmem_ld16_async(tbase + h * g.NP + ch * 16, v[h]);
             tmem_wait_ld_regs(v[0]);
 #pragma unroll
             for (int h = 1; h < MH; ++h) reg_dep16(v[h]);
 #pragma unroll
-            for (int h = 0; h < MH; ++h) {
+            for (int h = 0; h < MH; ++h)
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                if (obase + j < g.O) {
-                  float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
-                  if (out_scale != nullptr) val = __fadd_rn(__fmul_rn(val, osc[j]), osh[j]);
-                  sA[h] = __fadd_rn(sA[h], fabsf(val));
-                  word[h] |= (val >= 0.0f ? 1u : 0u) << ((ch & 1) * 16 + j);
-                }
-              }
-              if ((ch & 1) || ch == n_chunks - 1) {
-                if (ok[h]) next_bits[qix[h] * Cw_next + (ch >> 1)] = word[h];
-                word[h] = 0u;
-              }
-            }
+              for (int j = 0; j < 16; ++j)
+                if (ch * 16 + j < g.O) sA[h] = __fadd_rn(sA[h], __uint_as_float(v[h][j]));
           }
 #pragma unroll
           for (int h = 0; h < MH; ++h)
