@@ -532,6 +532,42 @@ def run_network(args, cfg_name):
     return res
 
 
+def binary_stack_summary(steps=10, warmup=3):
+    """C3 as one layer of a stack of binary layers (its input already in K1 form, the
+    next layer's batch norm folded in): the float epilogue followed by the next
+    layer's K1 pass, vs the sign-emitting epilogue that writes the next layer's K1
+    output directly (north star item 4).  Inputs resident; CUDA events."""
+    import torch
+    from paper_2007_14178_b200 import XnorConv2d, ops
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = torch.rand((256, 256, 56, 56), device=dev, generator=g) * 2 - 1
+    w = torch.rand((256, 256, 3, 3), device=dev, generator=g) * 2 - 1
+    bn = (torch.rand(256, device=dev, generator=g) + 0.5, torch.rand(256, device=dev, generator=g) - 0.5)
+    layer = XnorConv2d(w, pad=1, variant="auto", out_affine=bn)
+    bits, A = ops.pack_input(x)
+    p = ops.PackedInput(bits, A, 256)
+
+    def timed(fn):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / steps
+
+    f_ms = timed(lambda: ops.pack_input(layer.forward(p)))
+    e_ms = timed(lambda: layer.forward(p, emit_signs=True))
+    bops = 2.0 * 256 * 256 * 56 * 56 * 256 * 9
+    return {"workload": "C3 layer inside a stack of binary layers (input and output in K1 form, BN folded)",
+            "ms_per_layer_float_epilogue_then_next_k1": f_ms, "ms_per_layer_sign_emitting_epilogue": e_ms,
+            "Gbinop_s_sign_emitting": bops / (e_ms * 1e-3) / 1e9, "speedup": f_ms / e_ms}
+
+
 def count_own_kernels(fn) -> int | None:
     """Number of this library's kernels (names in namespace xnc::) one call of fn
     launches, from a torch.profiler trace of one extra call (None if CUPTI is not
@@ -651,6 +687,7 @@ def main():
         ws, rank, _ = dist_env()
         if res is not None and rank == 0 and ws == 1 and not args.no_ksweep:
             res["network_C4"] = network_summary(args.variant)
+            res["binary_stack_C3"] = binary_stack_summary()
         if res is not None and rank == 0 and ws == 1 and not args.no_cpu:
             try:
                 res["cpu_baseline"] = cpu_baseline_fields(args.config, args.cpu_budget, res.get("ksweep"))
