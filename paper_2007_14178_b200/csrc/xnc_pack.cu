@@ -37,6 +37,9 @@ namespace xnc {
 #endif
 constexpr int kPackThreads = XNC_PACK_THREADS;  // preferred block size (smaller if smem is short)
 constexpr int kPackUnroll = XNC_PACK_UNROLL;  // channel loads in flight per thread
+#ifndef XNC_ABS_BATCH
+#define XNC_ABS_BATCH 8  // k_absmean: channel loads issued per batch (16/32/64 measured slower)
+#endif
 
 template <int VEC, int THREADS, bool AFF>
 __global__ void __launch_bounds__(THREADS) k_pack_input(const float* __restrict__ x, int C, int HW,
@@ -185,17 +188,61 @@ __global__ void k_absmean(const float* __restrict__ x, int C, int HW, long npix,
         s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, fabsf(v[u].x)), fabsf(v[u].y)), fabsf(v[u].z)), fabsf(v[u].w));
     }
   } else {
+    // batches of kB channel loads ahead of the sequential adds
+    constexpr int kB = XNC_ABS_BATCH;
     int c = 0;
-    for (; c + 8 <= C; c += 8) {
-      float v[8];
+    for (; c + kB <= C; c += kB) {
+      float v[kB];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(xp + (long)(c + u) * HW);
+      for (int u = 0; u < kB; ++u) v[u] = __ldg(xp + (long)(c + u) * HW);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) s = __fadd_rn(s, fabsf(affine_in(v[u], in_scale, in_shift, c + u)));
+      for (int u = 0; u < kB; ++u) s = __fadd_rn(s, fabsf(affine_in(v[u], in_scale, in_shift, c + u)));
     }
     for (; c < C; ++c) s = __fadd_rn(s, fabsf(affine_in(__ldg(xp + (long)c * HW), in_scale, in_shift, c)));
   }
   A[q] = __fmul_rn(s, inv);
+}
+
+// K1 for few-pixel maps with up to 768 channels (the 13x13 / 6x6 inputs of conv3-5
+// and fc6): a block stages 32 consecutive pixels x all C channels in shared memory
+// (four warps issue the coalesced 128-byte loads, the folded BN applied on the
+// way in), then warp 0 runs each pixel's sequential |.| chain from shared memory
+// while warps 1-3 build the sign words.  x is read once; the per-word and
+// per-pixel kernels read it twice and the per-pixel chain waited out a memory
+// round trip per 8 channels (conv4's input: 76 -> ~20 us).
+constexpr int kSmallMaxC = 768;
+template <bool AFF>
+__global__ void __launch_bounds__(128) k_pack_small(const float* __restrict__ x, int C, int HW, int Cw, long npix,
+                                                    float inv, uint32_t* __restrict__ bits, float* __restrict__ A,
+                                                    const float* __restrict__ in_scale,
+                                                    const float* __restrict__ in_shift) {
+  extern __shared__ float tile[];  // [C][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long q = (long)blockIdx.x * 32 + lane;
+  const bool in = q < npix;
+  const long n = in ? q / HW : 0, p = in ? q - n * HW : 0;
+  const float* xp = x + n * C * (long)HW + p;
+  for (int c = warp; c < C; c += 4) {
+    float v = in ? __ldg(xp + (long)c * HW) : 0.0f;
+    if (AFF) v = __fadd_rn(__fmul_rn(v, __ldg(in_scale + c)), __ldg(in_shift + c));
+    tile[c * 32 + lane] = v;
+  }
+  __syncthreads();
+  if (!in) return;
+  if (warp == 0) {
+    float s = 0.0f;
+#pragma unroll 8
+    for (int c = 0; c < C; ++c) s = __fadd_rn(s, fabsf(tile[c * 32 + lane]));
+    if (A) A[q] = __fmul_rn(s, inv);
+  } else {
+    for (int j = warp - 1; j < Cw; j += 3) {
+      const int cend = min(32, C - 32 * j);
+      uint32_t word = 0u;
+#pragma unroll 8
+      for (int u = 0; u < cend; ++u) word |= (tile[(32 * j + u) * 32 + lane] >= 0.0f ? 1u : 0u) << u;
+      bits[q * Cw + j] = word;
+    }
+  }
 }
 
 // A for 1x1 images with long channel vectors (the fc7 input, 4096 channels): the
@@ -245,6 +292,19 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
     if (vec_groups < 2L * 148 * 256 && C >= 256) {
       const int Cw = cdiv(C, 32);
       const long words = npix * Cw;
+      if (H * W >= 32 && C <= kSmallMaxC) {  // one pass: 32 pixels x C channels per block
+        const size_t sm = (size_t)C * 32 * sizeof(float);
+        static size_t opted[2] = {0, 0};
+        const int ai = in_scale ? 1 : 0;
+        auto kern = in_scale ? k_pack_small<true> : k_pack_small<false>;
+        if (sm > 48 * 1024 && sm > opted[ai]) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          opted[ai] = sm;
+        }
+        kern<<<(unsigned)cdivl(npix, 32), 128, sm, s>>>(x, C, H * W, Cw, npix, (float)(1.0 / (double)C), bits, A,
+                                                        in_scale, in_shift);
+        return launch_status();
+      }
       k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, in_scale,
                                                               in_shift);
       if (A && H * W == 1 && C >= 1024)
