@@ -64,12 +64,49 @@ __global__ void k_max_pool_nhwc(const float* __restrict__ x, int C, int Hin, int
   }
 }
 
+// 4 channels per thread (C % 4 == 0, 16-byte aligned maps): float4 window loads and
+// stores, a quarter of the index math per output.
+__global__ void k_max_pool_nhwc4(const float4* __restrict__ x, int C4, int Hin, int Win, int Ho, int Wo, int pk,
+                                 int ps, int relu, int total, float4* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c = i % C4;
+    int t = i / C4;
+    const int ox = t % Wo;
+    t /= Wo;
+    const int oy = t % Ho;
+    const int n = t / Ho;
+    const float4* b = x + ((long)(n * Hin + oy * ps) * Win + ox * ps) * C4 + c;
+    float4 m = __ldg(b);
+    for (int dy = 0; dy < pk; ++dy)
+      for (int dx = 0; dx < pk; ++dx) {
+        const float4 v = __ldg(b + ((long)dy * Win + dx) * C4);
+        if (v.x > m.x || v.x != v.x) m.x = v.x;
+        if (v.y > m.y || v.y != v.y) m.y = v.y;
+        if (v.z > m.z || v.z != v.z) m.z = v.z;
+        if (v.w > m.w || v.w != v.w) m.w = v.w;
+      }
+    if (relu) {
+      if (m.x < 0.0f) m.x = 0.0f;
+      if (m.y < 0.0f) m.y = 0.0f;
+      if (m.z < 0.0f) m.z = 0.0f;
+      if (m.w < 0.0f) m.w = 0.0f;
+    }
+    out[i] = m;
+  }
+}
+
 int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
                          cudaStream_t s) {
   if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
   const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
   const long total = (long)N * Ho * Wo * C;
   if (total >= 0x7fffffffL || (long)N * Hin * Win * C >= 0x7fffffffL) return XNC_ENOTSUP;
+  if ((C & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+    const unsigned blocks = (unsigned)std::min<long>(cdivl(total / 4, 256), 148L * 16);
+    k_max_pool_nhwc4<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(x), C / 4, Hin, Win, Ho, Wo, pk, ps,
+                                            relu, (int)(total / 4), reinterpret_cast<float4*>(out));
+    return launch_status();
+  }
   const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
   k_max_pool_nhwc<<<blocks, 256, 0, s>>>(x, C, Hin, Win, Ho, Wo, pk, ps, relu, (int)total, out);
   return launch_status();
@@ -145,13 +182,44 @@ __global__ void k_pad_s2d_nhwc(const float* __restrict__ x, int C, int H, int W,
   }
 }
 
+// r = 4, channels-last: one thread per (n, yo, xo, c) writes its 16 outputs
+// (ii, jj) as four 16-byte stores (contiguous across threads with c fastest) from
+// four input row segments.
+__global__ void k_pad_s2d4_nhwc(const float* __restrict__ x, int C, int H, int W, int p, int Ho, int Wo, int total,
+                                float4* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c = i % C;
+    int t = i / C;
+    const int xo = t % Wo;
+    t /= Wo;
+    const int yo = t % Ho, n = t / Ho;
+    const float* plane = x + (long)(n * C + c) * H * W;
+    float4* o = out + (long)i * 4;  // 16 floats: (ii, jj) of channel c at pixel (yo, xo)
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int yi = yo * 4 + ii - p;
+      float v[4];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int xi = xo * 4 + jj - p;
+        v[jj] = (yi >= 0 && yi < H && xi >= 0 && xi < W) ? __ldg(plane + (long)yi * W + xi) : 0.0f;
+      }
+      o[ii] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  }
+}
+
 int launch_pad_s2d(const float* x, int N, int C, int H, int W, int p, int r, int nhwc, float* out,
                    cudaStream_t s) {
   if (r < 1 || p < 0 || (H + 2 * p) % r || (W + 2 * p) % r) return XNC_EINVAL;
   const int Hp = H + 2 * p, Ho = Hp / r, Wo = (W + 2 * p) / r;
   const long total = (long)N * C * Hp * Wo, out_total = (long)N * C * r * r * Ho * Wo;
   if (total >= 0x7fffffffL || out_total >= 0x7fffffffL) return XNC_ENOTSUP;
-  if (nhwc) {
+  if (nhwc && r == 4 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    const long tot = (long)N * C * Ho * Wo;
+    const unsigned blocks = (unsigned)std::min<long>(cdivl(tot, 256), 148L * 16);
+    k_pad_s2d4_nhwc<<<blocks, 256, 0, s>>>(x, C, H, W, p, Ho, Wo, (int)tot, reinterpret_cast<float4*>(out));
+  } else if (nhwc) {
     const unsigned blocks = (unsigned)std::min<long>(cdivl(out_total, 256), 148L * 16);
     k_pad_s2d_nhwc<<<blocks, 256, 0, s>>>(x, C, H, W, p, r, Ho, Wo, (int)out_total, out);
   } else {

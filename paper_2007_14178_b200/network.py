@@ -82,6 +82,7 @@ class XnorNetAlexNet:
         w12 = F.pad(self.conv1_w, (0, 1, 0, 1))
         self.conv1_w_s2d = (w12.view(96, 3, 3, 4, 3, 4).permute(0, 1, 3, 5, 2, 4)
                             .reshape(96, 48, 3, 3).contiguous())
+        self.conv1_w_s2d_cl = self.conv1_w_s2d.contiguous(memory_format=torch.channels_last)
         # XNOR-Net's binary block is BatchNorm -> BinActiv -> BinConv (-> Pool); the
         # batch norms are folded to a per-channel affine (scale, shift), random-init
         # like everything else.  After a pool it runs inside K1 of the next layer
@@ -126,11 +127,11 @@ class XnorNetAlexNet:
         settings as inside forward())."""
         with _tf32_full_precision_layers():
             # pad + space-to-depth and ReLU + pool are one pass each (our data-movement
-            # kernels, same values as F.pad / F.pixel_unshuffle and F.relu / F.max_pool2d).
-            # NCHW: cuDNN's channels-last conv is 0.22 ms faster here, but the
-            # channels-last s2d / pool passes cost more than that (tools/front_probe.py)
-            xs = ops.pad_space_to_depth(x, 2, 4)
-            h = F.conv2d(xs, self.conv1_w_s2d, self.conv1_b)
+            # kernels, same values as F.pad / F.pixel_unshuffle and F.relu / F.max_pool2d),
+            # channels-last end to end: cuDNN's NHWC TF32 conv is 0.39 vs 0.60 ms NCHW, and
+            # conv2's K1 reads the channels-last map directly (tools/front_probe.py)
+            xs = ops.pad_space_to_depth(x, 2, 4, channels_last=True)
+            h = F.conv2d(xs, self.conv1_w_s2d_cl, self.conv1_b)
             return ops.max_pool(h, 3, 2, relu=True)
 
     def _forward(self, x: torch.Tensor, return_features: bool):
