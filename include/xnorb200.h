@@ -120,10 +120,11 @@ int xnc_xnor_conv_umma_affine(const uint32_t* bits, const uint8_t* wq, const int
  * Max-pool in front of a binary layer (XNOR-Net: pool -> BN -> sign): out f32
  * [N][C][H][W] = max over pool_k x pool_k windows (stride pool_s, no padding) of
  * x [N][C][Hin][Win], H = (Hin - pool_k) / pool_s + 1; the values of
- * torch.max_pool2d (NaN propagates); relu != 0: torch.relu before the pool, in
- * the same pass.  pool_k <= 8. */
+ * torch.max_pool2d (NaN propagates).  bias f32 [C] (or NULL): pool of (x + bias),
+ * added after the max (max(v + b) == max(v) + b exactly: a conv's bias folded into
+ * the pool); relu != 0: torch.relu before the pool, in the same pass.  pool_k <= 8. */
 int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu,
-                 int nhwc, float* out, void* stream);
+                 int nhwc, const float* bias, float* out, void* stream);
 /* F.pixel_unshuffle(F.pad(x, pad on all sides), r) in one pass: out f32
  * [N][C*r*r][(H+2pad)/r][(W+2pad)/r] (conv1 11x11/4 as a 3x3 conv, network.py).
  * nhwc != 0 (xnc_max_pool too): the map is stored channels-last, [N][H][W][C]. */

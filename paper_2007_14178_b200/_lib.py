@@ -50,7 +50,7 @@ def lib() -> ctypes.CDLL:
         "xnc_umma_split_ws_bytes": ([I, I, I, I, I, I, I, I], S),
         "xnc_umma_emit_supported": ([I, I, I, I, I, I, I, I], I),
         "xnc_xnor_conv_umma_emit": ([P, P, P, P, P, I, I, I, I, I, I, I, I, P, P, P, P, P], I),
-        "xnc_max_pool": ([P, I, I, I, I, I, I, I, I, P, P], I),
+        "xnc_max_pool": ([P, I, I, I, I, I, I, I, I, P, P, P], I),
         "xnc_pad_space_to_depth": ([P, I, I, I, I, I, I, I, P, P], I),
         "xnc_pack_input_nhwc": ([P, I, I, I, I, P, P, P, P, P], I),
         "xnc_xnor_conv_umma_ws": ([P, P, P, P, P, I, I, I, I, I, I, I, I, P, P, P, P, P, P], I),

@@ -134,11 +134,11 @@ int xnc_xnor_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* s
 }
 
 int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu, int nhwc,
-                 float* out, void* stream) {
+                 const float* bias, float* out, void* stream) {
   if (!x || !out || N < 1 || C < 1 || pool_k < 1 || pool_k > 8 || pool_s < 1 || Hin < pool_k || Win < pool_k)
     return XNC_EINVAL;
-  return nhwc ? launch_max_pool_nhwc(x, N, C, Hin, Win, pool_k, pool_s, relu, out, as_stream(stream))
-              : launch_max_pool(x, N, C, Hin, Win, pool_k, pool_s, relu, out, as_stream(stream));
+  return nhwc ? launch_max_pool_nhwc(x, N, C, Hin, Win, pool_k, pool_s, relu, bias, out, as_stream(stream))
+              : launch_max_pool(x, N, C, Hin, Win, pool_k, pool_s, relu, bias, out, as_stream(stream));
 }
 
 int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, int r, int nhwc, float* out,

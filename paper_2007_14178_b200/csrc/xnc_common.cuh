@@ -58,12 +58,12 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
                      uint32_t* next_bits = nullptr, float* next_A = nullptr);
 bool umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad);
-int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
-                    cudaStream_t s);
+int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, const float* bias,
+                    float* out, cudaStream_t s);
 int launch_pad_s2d(const float* x, int N, int C, int H, int W, int p, int r, int nhwc, float* out,
                    cudaStream_t s);
-int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
-                         cudaStream_t s);
+int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu,
+                         const float* bias, float* out, cudaStream_t s);
 int launch_pack_input_nhwc(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A, cudaStream_t s,
                            const float* in_scale, const float* in_shift);
 }  // namespace xnc

@@ -15,8 +15,8 @@ namespace xnc {
 // so the values are torch.max_pool2d's; relu != 0 applies torch's relu after the
 // max (relu(max(w)) == max(relu(w)): the ReLU + pool of conv1 in one pass).
 template <int PK>
-__global__ void k_max_pool(const float* __restrict__ x, long planes, int Hin, int Win, int Ho, int Wo, int pk_rt,
-                           int ps, int relu, float* __restrict__ out) {
+__global__ void k_max_pool(const float* __restrict__ x, long planes, int C, int Hin, int Win, int Ho, int Wo,
+                           int pk_rt, int ps, int relu, const float* __restrict__ bias, float* __restrict__ out) {
   const int pk = PK > 0 ? PK : pk_rt;
   const long total = planes * Ho * Wo;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -35,6 +35,7 @@ __global__ void k_max_pool(const float* __restrict__ x, long planes, int Hin, in
         if (v > m || v != v) m = v;
       }
     }
+    if (bias != nullptr) m = __fadd_rn(m, __ldg(bias + (int)(pl % C)));  // max(v + b) == max(v) + b
     if (relu && m < 0.0f) m = 0.0f;  // clamp_min(0): NaN and -0.0 pass through
     out[i] = m;
   }
@@ -43,7 +44,8 @@ __global__ void k_max_pool(const float* __restrict__ x, long planes, int Hin, in
 // The same pool on channels-last (NHWC) maps, output NHWC: one thread per output
 // element with the channel fastest, so window loads and stores are coalesced.
 __global__ void k_max_pool_nhwc(const float* __restrict__ x, int C, int Hin, int Win, int Ho, int Wo, int pk,
-                                int ps, int relu, int total, float* __restrict__ out) {
+                                int ps, int relu, int total, const float* __restrict__ bias,
+                                float* __restrict__ out) {
   // 32-bit index math (host-checked): 64-bit div/mod made this pass 3x slower
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int c = i % C;
@@ -59,6 +61,7 @@ __global__ void k_max_pool_nhwc(const float* __restrict__ x, int C, int Hin, int
         const float v = __ldg(b + ((long)dy * Win + dx) * C);
         if (v > m || v != v) m = v;
       }
+    if (bias != nullptr) m = __fadd_rn(m, __ldg(bias + c));
     if (relu && m < 0.0f) m = 0.0f;
     out[i] = m;
   }
@@ -67,7 +70,8 @@ __global__ void k_max_pool_nhwc(const float* __restrict__ x, int C, int Hin, int
 // 4 channels per thread (C % 4 == 0, 16-byte aligned maps): float4 window loads and
 // stores, a quarter of the index math per output.
 __global__ void k_max_pool_nhwc4(const float4* __restrict__ x, int C4, int Hin, int Win, int Ho, int Wo, int pk,
-                                 int ps, int relu, int total, float4* __restrict__ out) {
+                                 int ps, int relu, int total, const float4* __restrict__ bias,
+                                 float4* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int c = i % C4;
     int t = i / C4;
@@ -85,6 +89,10 @@ __global__ void k_max_pool_nhwc4(const float4* __restrict__ x, int C4, int Hin, 
         if (v.z > m.z || v.z != v.z) m.z = v.z;
         if (v.w > m.w || v.w != v.w) m.w = v.w;
       }
+    if (bias != nullptr) {  // per-channel bias after the max: max(v + b) == max(v) + b exactly
+      const float4 b4 = __ldg(bias + c);
+      m.x = __fadd_rn(m.x, b4.x); m.y = __fadd_rn(m.y, b4.y); m.z = __fadd_rn(m.z, b4.z); m.w = __fadd_rn(m.w, b4.w);
+    }
     if (relu) {
       if (m.x < 0.0f) m.x = 0.0f;
       if (m.y < 0.0f) m.y = 0.0f;
@@ -95,35 +103,37 @@ __global__ void k_max_pool_nhwc4(const float4* __restrict__ x, int C4, int Hin, 
   }
 }
 
-int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
-                         cudaStream_t s) {
+int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu,
+                         const float* bias, float* out, cudaStream_t s) {
   if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
   const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
   const long total = (long)N * Ho * Wo * C;
   if (total >= 0x7fffffffL || (long)N * Hin * Win * C >= 0x7fffffffL) return XNC_ENOTSUP;
-  if ((C & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+  if ((C & 3) == 0 &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0) {
     const unsigned blocks = (unsigned)std::min<long>(cdivl(total / 4, 256), 148L * 16);
     k_max_pool_nhwc4<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(x), C / 4, Hin, Win, Ho, Wo, pk, ps,
-                                            relu, (int)(total / 4), reinterpret_cast<float4*>(out));
+                                            relu, (int)(total / 4), reinterpret_cast<const float4*>(bias),
+                                            reinterpret_cast<float4*>(out));
     return launch_status();
   }
   const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
-  k_max_pool_nhwc<<<blocks, 256, 0, s>>>(x, C, Hin, Win, Ho, Wo, pk, ps, relu, (int)total, out);
+  k_max_pool_nhwc<<<blocks, 256, 0, s>>>(x, C, Hin, Win, Ho, Wo, pk, ps, relu, (int)total, bias, out);
   return launch_status();
 }
 
-int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, float* out,
-                    cudaStream_t s) {
+int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, const float* bias,
+                    float* out, cudaStream_t s) {
   if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
   const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
   const long planes = (long)N * C, total = planes * Ho * Wo;
   const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
   if (pk == 3)
-    k_max_pool<3><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, relu, out);
+    k_max_pool<3><<<blocks, 256, 0, s>>>(x, planes, C, Hin, Win, Ho, Wo, pk, ps, relu, bias, out);
   else if (pk == 2)
-    k_max_pool<2><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, relu, out);
+    k_max_pool<2><<<blocks, 256, 0, s>>>(x, planes, C, Hin, Win, Ho, Wo, pk, ps, relu, bias, out);
   else
-    k_max_pool<0><<<blocks, 256, 0, s>>>(x, planes, Hin, Win, Ho, Wo, pk, ps, relu, out);
+    k_max_pool<0><<<blocks, 256, 0, s>>>(x, planes, C, Hin, Win, Ho, Wo, pk, ps, relu, bias, out);
   return launch_status();
 }
 

@@ -222,10 +222,25 @@ __global__ void __launch_bounds__(128) k_pack_small(const float* __restrict__ x,
   const bool in = q < npix;
   const long n = in ? q / HW : 0, p = in ? q - n * HW : 0;
   const float* xp = x + n * C * (long)HW + p;
-  for (int c = warp; c < C; c += 4) {
-    float v = in ? __ldg(xp + (long)c * HW) : 0.0f;
-    if (AFF) v = __fadd_rn(__fmul_rn(v, __ldg(in_scale + c)), __ldg(in_shift + c));
-    tile[c * 32 + lane] = v;
+  // 16 channel loads in flight per thread before any store (a load -> store loop
+  // waited out one memory latency per channel)
+  constexpr int kU = 16;
+  for (int c0 = warp; c0 < C; c0 += 4 * kU) {
+    float v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = c0 + 4 * u;
+      v[u] = (in && c < C) ? __ldg(xp + (long)c * HW) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = c0 + 4 * u;
+      if (c < C) {
+        float t = v[u];
+        if (AFF) t = __fadd_rn(__fmul_rn(t, __ldg(in_scale + c)), __ldg(in_shift + c));
+        tile[c * 32 + lane] = t;
+      }
+    }
   }
   __syncthreads();
   if (!in) return;

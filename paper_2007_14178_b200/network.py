@@ -131,8 +131,8 @@ class XnorNetAlexNet:
             # channels-last end to end: cuDNN's NHWC TF32 conv is 0.39 vs 0.60 ms NCHW, and
             # conv2's K1 reads the channels-last map directly (tools/front_probe.py)
             xs = ops.pad_space_to_depth(x, 2, 4, channels_last=True)
-            h = F.conv2d(xs, self.conv1_w_s2d_cl, self.conv1_b)
-            return ops.max_pool(h, 3, 2, relu=True)
+            h = F.conv2d(xs, self.conv1_w_s2d_cl)  # bias folded into the pool (exact: see max_pool)
+            return ops.max_pool(h, 3, 2, relu=True, bias=self.conv1_b)
 
     def _forward(self, x: torch.Tensor, return_features: bool):
         h = self.front_end(x)

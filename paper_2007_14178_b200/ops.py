@@ -68,9 +68,11 @@ def _channels_last(x: torch.Tensor) -> bool:
     return not x.is_contiguous() and x.is_contiguous(memory_format=torch.channels_last)
 
 
-def max_pool(x: torch.Tensor, k: int, s: int, relu: bool = False) -> torch.Tensor:
+def max_pool(x: torch.Tensor, k: int, s: int, relu: bool = False,
+             bias: torch.Tensor | None = None) -> torch.Tensor:
     """Max-pool k x k / stride s, no padding (torch.max_pool2d values), on the
-    device; relu=True: torch.relu first, in the same pass.  A channels-last x gives
+    device; bias f32 [C]: pool of x + bias (a conv's bias, added after the max:
+    exact); relu=True: torch.relu first, in the same pass.  A channels-last x gives
     a channels-last result."""
     _need_cuda(x, "x", torch.float32, channels_last_ok=True)
     nhwc = _channels_last(x)
@@ -80,8 +82,12 @@ def max_pool(x: torch.Tensor, k: int, s: int, relu: bool = False) -> torch.Tenso
     Ho, Wo = pool_dims(H, W, (k, s))
     fmt = torch.channels_last if nhwc else torch.contiguous_format
     out = torch.empty((N, C, Ho, Wo), dtype=torch.float32, device=x.device, memory_format=fmt)
+    if bias is not None:
+        _need_cuda(bias, "bias", torch.float32)
+        if bias.numel() != C:
+            raise ValueError(f"bias must have {C} entries")
     check(lib().xnc_max_pool(x.data_ptr(), N, C, H, W, int(k), int(s), int(bool(relu)), int(nhwc),
-                             out.data_ptr(), _stream(x.device)), "xnc_max_pool")
+                             _ptr(bias), out.data_ptr(), _stream(x.device)), "xnc_max_pool")
     return out
 
 

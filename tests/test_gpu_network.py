@@ -80,6 +80,10 @@ def test_relu_max_pool_matches_torch(shape, k, s):
     xl = x.contiguous(memory_format=torch.channels_last)  # channels-last in, channels-last out
     got = ops.max_pool(xl, k, s, relu=True)
     assert got.is_contiguous(memory_format=torch.channels_last) and torch.equal(got, want)
+    b = torch.randn(shape[1], device="cuda")  # a conv bias folded into the pool: exact
+    want_b = F.max_pool2d(F.relu(x + b.view(1, -1, 1, 1)), k, s)
+    assert torch.equal(ops.max_pool(x, k, s, relu=True, bias=b), want_b)
+    assert torch.equal(ops.max_pool(xl, k, s, relu=True, bias=b), want_b)
 
 
 @pytest.mark.parametrize("shape", [(3, 96, 27, 27), (2, 70, 5, 7), (2, 33, 4, 4)])
