@@ -1031,7 +1031,7 @@ static int split_factor(const PairGeom& g) {
 bool umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
   PairGeom g;
   size_t smem;
-  return pair_plan(N, C, H, W, O, kh, kw, pad, g, smem) && g.n_nb == 1;
+  return kPEpiWarps == 8 && pair_plan(N, C, H, W, O, kh, kw, pad, g, smem) && g.n_nb == 1;
 }
 
 size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
@@ -1095,6 +1095,8 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   size_t smem;
   if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
   if (next_bits != nullptr && g.n_nb != 1) return XNC_ENOTSUP;  // all channels of a pixel in one block
+  // the emitting epilogue splits each lane quadrant's chunks between exactly two warps
+  if (next_bits != nullptr && kPEpiWarps != 8) return XNC_ENOTSUP;
   if (next_bits != nullptr) split_ws = nullptr;
   // split K across CTA pairs when the caller passed the (zeroed) partial-sum buffer
   const int S = split_ws != nullptr ? split_factor(g) : 1;
