@@ -412,3 +412,45 @@ def test_layer_chain_with_emitted_signs():
     packed = l1.forward(x, emit_signs=True)
     got = l2.forward(packed)
     assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+
+
+def _random_shapes(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        k = int(rng.integers(1, 8))
+        kh, kw = (k, k) if rng.random() < 0.7 else (k, int(rng.integers(1, 8)))
+        pad = int(rng.integers(0, 4))
+        H, W = int(rng.integers(max(1, kh - 2 * pad), 40)), int(rng.integers(max(1, kw - 2 * pad), 40))
+        if H + 2 * pad < kh or W + 2 * pad < kw:
+            continue
+        out.append((int(rng.integers(1, 6)), int(rng.integers(1, 600)), H, W, int(rng.integers(1, 600)),
+                    kh, kw, pad))
+    return out
+
+
+@pytest.mark.parametrize("shape", _random_shapes(48, 2026), ids=lambda s: "x".join(map(str, s)))
+def test_random_shapes_umma_matches_popc(shape):
+    """Randomised shapes: the tcgen05 kernel (split K, MH = 1/2, odd channel and filter
+    tails, every pad) is bit-identical to the POPC kernel, ints and floats; the
+    sign-emitting epilogue, where it applies, matches K1 on the float output."""
+    from paper_2007_14178_b200 import ops
+    N, C, H, W, Oc, kh, kw, pad = shape
+    if not ops.umma_supported(N, C, H, W, Oc, kh, kw, pad):
+        pytest.skip("shape outside the tcgen05 plan")
+    rng = np.random.default_rng(list(shape))
+    dev = _dev()
+    x = torch.from_numpy(O.f32_exact(rng, (N, C, H, W))).to(dev)
+    w = torch.from_numpy(O.f32_exact(rng, (Oc, C, kh, kw))).to(dev)
+    filt = ops.pack_weights(w)
+    ops.attach_umma_weights(filt, w)
+    bits, A = ops.pack_input(x)
+    K = ops.scale_map(A, kh, kw, pad)
+    yu, au = ops.xnor_conv(bits, filt, K, pad, want_acc=True, variant="umma")
+    yp, ap = ops.xnor_conv(bits, filt, K, pad, want_acc=True, variant="popc")
+    assert torch.equal(au, ap)
+    assert torch.equal(yu.view(torch.int32), yp.view(torch.int32))
+    if ops.umma_emit_supported(N, C, H, W, Oc, kh, kw, pad):
+        got = ops.xnor_conv_emit(bits, filt, K, pad)
+        wb, wa = ops.pack_input(yu.contiguous())
+        assert torch.equal(got.bits, wb) and torch.equal(got.A.view(torch.int32), wa.view(torch.int32))
