@@ -74,7 +74,11 @@ namespace xnc {
 #define XNC_EPI_WARPS 8
 #endif
 constexpr int kPEpiWarps = XNC_EPI_WARPS;  // multiple of 4 (one group per TMEM lane quadrant)
-constexpr int kPThreads = 128 + 32 * kPEpiWarps;
+#ifndef XNC_A_WARPS_EXTRA
+#define XNC_A_WARPS_EXTRA 0  // A-producer warps after the epilogue warps (besides warps 2-3)
+#endif
+constexpr int kPAExtra = XNC_A_WARPS_EXTRA;
+constexpr int kPThreads = 128 + 32 * kPEpiWarps + 32 * kPAExtra;
 #ifndef XNC_A_ROWS
 #define XNC_A_ROWS 4  // A producer: bit rows per thread per batch (x 2 planes) loaded before expanding
 #endif
@@ -89,7 +93,7 @@ constexpr int kPCPS = XNC_PCPS;        // (tap, K block) chunks per B stage: one
 constexpr int kPMaxKB = 4;       // K blocks (128 channels each) of a tile resident: C <= 512
 constexpr int kPMaxA = 2 * kPMaxKB;  // A plane ring: two tiles' planes when they fit
 constexpr int kPAWarp0 = 2;      // first A-producer warp
-constexpr int kPAWarps = 2;
+constexpr int kPAWarps = 2 + kPAExtra;  // A-producer warps: 2, 3 and any extra after the epilogue
 constexpr int kPEpiWarp0 = 4;    // first epilogue warp
 constexpr int kProfSlots = 16;
 
@@ -446,9 +450,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       }
       if (prof) g_umma_prof[blockIdx.x][7] = w_be;
     }
-  } else if (warp >= kPAWarp0 && warp < kPAWarp0 + kPAWarps) {
+  } else if ((warp >= kPAWarp0 && warp < kPAWarp0 + 2) || warp >= kPEpiWarp0 + kPEpiWarps) {
     // ================= A producers: packed bits -> swizzled d-bytes, per K block
-    const int pt = tid - kPAWarp0 * 32, n_pt = kPAWarps * 32;
+    const int a_w = warp < kPEpiWarp0 ? warp - kPAWarp0 : 2 + (warp - kPEpiWarp0 - kPEpiWarps);
+    const int pt = a_w * 32 + lane, n_pt = kPAWarps * 32;
     const bool prof = (dbg & 128) && pt == 0;
     unsigned long long w_ae = 0;
     const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
