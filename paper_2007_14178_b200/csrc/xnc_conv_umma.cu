@@ -355,6 +355,8 @@ struct PairGeom {
                      // layers): the units add raw partial sums into a zeroed s32 buffer
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
+  int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
+                   // epilogue carries a pixel's running |.| sum and sign words across the blocks)
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
              // (kPCPS == 1 only), bit 8 = no B protocol at all after the first fill, bit 2 = build the
              // input planes once, bit 5 = epilogue does only the TMEM handshake, bit 6 = chunk
@@ -370,6 +372,23 @@ __device__ __forceinline__ uint4 d_bytes16(uint32_t bits16, uint32_t valid16) {
   r.z = (((d >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
   r.w = (((d >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
   return r;
+}
+
+// The i-th work unit of CTA pair `cluster` (-1 past the end): units strided over the
+// pairs, or, tile-major, whole tiles strided over the pairs with their filter blocks
+// back to back.  Every role walks the same sequence.
+__device__ __forceinline__ int unit_at(const PairGeom& g, int cluster, int n_clusters, int i) {
+  if (!g.tile_major) {
+    const int u = cluster + i * n_clusters;
+    return u < g.units ? u : -1;
+  }
+  const int t = cluster + (i / g.n_nb) * n_clusters;
+  return t < g.tiles ? t * g.n_nb + i % g.n_nb : -1;
+}
+
+__device__ __forceinline__ int units_of(const PairGeom& g, int cluster, int n_clusters) {
+  if (!g.tile_major) return (g.units - cluster + n_clusters - 1) / n_clusters;
+  return ((g.tiles - cluster + n_clusters - 1) / n_clusters) * g.n_nb;
 }
 
 // MH = M=128 row blocks per CTA (pair tile = 2*MH*128 extended pixels); the two
@@ -424,10 +443,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       const bool prof = dbg & 128;
       unsigned long long w_be = 0;
       const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
-      const int my_units = (g.units - cluster + n_clusters - 1) / n_clusters;
+      const int my_units = units_of(g, cluster, n_clusters);
       const uint32_t total = (uint32_t)my_units * g.KBu * g.taps;
       uint32_t step = 0;
-      for (int u = cluster; u < g.units; u += n_clusters) {
+      for (int iu = 0;; ++iu) {
+        const int u = unit_at(g, cluster, n_clusters, iu);
+        if (u < 0) break;
         const int nb = (u / g.S) % g.n_nb, kbu0 = (u % g.S) * g.KBu;
           for (int kb = kbu0; kb < kbu0 + g.KBu; ++kb)
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
@@ -467,7 +488,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     constexpr int kAR = XNC_A_ROWS;
     const int grp = g.a_unit ? g.KBu : 1;
     uint32_t it = 0;  // units of this pair so far: every unit builds its KBu planes
-    for (int u = cluster; u < g.units; u += n_clusters, ++it) {
+    for (;; ++it) {
+      const int u = unit_at(g, cluster, n_clusters, (int)it);
+      if (u < 0) break;
       const int t = u / (g.n_nb * g.S), kbu0 = (u % g.S) * g.KBu;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
@@ -571,13 +594,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
       const uint32_t row_skip = (uint32_t)(g.IC - g.kw + 1) * 8u;  // next tap row, in descriptor units
       const bool prof = PROF && (dbg & 128) && lane == 0;
       const bool trace = PROF && (dbg & 64) && blockIdx.x == 0 && lane == 0;
-      const int my_units = (g.units - cluster + n_clusters - 1) / n_clusters;
+      const int my_units = units_of(g, cluster, n_clusters);
       uint32_t left = (uint32_t)my_units * g.KBu * g.taps;  // chunks still to issue
       unsigned long long w_te = 0, w_af = 0, w_bf = 0, n_mma = 0;
       const unsigned long long t_start = PROF ? clock64() : 0ull;
       uint32_t j = 0, st = 0, ph = 0, stages = 0, step = 0;  // chunk in stage, stage slot, parity, stages done
       uint32_t item = 0;
-      for (int u = cluster; u < g.units; u += n_clusters, ++item) {
+      for (;; ++item) {
+        const int u = unit_at(g, cluster, n_clusters, (int)item);
+        if (u < 0) break;
         const uint32_t buf = item & 1;
         if (item >= 2) {
           mbar_wait_prof(&t_empty[buf], ((item >> 1) - 1) & 1, prof, w_te);
@@ -655,7 +680,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     // 32-bit filter-plane stride for the hot path (host guarantees O*oh*ow < 2^31)
     const int plane_out32 = g.oh * g.ow;
     const bool fast = y != nullptr && acc_out == nullptr;
-    for (int u = cluster; u < g.units; u += n_clusters, ++item) {
+    float emit_sA[MH];  // sign-emitting epilogue: running |.| sum of each pixel across filter blocks
+#pragma unroll
+    for (int h = 0; h < MH; ++h) emit_sA[h] = 0.0f;
+    for (;; ++item) {
+      const int u = unit_at(g, cluster, n_clusters, (int)item);
+      if (u < 0) break;
       const int t = u / (g.n_nb * g.S), nb = (u / g.S) % g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);
@@ -690,12 +720,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         const bool vec_c = vec_ok && ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
                            (out_scale == nullptr || (((reinterpret_cast<uintptr_t>(out_scale) |
                                                        reinterpret_cast<uintptr_t>(out_shift)) & 15) == 0));
-        float sA[MH];
+        // tile-major with several filter blocks: the running sum continues across the
+        // tile's blocks (this thread owns the same pixels in each), in channel order
+        if (nb == 0) {
+#pragma unroll
+          for (int h = 0; h < MH; ++h) emit_sA[h] = 0.0f;
+        }
+        float* sA = emit_sA;
         uint32_t word[MH];
 #pragma unroll
-        for (int h = 0; h < MH; ++h) { sA[h] = 0.0f; word[h] = 0u; }
+        for (int h = 0; h < MH; ++h) word[h] = 0u;
+        const int wbase = nb * (g.NP >> 5);  // this block's first sign word of the pixel
         for (int ch = c_lo; ch < c_hi; ++ch) {
-          const int obase = ch * 16;
+          const int obase = nb * g.NP + ch * 16;
           uint32_t v[MH][16];
 #pragma unroll
           for (int h = 0; h < MH; ++h) tmem_ld16_async(tbase + h * g.NP + ch * 16, v[h]);
@@ -742,7 +779,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
             }
             if (cg == 1) tmem_st16(tbase + h * g.NP + ch * 16, absv);
             if ((ch & 1) || ch == n_chunks - 1) {
-              if (ok[h]) next_bits[qix[h] * Cw_next + (ch >> 1)] = word[h];
+              if (ok[h] && wbase + (ch >> 1) < Cw_next) next_bits[qix[h] * Cw_next + wbase + (ch >> 1)] = word[h];
               word[h] = 0u;
             }
           }
@@ -763,11 +800,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
             for (int h = 0; h < MH; ++h)
 #pragma unroll
               for (int j = 0; j < 16; ++j)
-                if (ch * 16 + j < g.O) sA[h] = __fadd_rn(sA[h], __uint_as_float(v[h][j]));
+                if (nb * g.NP + ch * 16 + j < g.O) sA[h] = __fadd_rn(sA[h], __uint_as_float(v[h][j]));
           }
+          if (nb == g.n_nb - 1) {
 #pragma unroll
-          for (int h = 0; h < MH; ++h)
-            if (ok[h] && next_A != nullptr) next_A[qix[h]] = __fmul_rn(sA[h], g.inv_O);
+            for (int h = 0; h < MH; ++h)
+              if (ok[h] && next_A != nullptr) next_A[qix[h]] = __fmul_rn(sA[h], g.inv_O);
+          }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
@@ -1036,7 +1075,7 @@ static int split_factor(const PairGeom& g) {
 bool umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
   PairGeom g;
   size_t smem;
-  return kPEpiWarps == 8 && pair_plan(N, C, H, W, O, kh, kw, pad, g, smem) && g.n_nb == 1;
+  return kPEpiWarps == 8 && pair_plan(N, C, H, W, O, kh, kw, pad, g, smem);
 }
 
 size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
@@ -1099,7 +1138,9 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   PairGeom g;
   size_t smem;
   if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
-  if (next_bits != nullptr && g.n_nb != 1) return XNC_ENOTSUP;  // all channels of a pixel in one block
+  // several filter blocks: a pair takes whole tiles (all blocks back to back), so the
+  // emitting epilogue sees every channel of its pixels in order
+  if (next_bits != nullptr && g.S != 1) return XNC_ENOTSUP;
   // the emitting epilogue splits each lane quadrant's chunks between exactly two warps
   if (next_bits != nullptr && kPEpiWarps != 8) return XNC_ENOTSUP;
   if (next_bits != nullptr) split_ws = nullptr;
@@ -1126,7 +1167,8 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     g.debug = dbg;
   }
   const int sms = sm_count();
-  const int pairs = g.units < sms / 2 ? g.units : sms / 2;
+  const int work = (next_bits != nullptr && g.n_nb > 1) ? g.tiles : g.units;  // tile-major: tiles per pair
+  const int pairs = work < sms / 2 ? work : sms / 2;
   static size_t attr_smem[4] = {0, 0, 0, 0};  // one-time (per size increase) shared-memory opt-in
   auto kern = g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true> : k_conv_umma_pair<2, false>)
                         : (g.debug ? k_conv_umma_pair<1, true> : k_conv_umma_pair<1, false>);
@@ -1141,6 +1183,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
   }
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
+  g.tile_major = next_bits != nullptr && g.n_nb > 1;
   kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
                                           next_bits, next_A);
   if (part != nullptr) {

@@ -57,6 +57,7 @@ BINARY_LAYERS = (  # name, C_in, C_out, k, pad
     ("fc7", 4096, 4096, 1, 0),
 )
 POOLED_INPUT = ("conv3", "fc6")  # layers whose input is max-pool 3/2 of the previous output
+EMITS_NEXT = ("conv3", "conv4")   # binary -> binary with no pool between: the epilogue emits signs
 BINARY_MACS_PER_IMAGE = (27 * 27 * 256 * 96 * 25 + 13 * 13 * 384 * 256 * 9 + 13 * 13 * 384 * 384 * 9
                          + 13 * 13 * 256 * 384 * 9 + 4096 * 256 * 36 + 4096 * 4096)
 
@@ -65,7 +66,7 @@ class XnorNetAlexNet:
     """Random-init XNOR-Net AlexNet resident on one device."""
 
     def __init__(self, device: torch.device | str = "cuda", num_classes: int = 1000, seed: int = 0,
-                 variant: str = "auto"):
+                 variant: str = "auto", emit_signs: bool = True):
         dev = torch.device(device)
         g = torch.Generator().manual_seed(seed)
 
@@ -73,6 +74,7 @@ class XnorNetAlexNet:
             return ((torch.rand(shape, generator=g) * 2 - 1) * scale).to(dev)
 
         self.device = dev
+        self.emit_signs = emit_signs and variant in ("auto", "umma")
         self.conv1_w = rnd(96, 3, 11, 11, scale=(3 * 121) ** -0.5)
         self.conv1_b = rnd(96, scale=0.1)
         # conv1 as a 3x3/1 conv over the 4x4 space-to-depth input (48 channels):
@@ -138,8 +140,11 @@ class XnorNetAlexNet:
         h = self.front_end(x)
         feats = {}
         for name, *_ in BINARY_LAYERS:
-            # conv3 / fc6 take the pre-pool map (their in_pool)
-            h = self.binary[name](h)  # NCHW or channels-last (conv2's input)
+            # conv3 / fc6 take the pre-pool map (their in_pool); conv3 and conv4 hand the
+            # next layer its input in packed-sign form (sign-emitting epilogue, exact)
+            # unless the float feature maps are asked for
+            emit = self.emit_signs and not return_features and name in EMITS_NEXT
+            h = self.binary[name].forward(h, emit_signs=emit)  # NCHW / channels-last / packed
             feats[name] = h
         logits = F.linear(h.flatten(1), self.fc8_w, self.fc8_b)  # full precision
         return (logits, feats) if return_features else logits

@@ -115,3 +115,13 @@ def test_network_cuda_graph_matches_eager():
         torch.cuda.synchronize()
         assert torch.equal(logits, net.forward(x))
         x.copy_(torch.rand_like(x) * 2 - 1)
+
+
+def test_network_emitted_signs_match_float_chain():
+    """conv3 -> conv4 -> conv5 through the sign-emitting epilogue (the default forward)
+    give exactly the logits of the float-feature-map chain."""
+    from paper_2007_14178_b200.network import XnorNetAlexNet
+    a = XnorNetAlexNet("cuda", seed=5)
+    b = XnorNetAlexNet("cuda", seed=5, emit_signs=False)
+    x = torch.rand((3, 3, 224, 224), device="cuda") * 2 - 1
+    assert torch.equal(a.forward(x), b.forward(x))

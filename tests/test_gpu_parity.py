@@ -367,7 +367,10 @@ def test_layer_in_pool_matches_pooled_layer():
 
 
 @pytest.mark.parametrize("shape", [(2, 64, 20, 20, 256, 3, 3, 1), (1, 96, 14, 14, 250, 3, 3, 1),
-                                   (3, 32, 13, 13, 96, 5, 5, 2), (2, 200, 9, 9, 33, 3, 3, 1)],
+                                   (3, 32, 13, 13, 96, 5, 5, 2), (2, 200, 9, 9, 33, 3, 3, 1),
+                                   # several filter blocks: tile-major pairs, running sum carried
+                                   (4, 256, 13, 13, 384, 3, 3, 1), (2, 96, 11, 11, 300, 3, 3, 1),
+                                   (1, 64, 17, 9, 520, 3, 3, 1)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("affine", [False, True])
 def test_sign_emitting_epilogue(shape, affine):
