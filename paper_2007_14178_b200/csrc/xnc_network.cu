@@ -69,9 +69,13 @@ __global__ void k_max_pool_nhwc(const float* __restrict__ x, int C, int Hin, int
 
 // 4 channels per thread (C % 4 == 0, 16-byte aligned maps): float4 window loads and
 // stores, a quarter of the index math per output.
-__global__ void k_max_pool_nhwc4(const float4* __restrict__ x, int C4, int Hin, int Win, int Ho, int Wo, int pk,
+template <int PK>
+__global__ void k_max_pool_nhwc4(const float4* __restrict__ x, int C4, int Hin, int Win, int Ho, int Wo, int pk_rt,
                                  int ps, int relu, int total, const float4* __restrict__ bias,
                                  float4* __restrict__ out) {
+  // PK > 0: the window loops unroll, so all PK*PK loads are in flight at once (a
+  // runtime-bounded loop issued them one round trip at a time: 2 TB/s)
+  const int pk = PK > 0 ? PK : pk_rt;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int c = i % C4;
     int t = i / C4;
@@ -81,14 +85,19 @@ __global__ void k_max_pool_nhwc4(const float4* __restrict__ x, int C4, int Hin, 
     const int n = t / Ho;
     const float4* b = x + ((long)(n * Hin + oy * ps) * Win + ox * ps) * C4 + c;
     float4 m = __ldg(b);
-    for (int dy = 0; dy < pk; ++dy)
-      for (int dx = 0; dx < pk; ++dx) {
+#pragma unroll
+    for (int dy = 0; dy < (PK > 0 ? PK : 8); ++dy) {
+      if (PK == 0 && dy >= pk) break;
+#pragma unroll
+      for (int dx = 0; dx < (PK > 0 ? PK : 8); ++dx) {
+        if (PK == 0 && dx >= pk) break;
         const float4 v = __ldg(b + ((long)dy * Win + dx) * C4);
         if (v.x > m.x || v.x != v.x) m.x = v.x;
         if (v.y > m.y || v.y != v.y) m.y = v.y;
         if (v.z > m.z || v.z != v.z) m.z = v.z;
         if (v.w > m.w || v.w != v.w) m.w = v.w;
       }
+    }
     if (bias != nullptr) {  // per-channel bias after the max: max(v + b) == max(v) + b exactly
       const float4 b4 = __ldg(bias + c);
       m.x = __fadd_rn(m.x, b4.x); m.y = __fadd_rn(m.y, b4.y); m.z = __fadd_rn(m.z, b4.z); m.w = __fadd_rn(m.w, b4.w);
@@ -112,9 +121,9 @@ int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk,
   if ((C & 3) == 0 &&
       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0) {
     const unsigned blocks = (unsigned)std::min<long>(cdivl(total / 4, 256), 148L * 16);
-    k_max_pool_nhwc4<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(x), C / 4, Hin, Win, Ho, Wo, pk, ps,
-                                            relu, (int)(total / 4), reinterpret_cast<const float4*>(bias),
-                                            reinterpret_cast<float4*>(out));
+    auto kern = pk == 3 ? k_max_pool_nhwc4<3> : pk == 2 ? k_max_pool_nhwc4<2> : k_max_pool_nhwc4<0>;
+    kern<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(x), C / 4, Hin, Win, Ho, Wo, pk, ps, relu,
+                                (int)(total / 4), reinterpret_cast<const float4*>(bias), reinterpret_cast<float4*>(out));
     return launch_status();
   }
   const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
