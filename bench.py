@@ -686,8 +686,12 @@ def main():
         res = run_ours(args, args.config)
         ws, rank, _ = dist_env()
         if res is not None and rank == 0 and ws == 1 and not args.no_ksweep:
-            res["network_C4"] = network_summary(args.variant)
-            res["binary_stack_C3"] = binary_stack_summary()
+            for key, fn in (("network_C4", lambda: network_summary(args.variant)),
+                            ("binary_stack_C3", binary_stack_summary)):
+                try:  # extras: report a failure, never lose the main line
+                    res[key] = fn()
+                except Exception as exc:
+                    res[key] = {"error": repr(exc)}
         if res is not None and rank == 0 and ws == 1 and not args.no_cpu:
             try:
                 res["cpu_baseline"] = cpu_baseline_fields(args.config, args.cpu_budget, res.get("ksweep"))
