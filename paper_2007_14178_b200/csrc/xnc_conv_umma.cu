@@ -307,6 +307,9 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]
 #ifndef XNC_ST_HINT
 #define XNC_ST_HINT ".cs"
 #endif
+#ifndef XNC_EMIT_SPLIT
+#define XNC_EMIT_SPLIT 8
+#endif
 #ifndef XNC_PAIR_ST
 #define XNC_PAIR_ST 1
 #endif
@@ -730,7 +733,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         // two-warp barrier per lane quadrant) continues its running sum over the
         // upper chunks' |y'| from TMEM -- the same order as K1, half the work each.
         const int Cw_next = (g.O + 31) >> 5;
-        const int half = (n_chunks / 4) * 2;  // group 0: chunks [0, half); even: words never split
+        // group 0: chunks [0, half) in full, then the sum over the rest from TMEM; even:
+        // words never split.  XNC_EMIT_SPLIT / 16 of the chunks go to group 0.
+        const int half = ((n_chunks * XNC_EMIT_SPLIT) / 32) * 2;
         const int c_lo = cg == 0 ? 0 : half, c_hi = cg == 0 ? half : n_chunks;
         const bool vec_c = vec_ok && ((reinterpret_cast<uintptr_t>(sw) & 15) == 0) &&
                            (out_scale == nullptr || (((reinterpret_cast<uintptr_t>(out_scale) |
