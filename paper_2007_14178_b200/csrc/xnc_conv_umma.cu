@@ -367,6 +367,7 @@ struct PairGeom {
                      // layers): the units add raw partial sums into a zeroed s32 buffer
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
+  int cst_O;    // > 0: sw / alpha staged in shared memory (cst_O entries each, after the B ring)
   int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
                    // epilogue carries a pixel's running |.| sum and sign words across the blocks)
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
@@ -416,6 +417,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
   uint8_t* b_s = a_s + (size_t)g.NA * g.plane_bytes;     // stages x NP/2 rows x 128 B
+  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)kPStages * kPCPS * g.b_half_bytes);  // [cst_O]
+  float* al_s = reinterpret_cast<float*>(sw_s + g.cst_O);                                           // [cst_O]
   __shared__ __align__(8) uint64_t b_full[kPStages], b_empty[kPStages];
   __shared__ __align__(8) uint64_t a_full[kPMaxA], a_empty[kPMaxA];
   __shared__ __align__(8) uint64_t t_full[2], t_empty[2];
@@ -698,6 +701,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
     // at C3 (MH = 1), so MH = 2 only.
     const bool pair_st = XNC_PAIR_ST && MH == 2 && (g.IC & 1) == 0 && (g.ow & 1) == 0 && ((g.oh * g.ow) & 1) == 0 &&
                          ((reinterpret_cast<uintptr_t>(y) & 7) == 0);
+    if (g.cst_O > 0) {  // stage the per-filter constants once (epilogue warps only)
+      const int et = tid - kPEpiWarp0 * 32;
+      for (int o = et; o < g.cst_O; o += 32 * kPEpiWarps) {
+        sw_s[o] = o < g.O ? __ldg(sw + o) : 0;
+        al_s[o] = o < g.O ? __ldg(alpha + o) : 0.0f;
+      }
+      named_bar_sync(6, 32 * kPEpiWarps);
+    }
     float emit_sA[MH];  // sign-emitting epilogue: running |.| sum of each pixel across filter blocks
 #pragma unroll
     for (int h = 0; h < MH; ++h) emit_sA[h] = 0.0f;
@@ -843,7 +854,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
         // while the TMEM loads are in flight
         int swv[16];
         float av[16];
-        if (vec_ok && obase + 16 <= g.O) {
+        if (g.cst_O > 0 && obase + 16 <= g.cst_O) {  // shared-memory copy (zeros past O)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int4 si = reinterpret_cast<const int4*>(sw_s + obase)[q];
+            const float4 ai = reinterpret_cast<const float4*>(al_s + obase)[q];
+            swv[4 * q] = si.x; swv[4 * q + 1] = si.y; swv[4 * q + 2] = si.z; swv[4 * q + 3] = si.w;
+            av[4 * q] = ai.x; av[4 * q + 1] = ai.y; av[4 * q + 2] = ai.z; av[4 * q + 3] = ai.w;
+          }
+        } else if (vec_ok && obase + 16 <= g.O) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int4 si = __ldg(reinterpret_cast<const int4*>(sw + obase) + q);
@@ -1056,7 +1075,11 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   g.b_half_bytes = (uint32_t)(g.NP / 2) * 128u;
   const int cols = 2 * MH * g.NP;  // two accumulators x MH row blocks
   g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
-  const size_t b_bytes = (size_t)kPStages * kPCPS * g.b_half_bytes + 1024;
+  // S_w and alpha of every filter staged in shared memory for the epilogue (O <= 1024):
+  // its per-chunk constant loads were L1/L2 misses under the store stream (ncu: the
+  // first use after them was the epilogue's top stall, 12 % of samples)
+  g.cst_O = O <= 1024 ? round_up(O, 16) : 0;
+  const size_t b_bytes = (size_t)kPStages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 8;
   // A plane ring: two units' planes when they fit (the next unit's planes are
   // built during this unit's MMAs), else fewer; long K (fully connected layers
   // viewed as 1 x N images) streams through the ring.
