@@ -380,22 +380,20 @@ def run_ours(args, cfg_name):
         props = torch.cuda.get_device_properties(dev)
         sms = props.multi_processor_count
         peak_probe = None
+        peak_alt = None
         if kernel == "umma":
-            # The driver-measured dense bf16 peak (burst: the conv is timed on its own
-            # events) x 2 for the i8 tensor rate (B200: 4.5 POPS i8 vs 2.25 PFLOPS bf16;
-            # probe: 7874 vs 4096 MAC/clk/SM); 1 MAC = 2 binops, so i8 MAC/s x 2 =
-            # 2 x bf16 TFLOP/s in Tbinop/s.
+            # MEASURED_PEAKS has no int8 entry, so the peak is B200_PROFILING.md's dense
+            # fp8/int8 tensor rate, 4.5 POPS = 2.25e15 MAC/s = 4500 Tbinop/s (1 MAC = 2
+            # binops); our own kind::i8 probe at sm_max_mhz (7874 MAC/clk/SM) gives
+            # 4580.  2 x the driver-measured bf16 burst (the cuBLAS GEMM reaches ~73 % of
+            # its nominal rate) is reported beside: the conv exceeds it.
             bf16 = peaks.get("bf16_tflops")
             peak_probe = 2 * UMMA_I8_MAC_PER_CLK_SM * sms * f_max / 1e12
-            if bf16:
-                peak_tbinops = 2.0 * float(bf16)
-                basis = (f"2 x MEASURED_PEAKS bf16_tflops {float(bf16):.1f} (burst; i8 tensor rate = 2 x bf16) "
-                         f"= i8 MAC/s x 2 binops")
-            else:
-                peak_tbinops = peak_probe
-                basis = (f"{UMMA_I8_MAC_PER_CLK_SM} tcgen05 kind::i8 MAC/clk/SM (measured, "
-                         f"profiles/umma_probe_r1.jsonl) x 2 binops x {sms} SMs x "
-                         f"{f_max / 1e6:.0f} MHz (sm_max_mhz, {peaks_src}; no bf16 peak measured)")
+            peak_tbinops = 4500.0
+            basis = ("fallback B200_PROFILING.md: dense fp8/int8 tensor 4.5 POPS = 2.25e15 MAC/s x 2 binops "
+                     "(MEASURED_PEAKS.json has no int8 entry)")
+            peak_alt = {"2x_measured_bf16_burst": 2.0 * float(bf16) if bf16 else None,
+                        "i8_probe_at_sm_max": peak_probe}
             bound = "tensor"
         else:
             peak_tbinops = 2 * POPC_LANES_PER_CLK_SM * 32 * sms * f_max / 1e12
@@ -430,7 +428,7 @@ def run_ours(args, cfg_name):
                          "peak": peak_tbinops, "unit": "Tbinop/s", "frac": achieved / peak_tbinops,
                          "traffic": traffic,
                          "peak_basis": basis,
-                         "peak_probe_at_sm_max": peak_probe,
+                         "peak_alternatives_Tbinop_s": peak_alt,
                          "frac_of_probe_peak": (achieved / peak_probe) if peak_probe else None},
             "pack_roofline": {"bound": "hbm", "achieved": pack_bytes / (per_kernel["pack_input"] * 1e-3) / 1e9,
                               "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
