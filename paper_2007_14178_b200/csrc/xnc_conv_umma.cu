@@ -83,7 +83,7 @@ constexpr int kPThreads = 128 + 32 * kPEpiWarps + 32 * kPAExtra;
 #define XNC_A_ROWS 4  // A producer: bit rows per thread per batch (x 2 planes) loaded before expanding
 #endif
 #ifndef XNC_PSTAGES
-#define XNC_PSTAGES 4
+#define XNC_PSTAGES 6
 #endif
 #ifndef XNC_PCPS
 #define XNC_PCPS 1
