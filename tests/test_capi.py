@@ -52,6 +52,33 @@ def test_abi_version_and_errors_without_gpu():
     assert L.xnc_layer_workspace_bytes(1, 64, 8, 8, 9, 9, 1) == 0  # k > 8 rejected
 
 
+def test_newer_entry_points_validate_before_device_work():
+    """The network / binary-stack / K-split entry points reject bad arguments with
+    XNC_EINVAL (1) before any CUDA call, so this runs without a GPU."""
+    from paper_2007_14178_b200._lib import lib
+    L = lib()
+    EINVAL = 1
+    # max-pool: NULL tensors, pool larger than the map, kernel > 8
+    assert L.xnc_max_pool(None, 1, 1, 8, 8, 3, 2, 0, 0, None, None, None) == EINVAL
+    assert L.xnc_max_pool(1, 1, 1, 2, 2, 3, 2, 0, 0, None, 1, None) == EINVAL
+    assert L.xnc_max_pool(1, 1, 1, 16, 16, 9, 2, 0, 0, None, 1, None) == EINVAL
+    # pad + space-to-depth: padded size not a multiple of r
+    assert L.xnc_pad_space_to_depth(1, 1, 3, 9, 10, 1, 4, 0, 1, None) == EINVAL
+    assert L.xnc_pad_space_to_depth(None, 1, 3, 224, 224, 2, 4, 0, 1, None) == EINVAL
+    # channels-last K1: NULL x, and a scale without a shift
+    assert L.xnc_pack_input_nhwc(None, 1, 8, 4, 4, None, None, 1, None, None) == EINVAL
+    assert L.xnc_pack_input_nhwc(1, 1, 8, 4, 4, 1, None, 1, None, None) == EINVAL
+    # sign-emitting conv: no next_bits buffer
+    assert L.xnc_xnor_conv_umma_emit(1, 1, 1, 1, 1, 1, 64, 8, 8, 32, 3, 3, 1, None, None, None, None,
+                                     None) == EINVAL
+    # K-split conv: neither y nor acc
+    assert L.xnc_xnor_conv_umma_ws(1, 1, 1, 1, 1, 1, 64, 8, 8, 32, 3, 3, 1, None, None, None, None, None,
+                                   None) == EINVAL
+    # size queries: impossible shapes report 0
+    assert L.xnc_umma_split_ws_bytes(1, 64, 8, 8, 0, 3, 3, 1) == 0
+    assert L.xnc_umma_emit_supported(1, 64, 8, 8, 0, 3, 3, 1) == 0
+
+
 def test_product_package_never_imports_the_oracle():
     for path in glob.glob(os.path.join(PKG, "**", "*.py"), recursive=True):
         src = open(path).read()
