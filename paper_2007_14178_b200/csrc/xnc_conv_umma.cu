@@ -93,7 +93,6 @@ constexpr int kPCPS = XNC_PCPS;        // (tap, K block) chunks per B stage: one
 constexpr int kPMaxKB = 4;       // K blocks (128 channels each) of a tile resident: C <= 512
 constexpr int kPMaxA = 2 * kPMaxKB;  // A plane ring: two tiles' planes when they fit
 constexpr int kPAWarp0 = 2;      // first A-producer warp
-constexpr int kPAWarps = 2 + kPAExtra;  // A-producer warps: 2, 3 and any extra after the epilogue
 constexpr int kPEpiWarp0 = 4;    // first epilogue warp
 constexpr int kProfSlots = 16;
 
@@ -406,8 +405,11 @@ __device__ __forceinline__ int units_of(const PairGeom& g, int cluster, int n_cl
 
 // MH = M=128 row blocks per CTA (pair tile = 2*MH*128 extended pixels); the two
 // TMEM accumulators hold MH x NP columns each (MH * NP <= 256).
-template <int MH, bool PROF>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv_umma_pair(
+// AX = A-producer warps beyond warps 2-3 (after the epilogue warps): at N <= 128 a
+// chunk's four MMAs take half as long as at N = 256 and two producer warps fall
+// behind (C2k3: the issuer waited on a_full for a third of its time).
+template <int MH, bool PROF, int AX>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarps + 32 * AX, 1) k_conv_umma_pair(
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
     const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out,
@@ -434,7 +436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
   if (tid == 0) {
     for (int s = 0; s < kPStages; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
     for (int k = 0; k < kPMaxA; ++k) {
-      mbar_init(&a_full[k], 2 * kPAWarps * (g.a_unit ? g.KBu : 1));
+      mbar_init(&a_full[k], 2 * (2 + AX) * (g.a_unit ? g.KBu : 1));
       mbar_init(&a_empty[k], 1);
     }
     for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], 2 * kPEpiWarps); }
@@ -491,7 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1) k_conv
   } else if ((warp >= kPAWarp0 && warp < kPAWarp0 + 2) || warp >= kPEpiWarp0 + kPEpiWarps) {
     // ================= A producers: packed bits -> swizzled d-bytes, per K block
     const int a_w = warp < kPEpiWarp0 ? warp - kPAWarp0 : 2 + (warp - kPEpiWarp0 - kPEpiWarps);
-    const int pt = a_w * 32 + lane, n_pt = kPAWarps * 32;
+    const int pt = a_w * 32 + lane, n_pt = (2 + AX) * 32;
     const bool prof = (dbg & 128) && pt == 0;
     unsigned long long w_ae = 0;
     const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
@@ -1244,10 +1246,16 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   const int sms = sm_count();
   const int work = (next_bits != nullptr && g.n_nb > 1) ? g.tiles : g.units;  // tile-major: tiles per pair
   const int pairs = work < sms / 2 ? work : sms / 2;
-  static size_t attr_smem[4] = {0, 0, 0, 0};  // one-time (per size increase) shared-memory opt-in
-  auto kern = g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true> : k_conv_umma_pair<2, false>)
-                        : (g.debug ? k_conv_umma_pair<1, true> : k_conv_umma_pair<1, false>);
-  size_t& attr = attr_smem[(g.MH == 2 ? 1 : 0) + (g.debug ? 2 : 0)];
+  static size_t attr_smem[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // one-time (per size increase) shared-memory opt-in
+  // N <= 128: four more A-producer warps (C2k3 -9 %; at MH = 2 the 128-register cap
+  // of 512 threads costs a few spilled registers, outweighed by the faster A ring)
+  const bool wide_a = g.NP <= 128 && kPAExtra == 0;
+  auto kern = wide_a ? (g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true, 4> : k_conv_umma_pair<2, false, 4>)
+                                  : (g.debug ? k_conv_umma_pair<1, true, 4> : k_conv_umma_pair<1, false, 4>))
+              : g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true, kPAExtra> : k_conv_umma_pair<2, false, kPAExtra>)
+                          : (g.debug ? k_conv_umma_pair<1, true, kPAExtra> : k_conv_umma_pair<1, false, kPAExtra>);
+  const int threads = kPThreads + (wide_a ? 32 * 4 : 0);
+  size_t& attr = attr_smem[(g.MH == 2 ? 1 : 0) + (wide_a ? 2 : 0) + (g.debug ? 4 : 0)];
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
@@ -1259,7 +1267,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   }
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
   g.tile_major = next_bits != nullptr && g.n_nb > 1;
-  kern<<<2 * pairs, kPThreads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
+  kern<<<2 * pairs, threads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
                                           next_bits, next_A);
   if (part != nullptr) {
     const long total = (long)N * O * g.oh * g.ow;
