@@ -87,6 +87,21 @@ def test_pack_input_long_channel_vectors(C):
         assert np.array_equal(A[n].cpu().numpy().view(np.uint32), A_ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("shape", [(400, 3, 9, 7), (2, 2, 50, 3000)])
+def test_scale_map_bands_and_wide_maps(shape):
+    """K2's band blocks (many images: one band per image) and the tiled fallback for
+    maps too wide for a band in shared memory give the oracle's bits."""
+    from paper_2007_14178_b200 import ops
+    rng = np.random.default_rng(list(shape))
+    x = O.f32_exact(rng, shape)
+    _, A = ops.pack_input(torch.from_numpy(x).to(_dev()))
+    for (kh, kw), pad in (((3, 3), 1), ((5, 3), 2)):
+        K = ops.scale_map(A, kh, kw, pad).cpu().numpy()
+        for n in (0, shape[0] - 1):
+            _, K_ref = O.scale_map_f32(x[n], kh, kw, pad)
+            assert np.array_equal(K[n].view(np.uint32), K_ref.view(np.uint32))
+
+
 @pytest.mark.parametrize("k,pad", [((1, 1), 0), ((3, 3), 1), ((3, 3), 0), ((5, 5), 2), ((7, 7), 3),
                                    ((3, 5), 2), ((8, 8), 3), ((2, 2), 1)])
 def test_scale_map_bit_exact(k, pad):
