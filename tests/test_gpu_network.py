@@ -59,7 +59,8 @@ def test_network_kernel_selection():
     assert all(v in ("umma", "popc", "popc-fc", "umma-fc") for v in ks.values())
 
 
-@pytest.mark.parametrize("shape,pad,r", [((2, 3, 224, 224), 2, 4), ((3, 5, 10, 14), 1, 4), ((1, 2, 6, 6), 0, 2)])
+@pytest.mark.parametrize("shape,pad,r", [((2, 3, 224, 224), 2, 4), ((3, 5, 10, 14), 1, 4), ((1, 2, 6, 6), 0, 2),
+                                         ((2, 3, 12, 20), 2, 4), ((1, 3, 6, 10), 3, 4)])
 def test_pad_space_to_depth_matches_torch(shape, pad, r):
     from paper_2007_14178_b200 import ops
     x = torch.randn(shape, device="cuda")
