@@ -6,8 +6,10 @@
  * functions fill in place.  Every pointer is a DEVICE pointer (cudaMalloc /
  * torch CUDA storage) unless stated otherwise; `stream` is a cudaStream_t
  * (NULL = legacy default stream).  Calls only enqueue work: no allocation, no
- * synchronisation, no host<->device copies, no global mutable state beyond a
- * one-time per-kernel shared-memory opt-in.  Return value: 0 (XNC_OK) or an
+ * synchronisation, no host<->device copies.  The only library state is a cache,
+ * keyed by (device, kernel) and guarded by a mutex, of the dynamic shared-memory
+ * opt-in and each device's SM count: calls are thread-safe and may target any
+ * device (the current one at call time).  Return value: 0 (XNC_OK) or an
  * XNC_E* code below / a cudaError_t launch error (>= 1000 + cudaError_t).
  * Shape validation lives in the Python layer (which raises the reference's
  * exception types); the C layer re-checks cheaply and returns XNC_EINVAL.
@@ -125,6 +127,11 @@ int xnc_xnor_conv_umma_affine(const uint32_t* bits, const uint8_t* wq, const int
  * the pool); relu != 0: torch.relu before the pool, in the same pass.  pool_k <= 8. */
 int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu,
                  int nhwc, const float* bias, float* out, void* stream);
+/* y f32 [N][O][plane] in place: y[n][o][i] = y[n][o][i] * scale[o] + shift[o], one
+ * rounding per op (the fused tcgen05 epilogue's out_affine, for the popc / b1mma
+ * kernels, whose epilogues do not carry it). */
+int xnc_plane_affine(float* y, int N, int O, long plane, const float* scale, const float* shift,
+                     void* stream);
 /* F.pixel_unshuffle(F.pad(x, pad on all sides), r) in one pass: out f32
  * [N][C*r*r][(H+2pad)/r][(W+2pad)/r] (conv1 11x11/4 as a 3x3 conv, network.py).
  * nhwc != 0 (xnc_max_pool too): the map is stored channels-last, [N][H][W][C]. */
@@ -140,8 +147,11 @@ int xnc_pack_input_nhwc(const float* x, int N, int C, int H, int W, const float*
  * [N][H'][W'][ceil(O/32)] = sign words of y' (bit c = y'_c >= 0, tail bits 0) and
  * next_A f32 [N][H'][W'] = (sequential f32 sum over c of |y'_c|) * f32(1/O) (NULL
  * = not written), bit-identical to xnc_pack_input_affine run on the materialised
- * y'.  The 822 MB float map of a C3 layer is never written nor re-read.  Needs all
- * O filters in one 256-wide block: xnc_umma_emit_supported() (O <= 256). */
+ * y'.  The 822 MB float map of a C3 layer is never written nor re-read.  Any O the
+ * tcgen05 plan supports: with several filter blocks (O > 256) each CTA pair takes
+ * whole pixel tiles and runs their blocks back to back (tile-major), so a pixel's
+ * channels reach one thread in order; xnc_umma_emit_supported() says whether the
+ * shape's plan fits. */
 int xnc_umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 int xnc_xnor_conv_umma_emit(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
                             const float* K, const float* alpha, int N, int C, int H, int W,

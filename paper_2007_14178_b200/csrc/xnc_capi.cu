@@ -141,6 +141,11 @@ int xnc_max_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int
               : launch_max_pool(x, N, C, Hin, Win, pool_k, pool_s, relu, bias, out, as_stream(stream));
 }
 
+int xnc_plane_affine(float* y, int N, int O, long plane, const float* scale, const float* shift, void* stream) {
+  if (!y || !scale || !shift || N < 0 || O < 1 || plane < 0) return XNC_EINVAL;
+  return launch_plane_affine(y, N, O, plane, scale, shift, as_stream(stream));
+}
+
 int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, int r, int nhwc, float* out,
                            void* stream) {
   if (!x || !out || N < 1 || C < 1 || H < 1 || W < 1 || pad < 0 || r < 1 || (H + 2 * pad) % r ||

@@ -28,6 +28,16 @@ inline int launch_status() {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Per-device launch state (xnc_runtime.cu), thread-safe.  The dynamic shared-memory
+// opt-in is a per-device, per-function setting: a process-wide "done" flag would skip
+// it on a second GPU and its >48 KB launches would fail.
+// Raises func's opt-in on the current device to at least `bytes`; 0 or XNC_ECUDA_BASE+e.
+int smem_opt_in(const void* func, size_t bytes);
+template <class F>
+inline int smem_opt_in(F* func, size_t bytes) { return smem_opt_in(reinterpret_cast<const void*>(func), bytes); }
+// SM count of the current device (cached per device).
+int device_sm_count();
+
 }  // namespace xnc
 
 // Kernel launchers implemented in the per-kernel translation units.
@@ -64,6 +74,8 @@ int launch_pad_s2d(const float* x, int N, int C, int H, int W, int p, int r, int
                    cudaStream_t s);
 int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu,
                          const float* bias, float* out, cudaStream_t s);
+int launch_plane_affine(float* y, int N, int O, long plane, const float* scale, const float* shift,
+                        cudaStream_t s);
 int launch_pack_input_nhwc(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A, cudaStream_t s,
                            const float* in_scale, const float* in_shift);
 }  // namespace xnc

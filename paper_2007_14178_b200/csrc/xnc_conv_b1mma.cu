@@ -198,11 +198,7 @@ int launch_conv_b1mma(const uint32_t* bits, const uint32_t* wbits, const float* 
   if (smem > 200 * 1024 || threads > 512) return XNC_ENOTSUP;
   const int n_fb = cdiv(O, kB1TO), n_rt = cdiv(oh, TR);
   const long blocks = (long)n_fb * n_rt * N;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_conv_b1mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_done = true;
-  }
+  if (int rc = smem_opt_in(k_conv_b1mma, smem)) return rc;  // per device (xnc_runtime.cu)
   k_conv_b1mma<<<(unsigned)blocks, threads, smem, s>>>(bits, wbits, K, alpha, C, H, W, O, kh, kw, pad,
                                                        oh, ow, Cw, TR, SCs, n_fb, n_rt, Kw8, y, acc);
   return launch_status();

@@ -191,11 +191,7 @@ static int launch_kw(const uint32_t* bits, const uint32_t* wbits, const float* K
   const int threads = TR * TCg * FG;
   const int vec_ok = (ow % 4 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(acc) & 15) == 0);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_conv_popc<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_done = true;
-  }
+  if (int rc = smem_opt_in(k_conv_popc<KW>, smem)) return rc;  // per device (xnc_runtime.cu)
   k_conv_popc<KW><<<(unsigned)blocks, threads, smem, s>>>(
       bits, wbits, K, alpha, C, H, W, O, kh, pad, oh, ow, Cw, JC, TR, TCg, TO, SCs, n_fb, n_ct,
       n_rt, vec_ok, y, acc);

@@ -1126,15 +1126,7 @@ static bool pair_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad
   return false;
 }
 
-static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 2) sms = 148;
-  }
-  return sms;
-}
+static int sm_count() { return device_sm_count(); }
 
 // K splits for a shape: the largest divisor S of KBn with (tile, block) units * S
 // <= CTA pairs, when the unsplit shape leaves more than half of the pairs idle
@@ -1191,14 +1183,16 @@ bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) 
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  // a function-local static: initialised once, thread-safe (the driver entry point
+  // is process-wide, not per device)
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -1246,7 +1240,6 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   const int sms = sm_count();
   const int work = (next_bits != nullptr && g.n_nb > 1) ? g.tiles : g.units;  // tile-major: tiles per pair
   const int pairs = work < sms / 2 ? work : sms / 2;
-  static size_t attr_smem[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // one-time (per size increase) shared-memory opt-in
   // N <= 128: four more A-producer warps (C2k3 -9 %; at MH = 2 the 128-register cap
   // of 512 threads costs a few spilled registers, outweighed by the faster A ring)
   const bool wide_a = g.NP <= 128 && kPAExtra == 0;
@@ -1255,12 +1248,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
               : g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true, kPAExtra> : k_conv_umma_pair<2, false, kPAExtra>)
                           : (g.debug ? k_conv_umma_pair<1, true, kPAExtra> : k_conv_umma_pair<1, false, kPAExtra>);
   const int threads = kPThreads + (wide_a ? 32 * 4 : 0);
-  size_t& attr = attr_smem[(g.MH == 2 ? 1 : 0) + (wide_a ? 2 : 0) + (g.debug ? 4 : 0)];
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
-    attr = smem;
-  }
+  if (int rc = smem_opt_in(kern, smem)) return rc;  // per device (xnc_runtime.cu)
   int32_t* part = g.S > 1 && (long)N * O * g.oh * g.ow < 0x7fffffffL ? split_ws : nullptr;
   if (g.S > 1 && part == nullptr) {  // no buffer usable: run unsplit
     if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;

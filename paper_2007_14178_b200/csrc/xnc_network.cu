@@ -248,4 +248,31 @@ int launch_pad_s2d(const float* x, int N, int C, int H, int W, int p, int r, int
   return launch_status();
 }
 
+// The affine of the conv epilogue (y * scale[o] + shift[o], one rounding per op,
+// __fmul_rn then __fadd_rn) as a pass over a finished y [N][O][plane]: the popc /
+// b1mma kernels' form of the fused tcgen05 out_affine.  One block row per (n, o)
+// plane, so the filter index is a block constant.
+__global__ void k_plane_affine(float* __restrict__ y, long p0, int O, long plane, const float* __restrict__ scale,
+                               const float* __restrict__ shift) {
+  const long np = p0 + blockIdx.y;
+  const int o = (int)(np % O);
+  const float sc = __ldg(scale + o), sh = __ldg(shift + o);
+  float* row = y + np * plane;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < plane; i += (long)gridDim.x * blockDim.x)
+    row[i] = __fadd_rn(__fmul_rn(row[i], sc), sh);
+}
+
+int launch_plane_affine(float* y, int N, int O, long plane, const float* scale, const float* shift,
+                        cudaStream_t s) {
+  const long planes = (long)N * O;
+  if (planes == 0 || plane == 0) return XNC_OK;
+  const unsigned gx = (unsigned)std::min<long>(cdivl(plane, 256), 64);
+  // planes beyond the 65535 grid rows run as successive launches
+  for (long p0 = 0; p0 < planes; p0 += 65535) {
+    const unsigned gy = (unsigned)std::min<long>(planes - p0, 65535);
+    k_plane_affine<<<dim3(gx, gy), 256, 0, s>>>(y, p0, O, plane, scale, shift);
+  }
+  return launch_status();
+}
+
 }  // namespace xnc

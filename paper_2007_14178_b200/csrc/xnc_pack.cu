@@ -298,6 +298,24 @@ __global__ void __launch_bounds__(128) k_absmean_wide(const float* __restrict__ 
   if (lane == 0) A[q] = __fmul_rn(s, inv);
 }
 
+// The two-kernel form of K1 (sign words, then the sequential |.| means): no shared
+// word tile, so it serves any channel count; the preferred form for few pixels with
+// long channel loops.
+static int launch_pack_2d(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
+                          cudaStream_t s, const float* in_scale, const float* in_shift) {
+  const long npix = (long)N * H * W;
+  const int Cw = cdiv(C, 32);
+  const long words = npix * Cw;
+  k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, in_scale, in_shift);
+  if (A && H * W == 1 && C >= 1024)
+    k_absmean_wide<<<(unsigned)cdivl(npix, 4), 128, 0, s>>>(x, C, npix, (float)(1.0 / (double)C), A, in_scale,
+                                                            in_shift);
+  else if (A)
+    k_absmean<<<(unsigned)cdivl(npix, 128), 128, 0, s>>>(x, C, H * W, npix, (float)(1.0 / (double)C), A,
+                                                         in_scale, in_shift);
+  return launch_status();
+}
+
 int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A,
                       cudaStream_t s, const float* in_scale, const float* in_shift) {
   {
@@ -306,29 +324,15 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
     // few pixels with long channel loops (13x13 / 6x6 / 1x1 layers): the 2-D path
     if (vec_groups < 2L * 148 * 256 && C >= 256) {
       const int Cw = cdiv(C, 32);
-      const long words = npix * Cw;
       if (H * W >= 32 && C <= kSmallMaxC) {  // one pass: 32 pixels x C channels per block
         const size_t sm = (size_t)C * 32 * sizeof(float);
-        static size_t opted[2] = {0, 0};
-        const int ai = in_scale ? 1 : 0;
         auto kern = in_scale ? k_pack_small<true> : k_pack_small<false>;
-        if (sm > 48 * 1024 && sm > opted[ai]) {
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-          opted[ai] = sm;
-        }
+        if (int rc = smem_opt_in(kern, sm)) return rc;  // per device (xnc_runtime.cu)
         kern<<<(unsigned)cdivl(npix, 32), 128, sm, s>>>(x, C, H * W, Cw, npix, (float)(1.0 / (double)C), bits, A,
                                                         in_scale, in_shift);
         return launch_status();
       }
-      k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, in_scale,
-                                                              in_shift);
-      if (A && H * W == 1 && C >= 1024)
-        k_absmean_wide<<<(unsigned)cdivl(npix, 4), 128, 0, s>>>(x, C, npix, (float)(1.0 / (double)C), A, in_scale,
-                                                                in_shift);
-      else if (A)
-        k_absmean<<<(unsigned)cdivl(npix, 128), 128, 0, s>>>(x, C, H * W, npix, (float)(1.0 / (double)C), A,
-                                                             in_scale, in_shift);
-      return launch_status();
+      return launch_pack_2d(x, N, C, H, W, bits, A, s, in_scale, in_shift);
     }
   }
   const int HW = H * W;
@@ -342,17 +346,15 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   int threads = kPackThreads;
   while (threads > 128 && (size_t)Cw * (threads * vec + 4) * 4 > 100 * 1024) threads /= 2;
   const size_t smem = (size_t)Cw * (threads * vec + 4) * 4;
-  if (smem > 200 * 1024) return XNC_ENOTSUP;  // C > ~12k channels
+  // the word tile does not fit (C > ~3.1k channels at VEC = 4, ~12k at VEC = 1): the
+  // two-kernel form (words, then the |.| means) handles any C
+  if (smem > 200 * 1024) return launch_pack_2d(x, N, C, H, W, bits, A, s, in_scale, in_shift);
   const unsigned blocks = (unsigned)cdivl(total, threads);
-  static size_t opted[2][2][3] = {};  // one-time smem opt-in per instantiation
   const bool aff = in_scale != nullptr;
+  int opt_rc = XNC_OK;
   auto go = [&](auto kern, int t) {
-    size_t& o = opted[vec4 ? 1 : 0][aff ? 1 : 0][t == 512 ? 2 : t == 256 ? 1 : 0];
-    if (smem > 48 * 1024 && smem > o) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      o = smem;
-    }
-    kern<<<blocks, t, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, in_scale, in_shift);
+    opt_rc = smem_opt_in(kern, smem);  // per device (xnc_runtime.cu)
+    if (opt_rc == XNC_OK) kern<<<blocks, t, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, in_scale, in_shift);
   };
   auto pick = [&](auto aff_tag) {
     constexpr bool AF = decltype(aff_tag)::value;
@@ -368,6 +370,7 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   };
   if (aff) pick(std::true_type{});
   else pick(std::false_type{});
+  if (opt_rc) return opt_rc;
   return launch_status();
 }
 

@@ -25,14 +25,17 @@ def default_pad(kernel_h: int, kernel_w: int) -> int:
 class XnorConv2d:
     """Binary conv layer with packed weights resident on one device."""
 
-    def __init__(self, weight: torch.Tensor, pad: int | None = None, variant: str = "popc",
+    def __init__(self, weight: torch.Tensor, pad: int | None = None, variant: str = "auto",
                  in_affine=None, out_affine=None, in_pool=None):
         """in_affine = (scale, shift) f32 [C]: the layer binarizes x*scale + shift
         (a folded batch norm in front of the sign, computed inside K1); out_affine =
         (scale, shift) f32 [O]: y*scale + shift is written instead of y (the next
         binary layer's batch norm, fused into the conv epilogue); in_pool = (kernel,
         stride): the input is max-pooled first (no padding, xnc_max_pool) --
-        forward() then takes the pre-pool tensor."""
+        forward() then takes the pre-pool tensor.
+
+        variant: 'auto' (default) runs the tcgen05 kernel whenever its plan fits
+        the shape (kernel_for), else popc; 'umma' / 'popc' / 'b1mma' force one."""
         if weight.dim() != 4:
             raise ValueError(f"weight must be [O, C, kh, kw], got {tuple(weight.shape)}")
         O, C, kh, kw = weight.shape
@@ -95,7 +98,7 @@ class XnorConv2d:
         be an ops.PackedInput (a previous layer's emitted signs): K1 is skipped.
         emit_signs=True returns the NEXT binary layer's input as an
         ops.PackedInput (sign words + A of y [* out_affine]) instead of y, written
-        by the conv epilogue itself (tcgen05 kernel, O <= 256): the float map never
+        by the conv epilogue itself (tcgen05 kernel): the float map never
         reaches HBM."""
         if isinstance(x, ops.PackedInput):
             return self._forward_packed(x, out, want_acc, emit_signs)
@@ -210,8 +213,14 @@ class XnorConv2d:
 
     # ------------------------------------------------------------------ host path
     def forward_host(self, x_host: torch.Tensor, out: torch.Tensor | None = None,
-                     chunk: int | None = None, device: torch.device | None = None) -> torch.Tensor:
+                     chunk: int | None = None, device: torch.device | None = None,
+                     non_blocking: bool = False) -> torch.Tensor:
         """Host x in, host y out, with the PCIe copies overlapped with compute.
+
+        Returns once `out` holds the result (the last device->host copy is waited
+        for on the host).  non_blocking=True returns as soon as the work is queued:
+        the caller must then synchronise the current stream (which waits for the
+        copies) before reading `out`.
 
         The batch is cut into chunks; chunk i+1 is copied host->device on one
         stream while chunk i runs K1 -> K2 -> K3+K4 on a second and chunk i-1
@@ -254,6 +263,9 @@ class XnorConv2d:
                 out[a:b].copy_(yb, non_blocking=True)
                 st["y_free"][slot].record(s_out)
         cur.wait_stream(s_out)
+        if not non_blocking:
+            st["done"].record(s_out)
+            st["done"].synchronize()  # the D2H copies have landed in `out`
         return out
 
     def _host_state(self, dev, x_shape, chunk):
@@ -267,6 +279,7 @@ class XnorConv2d:
                   "x": xs,
                   "y": [torch.empty((chunk, O, oh, ow), dtype=torch.float32, device=dev) for _ in range(2)],
                   "ws": self.workspace(xs[0]),
+                  "done": torch.cuda.Event(),
                   **{k: [torch.cuda.Event() for _ in range(2)]
                      for k in ("x_ready", "x_free", "y_ready", "y_free")}}
             self._ws[key] = st
@@ -274,6 +287,6 @@ class XnorConv2d:
 
 
 def xnor_conv2d_layer(x: torch.Tensor, weight: torch.Tensor, pad: int | None = None,
-                      want_acc: bool = False, variant: str = "popc"):
+                      want_acc: bool = False, variant: str = "auto"):
     """Functional batched layer (packs the weights on every call)."""
     return XnorConv2d(weight, pad, variant).forward(x, want_acc=want_acc)

@@ -253,7 +253,8 @@ def xnor_conv_emit(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor, pad
     if words(C) != Cw:
         raise ValueError(f"bits hold {Cw} words per pixel; filters have {C} channels")
     if not umma_emit_supported(N, C, H, W, filt.O, filt.kh, filt.kw, pad):
-        raise ValueError(f"sign emission needs all {filt.O} filters in one 256-wide block (O <= 256)")
+        raise ValueError(f"no tcgen05 sign-emitting plan for N={N} C={C} {H}x{W} O={filt.O} "
+                         f"k={filt.kh}x{filt.kw} pad={pad}")
     oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
     dev = bits.device
     nbits = torch.empty((N, oh, ow, words(filt.O)), dtype=torch.int32, device=dev)
@@ -266,37 +267,98 @@ def xnor_conv_emit(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor, pad
     return PackedInput(nbits, nA, filt.O)
 
 
+def _check_out(t: torch.Tensor | None, name: str, dtype: torch.dtype, shape, device) -> None:
+    """A caller-supplied output must be exactly what the kernel writes: a kernel
+    told N*O*H'*W' elements of the wrong buffer would write out of bounds."""
+    if t is None:
+        return
+    if not t.is_cuda or t.device != device:
+        raise ValueError(f"{name} must be a CUDA tensor on {device}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def resolve_variant(variant: str, filt: PackedFilters, N: int, C: int, H: int, W: int, pad: int) -> str:
+    """'auto' -> 'umma' when the filters carry the tcgen05 layout and its plan fits
+    the shape, else 'popc'; explicit variants pass through."""
+    if variant == "auto":
+        if filt.wq is not None and umma_supported(N, C, H, W, filt.O, filt.kh, filt.kw, pad):
+            return "umma"
+        return "popc"
+    if variant not in ("popc", "b1mma", "umma"):
+        raise ValueError(f"unknown variant {variant!r}")
+    return variant
+
+
+# Zeroed s32 partial-sum buffers of the K split, one per (device, stream): the split
+# kernels leave them zeroed, so they are allocated (and zeroed) once, not per call.
+_SPLIT_WS: dict[tuple, torch.Tensor] = {}
+
+
+def _split_ws(nbytes: int, dev: torch.device) -> torch.Tensor:
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _SPLIT_WS.get(key)
+    if buf is None or buf.numel() * 4 < nbytes:
+        buf = torch.zeros(nbytes // 4, dtype=torch.int32, device=dev)
+        _SPLIT_WS[key] = buf
+    return buf
+
+
+def plane_affine_(y: torch.Tensor, out_affine) -> torch.Tensor:
+    """y[n, o] = y[n, o] * scale[o] + shift[o] in place on the device, with the fused
+    epilogue's two roundings (xnc_plane_affine)."""
+    _need_cuda(y, "y", torch.float32)
+    N, O = y.shape[:2]
+    plane = y[0, 0].numel() if y.numel() else 0
+    osc, osh = _affine(out_affine, O, y.device, "out_affine")
+    check(lib().xnc_plane_affine(y.data_ptr(), N, O, plane, osc.data_ptr(), osh.data_ptr(), _stream(y.device)),
+          "xnc_plane_affine")
+    return y
+
+
 def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, pad: int,
               C: int | None = None, want_y: bool = True, want_acc: bool = False,
-              variant: str = "popc", y: torch.Tensor | None = None,
+              variant: str = "auto", y: torch.Tensor | None = None,
               acc: torch.Tensor | None = None, W: int | None = None, out_affine=None):
     """K3+K4: (y f32 [N,O,H',W'] or None, acc i32 [N,O,H',W'] or None).
 
-    Every variant reads the packed bits `bits` (i32 [N,H,W,Cw], from pack_input)."""
+    Every variant reads the packed bits `bits` (i32 [N,H,W,Cw], from pack_input).
+    variant 'auto' (default) runs the tcgen05 kernel when the filters carry its
+    layout (attach_umma_weights) and its plan fits the shape, else popc."""
     C = filt.C if C is None else C
     _need_cuda(bits, "bits", torch.int32)
     N, H, W, Cw = bits.shape
     if words(C) != Cw or filt.C != C:
         raise ValueError(f"bits hold {Cw} words per pixel; filters have {filt.C} channels")
     oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    if oh < 1 or ow < 1:
+        raise ValueError("kernel larger than the padded input")
     dev = bits.device
-    if want_y and y is None:
-        y = torch.empty((N, filt.O, oh, ow), dtype=torch.float32, device=dev)
-    if want_acc and acc is None:
-        acc = torch.empty((N, filt.O, oh, ow), dtype=torch.int32, device=dev)
+    variant = resolve_variant(variant, filt, N, C, H, W, pad)
+    oshape = (N, filt.O, oh, ow)
     if not want_y:
         y = None
+    _check_out(y, "y", torch.float32, oshape, dev)
+    _check_out(acc, "acc", torch.int32, oshape, dev)
+    if want_y and y is None:
+        y = torch.empty(oshape, dtype=torch.float32, device=dev)
+    if want_acc and acc is None:
+        acc = torch.empty(oshape, dtype=torch.int32, device=dev)
     if want_y:
         if K is None:
             raise ValueError("K map required for the float output")
-        _need_cuda(K, "K", torch.float32)
+        _check_out(K, "K", torch.float32, (N, oh, ow), dev)
     if variant == "umma":
         if filt.wq is None:
             raise ValueError("umma variant needs attach_umma_weights() first")
         osc, osh = _affine(out_affine, filt.O, dev, "out_affine")
         # a K split (fully connected shapes) needs a zeroed s32 partial-sum buffer
         ws_bytes = lib().xnc_umma_split_ws_bytes(N, C, H, W, filt.O, filt.kh, filt.kw, pad)
-        split_ws = torch.zeros(ws_bytes // 4, dtype=torch.int32, device=dev) if ws_bytes else None
+        split_ws = _split_ws(ws_bytes, dev) if ws_bytes else None
         check(lib().xnc_xnor_conv_umma_ws(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), _ptr(K),
                                           filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
                                           _ptr(osc), _ptr(osh), _ptr(split_ws), _ptr(y), _ptr(acc),
@@ -308,9 +370,23 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
                                           filt.kw, pad, _ptr(y), _ptr(acc), _stream(dev)),
               "xnc_xnor_conv")
         if out_affine is not None and y is not None:  # same two roundings as the fused epilogue
-            osc, osh = _affine(out_affine, filt.O, dev, "out_affine")
-            y.mul_(osc.view(1, -1, 1, 1)).add_(osh.view(1, -1, 1, 1))
+            plane_affine_(y, out_affine)
     return y, acc
+
+
+def _check_layer_bufs(x, filt, pad, workspace, y, acc) -> None:
+    N, C, H, W = x.shape
+    oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    if oh < 1 or ow < 1:
+        raise ValueError("kernel larger than the padded input")
+    _check_out(y, "y", torch.float32, (N, filt.O, oh, ow), x.device)
+    _check_out(acc, "acc", torch.int32, (N, filt.O, oh, ow), x.device)
+    need = layer_workspace_bytes(N, C, H, W, filt.kh, filt.kw, pad)
+    if not workspace.is_cuda or workspace.device != x.device or not workspace.is_contiguous():
+        raise ValueError(f"workspace must be a contiguous CUDA tensor on {x.device}")
+    if workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"workspace holds {workspace.numel() * workspace.element_size()} bytes; "
+                         f"this shape needs {need}")
 
 
 def layer_workspace_bytes(N: int, C: int, H: int, W: int, kh: int, kw: int, pad: int) -> int:
@@ -325,6 +401,7 @@ def layer_forward(x: torch.Tensor, filt: PackedFilters, pad: int, workspace: tor
     if C != filt.C:
         raise ValueError(f"{C} input channels vs {filt.C} filter channels")
     oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    _check_layer_bufs(x, filt, pad, workspace, y, acc)
     if y is None:
         y = torch.empty((N, filt.O, oh, ow), dtype=torch.float32, device=x.device)
     check(lib().xnc_layer_forward(x.data_ptr(), filt.wbits.data_ptr(), filt.alpha.data_ptr(), N, C,
@@ -343,6 +420,7 @@ def layer_forward_umma(x: torch.Tensor, filt: PackedFilters, pad: int, workspace
     if filt.wq is None:
         raise ValueError("layer_forward_umma needs attach_umma_weights() first")
     oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    _check_layer_bufs(x, filt, pad, workspace, y, acc)
     if y is None:
         y = torch.empty((N, filt.O, oh, ow), dtype=torch.float32, device=x.device)
     check(lib().xnc_layer_forward_umma(x.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(),

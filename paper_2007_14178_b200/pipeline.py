@@ -49,6 +49,7 @@ class ConvWorkspace:
         self.ints = np.zeros((self.out_h, self.out_w), dtype=np.int32)
         self.filter: BinaryFilter | None = None
         self._packed: ops.PackedFilters | None = None
+        self.variant = "auto"  # conv kernel choice (ops.resolve_variant); tests pin 'popc' / 'umma' 
 
     def set_weights(self, weights: Tensor3) -> None:
         """Binarize one filter (untimed, pipeline.py:77-83): the reference-layout
@@ -56,7 +57,11 @@ class ConvWorkspace:
         if weights.channels != self.channels:
             raise ValueError(f"{weights.channels} weight channels for a {self.channels}-channel workspace")
         self.filter = build_filter(weights, self.geometry)
-        self._packed = ops.pack_weights_f64(_dev.to_dev(weights.data[np.newaxis]))
+        w64 = _dev.to_dev(weights.data[np.newaxis])
+        self._packed = ops.pack_weights_f64(w64)
+        # the tcgen05 layout too: run() takes that kernel whenever its plan fits
+        # (ops.xnor_conv's 'auto'), else the popc kernel
+        ops.attach_umma_weights(self._packed, w64)
 
     def load_input(self, t: Tensor3) -> None:
         """Copy the image to the device as float32 (the reference's cast, pipeline.py:85-93)."""
@@ -74,7 +79,14 @@ class ConvWorkspace:
             ops.scale_map_into(self._A, k.kernel_h, k.kernel_w, self.pad, self._K)
         ops.xnor_conv(self._bits, self._packed, self._K if want_y else None, self.pad,
                       want_y=want_y, want_acc=want_acc, y=self._y if want_y else None,
-                      acc=self._acc if want_acc else None)
+                      acc=self._acc if want_acc else None, variant=self.variant)
+
+    @property
+    def kernel(self) -> str:
+        """The conv kernel run() launches for this shape ('umma' or 'popc')."""
+        k = self.geometry
+        return ops.resolve_variant(self.variant, self._packed, 1, self.channels, self.height, self.width,
+                                   self.pad) if self._packed is not None else self.variant
 
     def run(self, threads: int = 1, two_stream: bool = False) -> np.ndarray:
         """One full convolution; returns the reused float32 host output array."""

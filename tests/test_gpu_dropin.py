@@ -147,15 +147,22 @@ def test_scale_kats(xc):
 
 
 # ---------------------------------------------------------------- pipeline (ConvWorkspace / xnor_conv)
+@pytest.mark.parametrize("variant", ["auto", "popc", "umma"])
 @pytest.mark.parametrize("case", [c for c in golden_io.layer_cases() if c["N"] * c["O"] <= 16],
                          ids=lambda c: c["name"])
-def test_workspace_matches_reference_golden(xc, case):
+def test_workspace_matches_reference_golden(xc, case, variant):
+    from paper_2007_14178_b200 import ops
     N, C, H, W, Oc = case["N"], case["C"], case["H"], case["W"], case["O"]
+    if variant == "umma" and not ops.umma_supported(1, C, H, W, 1, case["kh"], case["kw"], case["pad"]):
+        pytest.skip("shape outside the tcgen05 kernel's smem plan")
     ws = xc.ConvWorkspace(C, H, W, case["kh"], case["kw"], case["pad"], case["word_bits"])
+    ws.variant = variant
     for n in range(N):
         ws.load_input(xc.Tensor3(case["x"][n].astype(np.float64)))
         for o in range(Oc):
             ws.set_weights(xc.Tensor3(case["w"][o].astype(np.float64)))
+            if variant != "popc":
+                assert ws.kernel == "umma" or variant == "auto"
             out = ws.run(threads=4)
             assert np.array_equal(out.view(np.uint32), case["out"][n, o].view(np.uint32))
             assert np.array_equal(ws.int_plane().values, case["ints"][n, o])

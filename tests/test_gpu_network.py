@@ -11,15 +11,18 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def test_network_binary_layers_match_oracle():
+@pytest.mark.parametrize("batch", [3, 256])
+def test_network_binary_layers_match_oracle(batch):
+    """batch 256 is BASELINE config 4 (C4): the tile counts, K splits and tails of the
+    benched forward, sampled at the first, middle and last image."""
     from paper_2007_14178_b200.network import BINARY_LAYERS, XnorNetAlexNet
     torch.manual_seed(0)
     net = XnorNetAlexNet("cuda", seed=3)
-    x = torch.rand((3, 3, 224, 224), device="cuda") * 2 - 1
+    x = torch.rand((batch, 3, 224, 224), device="cuda") * 2 - 1
     logits, feats = net.forward(x, return_features=True)
     logits2 = net.forward(x)
     torch.cuda.synchronize()
-    assert logits.shape == (3, 1000) and torch.isfinite(logits).all()
+    assert logits.shape == (batch, 1000) and torch.isfinite(logits).all()
     assert torch.equal(logits, logits2)
     # layer inputs: conv1 -> relu -> pool for conv2; pooled / raw previous outputs after
     with torch.no_grad():
@@ -33,9 +36,10 @@ def test_network_binary_layers_match_oracle():
         h = feats[name]
         if name in ("conv2", "conv5"):
             h = F.max_pool2d(h, 3, 2)
+    n_idx = [0, 1] if batch <= 3 else [0, batch // 2, batch - 1]
     for name, cin, cout, k, pad in BINARY_LAYERS:
         layer = net.binary[name]
-        xin = inputs[name][:2].contiguous()
+        xin = inputs[name][n_idx].contiguous()
         if layer.in_affine is not None:  # the folded BN K1 applies: x*scale + shift, two roundings
             sc, sh = layer.in_affine
             xin = xin * sc.view(1, -1, 1, 1) + sh.view(1, -1, 1, 1)
@@ -47,7 +51,7 @@ def test_network_binary_layers_match_oracle():
             sc, sh = (t[o_idx].cpu().numpy() for t in layer.out_affine)
             want = (want * sc.reshape(1, -1, 1, 1)).astype(np.float32)
             want = (want + sh.reshape(1, -1, 1, 1)).astype(np.float32)
-        got = feats[name][:2][:, o_idx].cpu().numpy()
+        got = feats[name][n_idx][:, o_idx].cpu().numpy()
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), name
 
 
@@ -118,11 +122,12 @@ def test_network_cuda_graph_matches_eager():
         x.copy_(torch.rand_like(x) * 2 - 1)
 
 
-def test_network_emitted_signs_match_float_chain():
+@pytest.mark.parametrize("batch", [3, 256])
+def test_network_emitted_signs_match_float_chain(batch):
     """conv3 -> conv4 -> conv5 through the sign-emitting epilogue (the default forward)
     give exactly the logits of the float-feature-map chain."""
     from paper_2007_14178_b200.network import XnorNetAlexNet
     a = XnorNetAlexNet("cuda", seed=5)
     b = XnorNetAlexNet("cuda", seed=5, emit_signs=False)
-    x = torch.rand((3, 3, 224, 224), device="cuda") * 2 - 1
+    x = torch.rand((batch, 3, 224, 224), device="cuda") * 2 - 1
     assert torch.equal(a.forward(x), b.forward(x))

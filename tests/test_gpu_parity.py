@@ -30,18 +30,78 @@ def _layer(x, w, pad, variant="popc"):
     return y.cpu().numpy(), acc.cpu().numpy(), layer
 
 
+def _skip_unless_umma(variant, shape4, w_shape, pad):
+    """variant 'umma' forced on a shape outside the tcgen05 plan: skip (auto would
+    pick popc there)."""
+    from paper_2007_14178_b200 import ops
+    N, C, H, W = shape4
+    Oc, _, kh, kw = w_shape
+    if variant == "umma" and not ops.umma_supported(N, C, H, W, Oc, kh, kw, pad):
+        pytest.skip("shape outside the tcgen05 kernel's smem plan")
+
+
+VARIANTS = ["popc", "b1mma", "umma", "auto"]
+
+
 def _assert_float_parity(got, want):
     denom = max(float(np.abs(want).max()), 1e-30)
     assert float(np.abs(got.astype(np.float64) - want).max()) / denom <= REL_TOL
     assert np.array_equal(got.view(np.uint32), want.astype(np.float32).view(np.uint32))
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("case", golden_io.layer_cases(), ids=lambda c: c["name"])
-def test_layer_matches_reference_golden(case):
-    y, acc, layer = _layer(case["x"], case["w"], case["pad"])
+def test_layer_matches_reference_golden(case, variant):
+    """The reference-generated fixtures (its fused kernel at threads=1, pipeline.py:
+    124-151) through every conv kernel: popc, b1 mma.sync, the tcgen05 pair kernel
+    (the benched one) and 'auto' (the default)."""
+    _skip_unless_umma(variant, case["x"].shape, case["w"].shape, case["pad"])
+    y, acc, layer = _layer(case["x"], case["w"], case["pad"], variant=variant)
+    if variant == "auto":
+        assert layer.kernel_for(case["x"].shape) in ("umma", "popc")
     assert np.array_equal(acc, case["ints"])
     _assert_float_parity(y, case["out"])
     assert np.array_equal(layer.alpha64.cpu().numpy(), case["alpha"])
+
+
+def test_golden_cases_reach_the_tcgen05_kernel():
+    """'auto' resolves to the tcgen05 kernel on (nearly) every golden case, so the
+    golden parametrisation above pins the benched kernel directly."""
+    from paper_2007_14178_b200 import ops
+    cases = golden_io.layer_cases()
+    umma = [c["name"] for c in cases
+            if ops.umma_supported(*c["x"].shape, c["w"].shape[0], c["w"].shape[2], c["w"].shape[3], c["pad"])]
+    assert len(umma) >= len(cases) - 1, sorted(set(c["name"] for c in cases) - set(umma))
+    for must in ("c1_slice", "zeros_negzeros", "all_negative", "sign_dominated", "c257_tail", "k3x1_w32"):
+        assert must in umma
+
+
+def test_c1_full_size_all_filters_auto():
+    """BASELINE config 1 at full size (1 x 64 x 32 x 32, all 64 filters, k = 3,
+    pad 1) through the default 'auto' path, which must be the tcgen05 kernel, against
+    the oracle: ints and floats bit-exact."""
+    from paper_2007_14178_b200 import XnorConv2d
+    rng = np.random.default_rng((0, 1))  # bench.py's (seed, config_id) pattern
+    x = O.f32_exact(rng, (1, 64, 32, 32))
+    w = O.f32_exact(rng, (64, 64, 3, 3))
+    layer = XnorConv2d(torch.from_numpy(w).to(_dev()), pad=1)
+    assert layer.kernel_for(x.shape) == "umma"
+    y, acc = layer.forward(torch.from_numpy(x).to(_dev()), want_acc=True)
+    y_fused = layer.forward(torch.from_numpy(x).to(_dev()))  # one-call K1 -> K2 -> K3 path
+    torch.cuda.synchronize()
+    want, ints = O.conv_layer(x, w, 1, want_ints=True)
+    assert np.array_equal(acc.cpu().numpy(), ints)
+    _assert_float_parity(y.cpu().numpy(), want)
+    assert torch.equal(y, y_fused)
+
+
+def test_default_public_path_is_tcgen05_at_c3():
+    """XnorConv2d(w) with no variant runs the tcgen05 kernel at C3 (the benched
+    path is the default path)."""
+    from paper_2007_14178_b200 import XnorConv2d
+    w = torch.rand((256, 256, 3, 3), device=_dev()) * 2 - 1
+    assert XnorConv2d(w).kernel_for((256, 256, 56, 56)) == "umma"
+    assert XnorConv2d(w, pad=1).variant == "auto"
 
 
 def _unpack_bits(bits, C):
@@ -133,13 +193,14 @@ RANDOM_CASES = [
 ]
 
 
+@pytest.mark.parametrize("variant", ["popc", "auto"])
 @pytest.mark.parametrize("shape", RANDOM_CASES, ids=lambda s: "x".join(map(str, s)))
-def test_layer_vs_oracle_random(shape):
+def test_layer_vs_oracle_random(shape, variant):
     N, C, H, W, Oc, kh, kw, pad = shape
     rng = np.random.default_rng(list(shape))
     x = O.f32_exact(rng, (N, C, H, W))
     w = O.f32_exact(rng, (Oc, C, kh, kw))
-    y, acc, _ = _layer(x, w, pad)
+    y, acc, _ = _layer(x, w, pad, variant=variant)
     want, ints = O.conv_layer(x, w, pad, want_ints=True)
     assert np.array_equal(acc, ints)
     _assert_float_parity(y, want)
@@ -216,20 +277,23 @@ def test_fc_mode_matches_oracle(N, C, S, O_, k):
     _assert_float_parity(y.cpu().numpy(), want)
 
 
-def test_edge_all_negative_padding_plus_one():
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_edge_all_negative_padding_plus_one(variant):
     x = -np.ones((1, 4, 4, 4), np.float32)
     w = np.ones((1, 4, 3, 3), np.float32)
-    _, acc, _ = _layer(x, w, 1)
+    _skip_unless_umma(variant, x.shape, w.shape, 1)
+    _, acc, _ = _layer(x, w, 1, variant=variant)
     assert acc[0, 0, 0, 0] == 4 * (5 - 4) and acc[0, 0, 1, 1] == -36
 
 
-def test_repeat_runs_bit_identical():
+@pytest.mark.parametrize("variant", ["popc", "umma"])
+def test_repeat_runs_bit_identical(variant):
     rng = np.random.default_rng(7)
     x = O.f32_exact(rng, (2, 64, 20, 20))
     w = O.f32_exact(rng, (32, 64, 5, 5))
-    y0, a0, _ = _layer(x, w, 2)
+    y0, a0, _ = _layer(x, w, 2, variant=variant)
     for _ in range(5):
-        y1, a1, _ = _layer(x, w, 2)
+        y1, a1, _ = _layer(x, w, 2, variant=variant)
         assert np.array_equal(a0, a1) and np.array_equal(y0.view(np.uint32), y1.view(np.uint32))
 
 
@@ -275,12 +339,14 @@ def test_host_pipelined_forward_matches_device(N, chunk):
     w = torch.rand((24, 40, 3, 3), generator=g) * 2 - 1
     layer = XnorConv2d(w.to(_dev()), pad=1)
     y_dev = layer.forward(x.to(_dev())).cpu()
+    # forward_host returns only once the D2H copies have landed: no synchronize here
     y_host = layer.forward_host(x, chunk=chunk)
-    torch.cuda.synchronize()
     assert not y_host.is_cuda and torch.equal(y_host, y_dev)
     y2 = layer.forward(x.pin_memory())
-    torch.cuda.synchronize()
     assert torch.equal(y2, y_dev)
+    y3 = layer.forward_host(x, chunk=chunk, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    assert torch.equal(y3, y_dev)
 
 
 @pytest.mark.parametrize("C", [1, 31, 64, 128, 200, 256])
@@ -472,3 +538,62 @@ def test_random_shapes_umma_matches_popc(shape):
         got = ops.xnor_conv_emit(bits, filt, K, pad)
         wb, wa = ops.pack_input(yu.contiguous())
         assert torch.equal(got.bits, wb) and torch.equal(got.A.view(torch.int32), wa.view(torch.int32))
+
+
+def _conv_on(device, seed):
+    from paper_2007_14178_b200 import XnorConv2d
+    rng = np.random.default_rng(seed)
+    x = O.f32_exact(rng, (2, 256, 20, 20))   # tcgen05 plan needs the > 48 KB smem opt-in
+    w = O.f32_exact(rng, (256, 256, 3, 3))
+    with torch.cuda.device(device):
+        layer = XnorConv2d(torch.from_numpy(w).to(device), pad=1)
+        assert layer.kernel_for(x.shape) == "umma"
+        y, acc = layer.forward(torch.from_numpy(x).to(device), want_acc=True)
+        torch.cuda.synchronize(device)
+    return x, w, y.cpu().numpy(), acc.cpu().numpy()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs in one process")
+def test_two_devices_in_one_process():
+    """The smem opt-in and SM count are cached per device (xnc_runtime.cu): a second
+    GPU in the same process gets its own opt-in, so its > 48 KB launches succeed."""
+    for dev, seed in ((torch.device("cuda:0"), 1), (torch.device("cuda:1"), 2)):
+        x, w, y, acc = _conv_on(dev, seed)
+        want, ints = O.conv_layer(x[:1], w[:4], 1, want_ints=True)
+        assert np.array_equal(acc[:1, :4], ints)
+        _assert_float_parity(y[:1, :4], want)
+
+
+def test_host_threads_share_the_library():
+    """Several host threads launching (and opting in) concurrently: the per-device
+    caches are mutex-guarded, every thread's result is exact."""
+    import threading
+    from paper_2007_14178_b200 import XnorConv2d
+    results, errors = {}, []
+
+    def run(i):
+        try:
+            torch.cuda.set_device(0)
+            rng = np.random.default_rng(100 + i)
+            shape = [(2, 128, 18, 18), (1, 256, 14, 14), (3, 64, 30, 30), (2, 96, 9, 33)][i]
+            x = O.f32_exact(rng, shape)
+            w = O.f32_exact(rng, (48 + 16 * i, shape[1], 3, 3))
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                layer = XnorConv2d(torch.from_numpy(w).cuda(), pad=1)
+                y, acc = layer.forward(torch.from_numpy(x).cuda(), want_acc=True)
+            s.synchronize()
+            results[i] = (x, w, acc.cpu().numpy(), y.cpu().numpy())
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for i, (x, w, acc, y) in results.items():
+        want, ints = O.conv_layer(x, w, 1, want_ints=True)
+        assert np.array_equal(acc, ints)
+        _assert_float_parity(y, want)
