@@ -51,6 +51,7 @@ CONFIG_TEXT = {
     "C3": "ResNet-stage binary conv 3x3, C=256, 56x56, batch 256 (BASELINE config 3)",
 }
 METRIC = "XNOR-conv Gbinop/s and images/sec at 1/2/4/8 B200 vs host-CPU reference"
+NCCL_LOG_DIR = os.path.join(ROOT, "gpurun_out")
 POPC_LANES_PER_CLK_SM = 15.95  # measured, profiles/int_peaks_r1.jsonl
 UMMA_I8_MAC_PER_CLK_SM = 7874.4  # measured tcgen05 kind::i8 M128 N256 K32, profiles/umma_probe_r1.jsonl
 
@@ -134,6 +135,47 @@ def dist_env():
     return ws, rank, local
 
 
+def init_dist(dev=None):
+    """One process group per bench process (NCCL on the GPU box, gloo for --dry-run),
+    created on first use and kept for every leg of the run."""
+    import torch.distributed as dist
+    ws, _, _ = dist_env()
+    if ws > 1 and not dist.is_initialized():
+        if dev is None:
+            dist.init_process_group("gloo")
+        else:
+            # log NCCL's communicator init (rank count, transports) to a per-process file,
+            # never stdout (rank 0's stdout carries the one JSON line); device_id makes the
+            # init eager, so the log exists before the first timed step
+            os.makedirs(NCCL_LOG_DIR, exist_ok=True)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(NCCL_LOG_DIR, "nccl_init.%h.%p.log"))
+            dist.init_process_group("nccl", device_id=dev)
+    return ws
+
+
+def comm_info():
+    """What the data plane saw: backend and communicator size (the NCCL init lines
+    themselves go to stderr when bench.py spawned the ranks: NCCL_DEBUG=INFO,
+    NCCL_DEBUG_SUBSYS=INIT)."""
+    import re
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return {"backend": None, "nranks": 1, "collectives_on_hot_path": 0}
+    info = {"backend": dist.get_backend(), "nranks": dist.get_world_size(), "collectives_on_hot_path": 0}
+    log = os.environ.get("NCCL_DEBUG_FILE", "").replace("%h", platform.node()).replace("%p", str(os.getpid()))
+    if info["backend"] == "nccl" and log and os.path.exists(log):
+        # NCCL's own record of the communicator: "... comm 0x.. rank 0 nRanks 8 nNodes 1 ..."
+        with open(log) as fh:
+            txt = fh.read()
+        m = re.search(r"nRanks (\d+)", txt)
+        info["nccl_comm_nranks"] = int(m.group(1)) if m else None
+        lines = [ln.strip() for ln in txt.splitlines() if "nRanks" in ln or "NVLS" in ln]
+        info["nccl_init_lines"] = [ln[-160:] for ln in lines[:4]]
+    return info
+
+
 def max_over_ranks(value: float, ws: int, device) -> float:
     if ws == 1:
         return value
@@ -189,6 +231,15 @@ class RefRunner:
         self.ws = [self.R.workspace(self.x[i], self.pad, k, k) for i in range(n_img)]
         self.threads = os.cpu_count() or 1
 
+    def pair_rates(self, budget_s: float, threads=None, reps: int = 5):
+        """reps samples of pair_rate over budget_s in total: [s_per_pair], pairs."""
+        out, total = [], 0
+        for _ in range(reps):
+            sp, n = self.pair_rate(budget_s / reps, threads)
+            out.append(sp)
+            total += n
+        return out, total
+
     def pair_rate(self, budget_s: float, threads=None):
         """Time (image, filter) pairs for ~budget_s seconds; returns (s_per_pair, pairs)."""
         threads = threads or self.threads
@@ -205,6 +256,78 @@ class RefRunner:
 
 
 # ------------------------------------------------------------------ GPU arm
+def numa_local_cpus(dev) -> set[int] | None:
+    """The host CPUs on the GPU's NUMA node (sysfs local_cpulist of its PCI device)."""
+    import torch
+    try:
+        p = torch.cuda.get_device_properties(dev)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as fh:
+            spec = fh.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        return cpus & os.sched_getaffinity(0) or None
+    except Exception:
+        return None
+
+
+class numa_local:
+    """Run the block (pinned host allocations, first touch) on the GPU-local NUMA
+    node's CPUs, then restore the affinity (the CPU baseline uses every core)."""
+
+    def __init__(self, dev):
+        self.cpus = numa_local_cpus(dev)
+        self.saved = None
+
+    def __enter__(self):
+        if self.cpus:
+            self.saved = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, self.cpus)
+        return self
+
+    def __exit__(self, *a):
+        if self.saved:
+            os.sched_setaffinity(0, self.saved)
+
+
+def pcie_peak(dev, nbytes: int = 256 << 20, reps: int = 5) -> dict:
+    """Host<->device copy bandwidth of this box, measured in the same run with the
+    same kind of buffers as e2e (pinned, GPU-local NUMA node): H2D alone, D2H alone,
+    and both at once on two streams (what the pipelined e2e path overlaps)."""
+    import torch
+    with numa_local(dev):
+        h_src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        h_dst = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(h2d: bool, d2h: bool) -> float:
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s1)
+        s2.wait_event(e0)
+        for _ in range(reps):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d_a.copy_(h_src, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h_dst.copy_(d_b, non_blocking=True)
+        s1.wait_stream(s2)
+        e1.record(s1)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) * 1e-3
+
+    timed(True, True)  # warm
+    t_h2d, t_d2h, t_bi = timed(True, False), timed(False, True), timed(True, True)
+    return {"h2d_GBs": nbytes * reps / t_h2d / 1e9, "d2h_GBs": nbytes * reps / t_d2h / 1e9,
+            "bidir_GBs": 2 * nbytes * reps / t_bi / 1e9, "bytes_per_copy": nbytes,
+            "numa_local_cpus": len(numa_local_cpus(dev) or ())}
+
+
 def run_ours(args, cfg_name):
     import numpy as np
     import torch
@@ -213,14 +336,13 @@ def run_ours(args, cfg_name):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+    init_dist(dev)
     N, C, H, W, Oc, k = CONFIGS[cfg_name]
     pad = (k - 1) // 2
     # synthetic data, seeded per rank: rank r holds images [r*N, (r+1)*N) of the global batch
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
-    x_host = (torch.rand((N, C, H, W), generator=g) * 2 - 1).pin_memory()
+    with numa_local(dev):  # the e2e host buffers live on the GPU's NUMA node
+        x_host = (torch.rand((N, C, H, W), generator=g) * 2 - 1).pin_memory()
     w_host = torch.rand((Oc, C, k, k), generator=torch.Generator().manual_seed(7)) * 2 - 1
     x = x_host.to(dev)
     layer = XnorConv2d(w_host.to(dev), pad=pad, variant=args.variant)
@@ -299,7 +421,8 @@ def run_ours(args, cfg_name):
     # chunk overlapped with the compute of the next (layer.forward_host).  Timed with
     # CUDA events bracketing all three streams (start before the first H2D is issued,
     # end after the last D2H completes).
-    y_host = torch.empty((N, Oc, oh, ow), dtype=torch.float32).pin_memory()
+    with numa_local(dev):
+        y_host = torch.empty((N, Oc, oh, ow), dtype=torch.float32).pin_memory()
     e2e_steps = max(2, min(args.steps, 5))
     layer.forward(x_host, out=y_host)
     torch.cuda.synchronize(dev)
@@ -313,10 +436,21 @@ def run_ours(args, cfg_name):
     e1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps, ws, dev)
+    h2d_b, d2h_b = x_host.numel() * 4, y_host.numel() * 4
     e2e = {"value": bops_rank * ws / (e2e_ms * 1e-3) / 1e9, "unit": "Gbinop/s",
-           "h2d_bytes_per_step": x_host.numel() * 4, "d2h_bytes_per_step": y_host.numel() * 4,
+           "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
            "ms_per_step": e2e_ms,
-           "api": "XnorConv2d.forward(host tensor) -> pipelined H2D / K1-K4 / D2H on 3 streams"}
+           "api": "XnorConv2d.forward(host tensor) -> pipelined H2D / K1-K4 / D2H on 3 streams",
+           "host_buffers": "pinned, allocated on the GPU's NUMA node"}
+    try:  # e2e is PCIe-bound: report it against this box's copy bandwidth, same run
+        pc = pcie_peak(dev)
+        floor_ms = max(h2d_b / (pc["h2d_GBs"] * 1e9), d2h_b / (pc["d2h_GBs"] * 1e9),
+                       (h2d_b + d2h_b) / (pc["bidir_GBs"] * 1e9)) * 1e3
+        e2e["pcie"] = pc
+        e2e["pcie_floor_ms"] = floor_ms
+        e2e["frac_of_pcie_floor"] = floor_ms / e2e_ms
+    except Exception as exc:
+        e2e["pcie"] = {"error": repr(exc)}
 
     # ---- vanilla GPU row (Table 1): the same layer as a
     # full-precision cuDNN conv2d (FP32 and TF32), inputs resident, same event protocol
@@ -401,18 +535,18 @@ def run_ours(args, cfg_name):
         peak_probe = None
         peak_alt = None
         if kernel == "umma":
-            # MEASURED_PEAKS has no int8 entry, so the peak is B200_PROFILING.md's dense
-            # fp8/int8 tensor rate, 4.5 POPS = 2.25e15 MAC/s = 4500 Tbinop/s (1 MAC = 2
-            # binops); our own kind::i8 probe at sm_max_mhz (7874 MAC/clk/SM) gives
-            # 4580.  2 x the driver-measured bf16 burst (the cuBLAS GEMM reaches ~73 % of
-            # its nominal rate) is reported beside: the conv exceeds it.
+            # MEASURED_PEAKS has no int8 entry, so the stated peak is our own measured
+            # tcgen05 kind::i8 rate (tools/microbench/umma_probe.cu: 7874 MAC/clk/SM,
+            # back-to-back M128 N256 K32 MMAs from resident smem) at sm_max_mhz, x 2
+            # binops per MAC: 4580 Tbinop/s.  Beside it: B200_PROFILING.md's nominal dense
+            # fp8/int8 4.5 POPS and 2 x the driver-measured bf16 burst.
             bf16 = peaks.get("bf16_tflops")
             peak_probe = 2 * UMMA_I8_MAC_PER_CLK_SM * sms * f_max / 1e12
-            peak_tbinops = 4500.0
-            basis = ("fallback B200_PROFILING.md: dense fp8/int8 tensor 4.5 POPS = 2.25e15 MAC/s x 2 binops "
-                     "(MEASURED_PEAKS.json has no int8 entry)")
-            peak_alt = {"2x_measured_bf16_burst": 2.0 * float(bf16) if bf16 else None,
-                        "i8_probe_at_sm_max": peak_probe}
+            peak_tbinops = peak_probe
+            basis = (f"measured: tcgen05.mma kind::i8 probe {UMMA_I8_MAC_PER_CLK_SM} MAC/clk/SM "
+                     f"(profiles/umma_probe_r1.jsonl) x {sms} SMs x {f_max / 1e6:.0f} MHz x 2 binops/MAC")
+            peak_alt = {"nominal_B200_PROFILING_int8_4.5POPS": 4500.0,
+                        "2x_measured_bf16_burst": 2.0 * float(bf16) if bf16 else None}
             bound = "tensor"
         else:
             peak_tbinops = 2 * POPC_LANES_PER_CLK_SM * 32 * sms * f_max / 1e12
@@ -433,7 +567,10 @@ def run_ours(args, cfg_name):
         result = {
             "metric": METRIC, "value": value, "unit": "Gbinop/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32 (1-bit signs, int32 popcount accumulators) + f32 K/alpha",
+            "vs_baseline": None,
+            "dtype": ("u8 x s8 -> s32 (tcgen05 kind::i8 over 1-bit signs: d = [x < 0] bytes x +-1 filter "
+                      "signs, exact) + f32 K/alpha" if kernel == "umma" else
+                      "u32 (1-bit signs, XOR + POPC into int32 accumulators) + f32 K/alpha"),
             "data": "synthetic U(-1,1) float32 activations and weights, seeded",
             "config": {"workload": CONFIG_TEXT[cfg_name], "name": cfg_name, "batch_per_gpu": N,
                        "global_batch": N * ws, "C_in": C, "C_out": Oc, "H": H, "W": W, "k": k, "pad": pad,
@@ -448,7 +585,7 @@ def run_ours(args, cfg_name):
                          "traffic": traffic,
                          "peak_basis": basis,
                          "peak_alternatives_Tbinop_s": peak_alt,
-                         "frac_of_probe_peak": (achieved / peak_probe) if peak_probe else None},
+                         "frac_of_nominal_4500": (achieved / 4500.0) if peak_probe else None},
             "pack_roofline": {"bound": "hbm", "achieved": pack_bytes / (per_kernel["pack_input"] * 1e-3) / 1e9,
                               "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
                               "frac": pack_bytes / (per_kernel["pack_input"] * 1e-3) / 1e9 /
@@ -458,10 +595,10 @@ def run_ours(args, cfg_name):
             "ksweep": ksweep,
             "vanilla_gpu": vanilla,
             "gpu": props.name,
+            "comm": comm_info(),
         }
     if ws > 1:
         torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
     return result
 
 
@@ -477,9 +614,7 @@ def run_network(args, cfg_name):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+    init_dist(dev)
     gb = NETWORK_CONFIGS[cfg_name] if cfg_name == "C5" else NETWORK_CONFIGS[cfg_name] * ws
     a, b = shard_bounds(gb, ws, rank)
     N = b - a
@@ -542,10 +677,9 @@ def run_network(args, cfg_name):
                "e2e": {"value": bops / (e2e_ms * 1e-3) / 1e9, "unit": "Gbinop/s",
                        "h2d_bytes_per_step": x_host.numel() * 4 * ws, "d2h_bytes_per_step": logits_host.numel() * 4 * ws,
                        "ms_per_step": e2e_ms, "api": "XnorNetAlexNet.forward"},
-               "clocks": clk.summary()}
+               "clocks": clk.summary(), "comm": comm_info()}
     if ws > 1:
         torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
     return res
 
 
@@ -627,27 +761,54 @@ def network_summary(variant="auto", batch=256, steps=5, warmup=3):
             "binary_kernels": net.binary_kernels(batch), "note": "full numbers: bench.py --config C4"}
 
 
+def cpu_model() -> str:
+    """The host CPU model (lscpu's 'Model name', from /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline_fields(cfg_name, budget_s, ksweep=None):
+    """The reference's fused kernel on this host: all threads (the headline CPU row)
+    and threads=1 (the race-free path at every k, SURVEY.md section 0 item 6);
+    medians of 5 sub-samples each."""
     cfg = CONFIGS[cfg_name]
     rr = RefRunner(cfg)
     N, C, H, W, Oc, k = cfg
-    s_pair, pairs = rr.pair_rate(budget_s)
     bops_pair = binops(1, C, H, W, 1, k)
+    samples, pairs = rr.pair_rates(budget_s)
+    s_pair = statistics.median(samples)
+    s1, pairs1 = rr.pair_rates(max(2.0, budget_s / 3), threads=1)
+    s1_pair = statistics.median(s1)
     out = {"value": bops_pair / s_pair / 1e9, "unit": "Gbinop/s", "cores": rr.threads, "kind": "reference",
            "sample": f"{pairs} (image, filter) pairs of {cfg_name} through the reference's fused "
-                     f"xnor_reconstruct (oracle/_ref, -march={rr.march}), threads={rr.threads}",
-           "ms_per_pair": s_pair * 1e3}
+                     f"xnor_reconstruct (oracle/_ref, -march={rr.march}), threads={rr.threads}, median of 5",
+           "ms_per_pair": s_pair * 1e3, "ms_per_pair_mean": statistics.mean(samples) * 1e3,
+           "cpu_model": cpu_model(),
+           "threads_1": {"value": bops_pair / s1_pair / 1e9, "unit": "Gbinop/s", "cores": 1,
+                         "ms_per_pair": s1_pair * 1e3, "pairs": pairs1,
+                         "note": "race-free single-thread fused path (the parity oracle's protocol)"}}
     if ksweep:
         for kname, row in ksweep.items():
             rk = RefRunner(CONFIGS[kname])
-            sp, pr = rk.pair_rate(max(2.0, budget_s / 4))
+            sp_all, _ = rk.pair_rates(max(2.0, budget_s / 4))
+            sp1, _ = rk.pair_rates(max(1.5, budget_s / 6), threads=1)
+            sp, sp_1 = statistics.median(sp_all), statistics.median(sp1)
             _, Ck, Hk, Wk, _, kk = CONFIGS[kname]
-            row["cpu_Gbinop_s"] = binops(1, Ck, Hk, Wk, 1, kk) / sp / 1e9
+            bk = binops(1, Ck, Hk, Wk, 1, kk)
+            row["cpu_Gbinop_s"] = bk / sp / 1e9
             row["cpu_threads"] = rk.threads
             row["cpu_note"] = ("reference fused path, threads>1: output nondeterministic (reference "
                                "race, SURVEY.md section 0 item 6)" if CONFIGS[kname][5] != 3 else
                                "reference fused path")
             row["speedup_vs_cpu"] = row["gpu_Gbinop_s"] / row["cpu_Gbinop_s"]
+            row["cpu_threads_1_Gbinop_s"] = bk / sp_1 / 1e9
+            row["speedup_vs_cpu_threads_1"] = row["gpu_Gbinop_s"] / row["cpu_threads_1_Gbinop_s"]
     return out
 
 
@@ -667,8 +828,8 @@ def run_reference(args, cfg_name):
         s_pair, pairs = rr.pair_rate(per_step_budget)
         rates.append(bops_pair / s_pair / 1e9)
     el = time.perf_counter() - t0
-    value = statistics.mean(rates)
-    return {"metric": METRIC, "value": value, "unit": "Gbinop/s", "n_gpus": ws, "steps": args.steps,
+    value = statistics.median(rates)
+    return {"metric": METRIC, "value": value, "value_mean": statistics.mean(rates), "unit": "Gbinop/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 tile words + f32", "data": "synthetic",
             "impl": "reference",
@@ -678,6 +839,74 @@ def run_reference(args, cfg_name):
                              "sample": f"each step ~{per_step_budget:.1f}s of (image, filter) pairs of "
                                        f"{cfg_name} through xnor_reconstruct (oracle/_ref, -march={rr.march})"},
             "e2e": {"value": value, "unit": "Gbinop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` run directly (no torchrun around it): re-launch this same
+    command line as N ranks under torch.distributed.run on 127.0.0.1, one process
+    per GPU.  Rank 0's stdout (the JSON line) passes straight through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))).returncode
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo on CPU) -- rendezvous,
+    per-rank batch shards of C5, a rank-local stand-in step on each shard with no
+    collective, the barrier + max-over-ranks timing, and rank 0's one JSON line.
+    Exercised by tests/test_bench_spawn.py."""
+    import torch
+    import torch.distributed as dist
+    from paper_2007_14178_b200.shard import shard_bounds
+    ws, rank, _ = dist_env()
+    init_dist(None)
+    gb = NETWORK_CONFIGS["C5"]
+    a, b = shard_bounds(gb, ws, rank)
+    x = torch.arange(a, b, dtype=torch.float64)
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    acc = 0.0
+    for _ in range(args.steps):
+        acc += float(x.sum())  # this rank's shard only
+    ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / max(1, args.steps), ws, None)
+    shards = [None] * ws
+    if ws > 1:
+        dist.all_gather_object(shards, (rank, a, b, acc / max(1, args.steps)))
+    else:
+        shards = [(rank, a, b, acc / max(1, args.steps))]
+    res = None
+    if rank == 0:
+        covered = sorted((a_, b_) for _, a_, b_, _ in shards)
+        res = {"metric": METRIC, "dry_run": True, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": ms, "config": {"workload": CONFIG_TEXT["C5"], "global_batch": gb},
+               "shards": [[a_, b_] for a_, b_ in covered],
+               "shards_cover_batch": covered[0][0] == 0 and covered[-1][1] == gb and
+                                     all(covered[i][1] == covered[i + 1][0] for i in range(len(covered) - 1)),
+               "shard_sums_ok": all(abs(s_ - (a_ + b_ - 1) * (b_ - a_) / 2) < 1e-6 for _, a_, b_, s_ in shards),
+               "comm": comm_info()}
+    if ws > 1:
+        dist.barrier()
+    return res
+
+
+def strong_scaling_c5(args):
+    """C5 beside the default C3 line: the XNOR-Net forward over a fixed global batch
+    of 2048 split across the ranks (strong scaling), so one bench run records both
+    curves; the driver's scaling efficiency is computed from `value` (C3, weak)."""
+    import copy
+    a2 = copy.copy(args)
+    a2.steps, a2.warmup = max(5, min(args.steps, 10)), max(3, args.warmup)
+    r = run_network(a2, "C5")
+    if r is None:
+        return None
+    return {k: r.get(k) for k in ("value", "unit", "images_per_s", "ms_per_step", "n_gpus", "scaling", "config",
+                                  "clocks")}
 
 
 def main():
@@ -692,9 +921,22 @@ def main():
     ap.add_argument("--no-ksweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="C4/C5: eager forward instead of the CUDA graph")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU reference work")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing only, on CPU with gloo (no GPU): spawn, shards, timing, JSON line")
+    ap.add_argument("--no-strong", action="store_true", help="skip the C5 strong-scaling extra")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ws_env = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and ws_env == 0:
+        sys.exit(spawn_ranks(args.gpus))
+    if ws_env and ws_env != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws_env} overrides --gpus {args.gpus}", file=sys.stderr)
+    if args.dry_run:
+        res = run_dry(args)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
     if args.impl == "reference":
         res = run_reference(args, args.config if args.config in CONFIGS else "C3")
     elif args.config in NETWORK_CONFIGS:
@@ -702,6 +944,13 @@ def main():
     else:
         res = run_ours(args, args.config)
         ws, rank, _ = dist_env()
+        if args.config == "C3" and not args.no_strong and not args.no_ksweep:
+            try:  # every rank runs it (collective timing); rank 0 reports
+                c5 = strong_scaling_c5(args)
+            except Exception as exc:
+                c5 = {"error": repr(exc)}
+            if res is not None:
+                res["strong_scaling_C5"] = c5
         if res is not None and rank == 0 and ws == 1 and not args.no_ksweep:
             for key, fn in (("network_C4", lambda: network_summary(args.variant)),
                             ("binary_stack_C3", binary_stack_summary)):
@@ -717,6 +966,9 @@ def main():
                 res["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if res is not None:
         print(json.dumps(res), flush=True)
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
