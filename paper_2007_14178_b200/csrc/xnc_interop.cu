@@ -180,6 +180,39 @@ __global__ void k_channel_abs_mean_f64(const double* __restrict__ x, int C, long
   A[i] = __ddiv_rn(s, (double)C);
 }
 
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src pairwise_sum):
+// what np.abs(x).mean(axis=0) does when the reduced axis is the only one, i.e. a
+// (C,1,1) tensor.  <8 terms: one running sum; <=128: eight strided accumulators
+// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail; above that
+// split at n/2 rounded down to a multiple of 8 and recurse.
+__device__ double np_pairwise_abs_sum(const double* a, long n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (long i = 0; i < n; ++i) r = __dadd_rn(r, fabs(a[i]));
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = fabs(a[j]);
+    long i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], fabs(a[i + j]));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, fabs(a[i]));
+    return res;
+  }
+  long n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_abs_sum(a, n2), np_pairwise_abs_sum(a + n2, n - n2));
+}
+
+// channel_abs_mean of a (C,1,1) tensor: numpy reduces the lone contiguous axis
+// pairwise (0.0 identity first), not sequentially.
+__global__ void k_channel_abs_mean_1x1_f64(const double* __restrict__ x, int C, double* __restrict__ A) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) A[0] = __ddiv_rn(__dadd_rn(0.0, np_pairwise_abs_sum(x, C)), (double)C);
+}
+
 // apply_scaling (scaling.py:91-98): ints * K * alpha in float64, left to right.
 __global__ void k_apply_scaling_f64(const int32_t* __restrict__ ints, const double* __restrict__ K,
                                     double alpha, long n, double* __restrict__ out) {
@@ -357,6 +390,10 @@ int xnc_xnor_reconstruct(const uint64_t* weight_words, uint64_t mask, int tile_h
 int xnc_channel_abs_mean_f64(const double* x, int C, int H, int W, double* A, void* stream) {
   if (!x || !A || C < 1 || H < 1 || W < 1) return XNC_EINVAL;
   long hw = (long)H * W;
+  if (hw == 1) {  // numpy's pairwise order for a lone reduced axis (see above)
+    k_channel_abs_mean_1x1_f64<<<1, 32, 0, as_stream(stream)>>>(x, C, A);
+    return launch_status();
+  }
   k_channel_abs_mean_f64<<<blocks_for(hw), 256, 0, as_stream(stream)>>>(x, C, hw, A);
   return launch_status();
 }

@@ -119,6 +119,15 @@ def test_geometry_mismatch_errors(xc):
         xc.build_filter(xc.Tensor3(np.ones((2, 5, 5))), geom)
 
 
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 1, 1), (8, 1, 1), (9, 1, 1), (129, 1, 1), (1000, 1, 1),
+                                   (3001, 1, 1), (13, 1, 5), (13, 5, 1), (200, 3, 3)])
+def test_channel_abs_mean_is_numpys(xc, shape):
+    # the reference's own formula (tensor.py:103-105); (C,1,1) takes numpy's pairwise order
+    rng = np.random.default_rng(shape[0])
+    x = rng.standard_normal(shape) * 37.0
+    assert np.array_equal(xc.channel_abs_mean(xc.Tensor3(x)).data, np.abs(x).mean(axis=0))
+
+
 # ---------------------------------------------------------------- scaling (float64 operator API)
 @pytest.mark.parametrize("case", golden_io.scale_cases(), ids=lambda c: c["name"])
 def test_float64_scale_path_matches_reference_golden(xc, case):

@@ -50,6 +50,16 @@ def test_oracle_float64_operator_api(case):
     assert np.array_equal(y, case["y"])
 
 
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 1, 1), (8, 1, 1), (9, 1, 1), (129, 1, 1), (1000, 1, 1),
+                                   (3001, 1, 1), (13, 1, 5), (13, 5, 1), (200, 3, 3)])
+def test_oracle_channel_abs_mean_is_numpys(shape):
+    # tensor.py:103-105 is np.abs(x).mean(axis=0): pairwise when axis 0 is the lone
+    # axis (C,1,1), sequential per pixel otherwise -- bit-exact either way
+    rng = np.random.default_rng(shape[0])
+    x = rng.standard_normal(shape) * 37.0
+    assert np.array_equal(O.channel_abs_mean_f64(x), np.abs(x).mean(axis=0))
+
+
 # ---- the reference's own KATs -------------------------------------------------------
 
 def test_kat_padding_is_plus_one():
