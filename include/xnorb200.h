@@ -246,6 +246,25 @@ int xnc_channel_abs_mean_f64(const double* x, int C, int H, int W, double* A, vo
 int xnc_apply_scaling_f64(const int32_t* ints, const double* K, double alpha, long n, double* out,
                           void* stream);
 
+/* ---- the reference's naive truth (reference.py) and vanilla_conv ---------
+ * Not on the hot path: the checkers of paper_2007_14178_b200.verify (the
+ * reference's verify.py:42-145 gates) and the float baseline of its bench
+ * (bench.py:196-256).  One thread per output, the reference's (ch, ky, kx)
+ * order, one rounding per operation (no FMA).  Independent of the packed engine.
+ * sign_conv2d_int (reference.py:57-90): signs / wsigns int8 +-1 [C][h][w] /
+ * [C][kh][kw], taps outside the plane count +1 -> out i32 [h+2p-kh+1][w+2p-kw+1]. */
+int xnc_ref_sign_conv2d(const int8_t* signs, const int8_t* wsigns, int C, int h, int w, int kh, int kw,
+                        int pad, int32_t* out, void* stream);
+/* conv2d_float (reference.py:30-54), bwn == 0: f64 cross-correlation with zero
+ * padding.  bwn_conv (reference.py:93-122), bwn != 0: +-x by sign(w > 0), then
+ * * scale.  x [C][h][w], w [C][kh][kw] f64 -> out f64 [h+2p-kh+1][w+2p-kw+1]. */
+int xnc_ref_conv2d_f64(const double* x, const double* wt, int C, int h, int w, int kh, int kw, int pad,
+                       int bwn, double scale, double* out, void* stream);
+/* vanilla_conv (_kernels_cy.pyx:107-123): padded [C][ph][pw] against weights
+ * [C][kh][kw], both f32 (dtype 0) or f64 (dtype 1) -> out [ph-kh+1][pw-kw+1]. */
+int xnc_vanilla_conv(const void* padded, int dtype, int C, int ph, int pw, const void* weights, int kh,
+                     int kw, void* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

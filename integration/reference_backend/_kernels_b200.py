@@ -61,6 +61,7 @@ _lib.xnc_scale_rows.argtypes = [_P, _I, _I, _I, _I, _I, _P, _P]
 _lib.xnc_scale_join.argtypes = [_P, _I, _P, _I, _D, _D, _I, _I, _P, _P]
 _lib.xnc_xnor_reconstruct.argtypes = [_P, _U64, _I, _I, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I,
                                       _D, _D, _P, _P]
+_lib.xnc_vanilla_conv.argtypes = [_P, _I, _I, _I, _I, _P, _I, _I, _P, _P]
 _lib.xnc_strerror.argtypes = [_I]
 _lib.xnc_strerror.restype = ctypes.c_char_p
 _rt.cudaMalloc.argtypes = [ctypes.POINTER(_P), ctypes.c_size_t]
@@ -185,5 +186,13 @@ def xnor_reconstruct(weight_words, mask, tile_h, tile_w, stride_y, stride_x, k_a
 
 
 def vanilla_conv(padded, weights, out, threads) -> None:
-    """_kernels_cy.pyx:107-123: the float comparison baseline, not on the XNOR path."""
-    raise NotImplementedError("vanilla_conv is not part of the B200 XNOR path; use backend='compiled'")
+    """_kernels_cy.pyx:107-123 -> xnc_vanilla_conv: the bench's float baseline,
+    (ch, ky, kx) order, one rounding per multiply and per add."""
+    _contig(padded, "padded", _F)
+    _contig(weights, "weights", (padded.dtype,))
+    _contig(out, "out", (padded.dtype,))
+    p, w, o = _Dev(padded), _Dev(weights), _Dev(out, upload=False)
+    c, ph, pw = padded.shape
+    _ok(_lib.xnc_vanilla_conv(p.ptr, _DT[padded.dtype], c, ph, pw, w.ptr, weights.shape[1], weights.shape[2],
+                              o.ptr, None), "vanilla_conv")
+    o.download()

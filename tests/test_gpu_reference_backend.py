@@ -169,3 +169,34 @@ def test_reference_b200_equals_reference_compiled(xnorconv, k, word_bits):
         outs[be] = (y, ints, eng, K)
     for a, b in zip(outs["compiled"], outs["b200"]):
         assert a.dtype == b.dtype and np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_reference_vanilla_conv_b200_equals_python(xnorconv, dtype):
+    """vanilla_conv (_kernels_py.py:90-108 order: products rounded, then added, in
+    (ch, ky, kx) order) -- the b200 kernel and the reference's numpy fallback agree bit for bit."""
+    from xnorconv import _backend
+    rng = np.random.default_rng(4)
+    padded = rng.uniform(-1, 1, (5, 21, 19)).astype(dtype)
+    w = rng.uniform(-1, 1, (5, 3, 3)).astype(dtype)
+    outs = []
+    for be in ("python", "b200"):
+        out = np.empty((19, 17), dtype=dtype)
+        _backend.get_kernels(be).vanilla_conv(padded, w, out, 1)
+        outs.append(out)
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_reference_bench_harness_on_b200(xnorconv):
+    """The reference's own bench (bench.py:223-260) with backend='b200': its
+    pre-timing gates (exact ints vs the naive loops, decomposition <= 1e-5, bwn
+    and vanilla interior checks, thread-count invariance) all pass on our kernels."""
+    from xnorconv.bench import BenchConfig, emit_report, parse_csv, run_bench
+    cfg = BenchConfig(sizes=(48, 64), kernel=3, channels=2, repeats=2, warmup=1, threads=2, backend="b200")
+    report = run_bench(cfg)
+    assert {r.impl for r in report.rows} == {"vanilla-1t", "vanilla-mt", "xnor-1t", "xnor-mt"}
+    assert parse_csv(emit_report(report, "csv")).rows == report.rows
