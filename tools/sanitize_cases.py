@@ -27,10 +27,12 @@ def case_pack(rng):
     for shape in ((2, 40, 9, 12), (1, 300, 5, 5), (3, 64, 16, 16)):
         x = O.f32_exact(rng, shape)
         bits, A = ops.pack_input(torch.from_numpy(x).cuda())
-        wb, wa = O.pack_input(x) if hasattr(O, "pack_input") else (None, None)
+        N, C, H, W = shape
+        sgn = np.zeros((N, H, W, (C + 31) // 32 * 32), dtype=np.uint64)
+        sgn[..., :C] = (x >= 0).transpose(0, 2, 3, 1)
+        want = (sgn.reshape(N, H, W, -1, 32) << np.arange(32, dtype=np.uint64)).sum(-1).astype(np.uint32)
         torch.cuda.synchronize()
-        if wa is not None:
-            assert np.array_equal(A.cpu().numpy().view(np.uint32), wa.view(np.uint32))
+        assert np.array_equal(bits.cpu().numpy().view(np.uint32), want)
 
 
 def _check_conv(x, w, pad, variant, **kw):
