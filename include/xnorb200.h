@@ -246,6 +246,20 @@ int xnc_channel_abs_mean_f64(const double* x, int C, int H, int W, double* A, vo
 int xnc_apply_scaling_f64(const int32_t* ints, const double* K, double alpha, long n, double* out,
                           void* stream);
 
+/* ---- XNOR-Net AlexNet conv1 on the tensor cores (network.py front end) -----
+ * The network's full-precision first layer (11x11, stride 4, pad 2, 3 -> 96,
+ * 224 x 224 -> 55 x 55) as one tcgen05 kind::tf32 kernel on CTA pairs, reading the
+ * raw images (no space-to-depth pass).  Operands are rounded to TF32 (cvt.rna, as
+ * cuDNN's TF32 mode), products accumulate in f32.  Not on the binary path.
+ * xnc_conv1_pack_weights: w f32 [96][3][11][11] -> wq f32, xnc_conv1_weight_bytes()
+ * bytes (27 (c, tap) blocks x 96 filters x 16 phases, TF32-rounded).
+ * xnc_conv1_forward: x f32 [N][3][224][224] (8-byte aligned) -> y f32
+ * [N][55][55][96] channels-last (16-byte aligned), the raw conv (no bias: the
+ * caller's xnc_max_pool adds it with the ReLU). */
+size_t xnc_conv1_weight_bytes(void);
+int xnc_conv1_pack_weights(const float* w, float* wq, void* stream);
+int xnc_conv1_forward(const float* x, int N, const float* wq, float* y, void* stream);
+
 /* ---- the reference's naive truth (reference.py) and vanilla_conv ---------
  * Not on the hot path: the checkers of paper_2007_14178_b200.verify (the
  * reference's verify.py:42-145 gates) and the float baseline of its bench

@@ -71,6 +71,9 @@ def lib() -> ctypes.CDLL:
         "xnc_ref_sign_conv2d": ([P, P, I, I, I, I, I, I, P, P], I),
         "xnc_ref_conv2d_f64": ([P, P, I, I, I, I, I, I, I, D, P, P], I),
         "xnc_vanilla_conv": ([P, I, I, I, I, P, I, I, P, P], I),
+        "xnc_conv1_weight_bytes": ([], S),
+        "xnc_conv1_pack_weights": ([P, P, P], I),
+        "xnc_conv1_forward": ([P, I, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -90,7 +93,8 @@ def exported_symbols() -> list[str]:
             "xnc_pack_input_nhwc", "xnc_umma_emit_supported", "xnc_xnor_conv_umma_emit", "xnc_pack_plane", "xnc_unpack_plane",
             "xnc_sign_plane", "xnc_xnor_accumulate", "xnc_filter_words", "xnc_box_mean",
             "xnc_scale_rows", "xnc_scale_join", "xnc_xnor_reconstruct", "xnc_channel_abs_mean_f64",
-            "xnc_apply_scaling_f64", "xnc_ref_sign_conv2d", "xnc_ref_conv2d_f64", "xnc_vanilla_conv"]
+            "xnc_apply_scaling_f64", "xnc_ref_sign_conv2d", "xnc_ref_conv2d_f64", "xnc_vanilla_conv",
+            "xnc_conv1_weight_bytes", "xnc_conv1_pack_weights", "xnc_conv1_forward"]
 
 DTYPE_F32, DTYPE_F64, DTYPE_I8 = 0, 1, 2
 

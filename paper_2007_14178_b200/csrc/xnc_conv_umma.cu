@@ -67,6 +67,7 @@
 #include <cstdlib>
 
 #include "xnc_common.cuh"
+#include "xnc_tcgen05.cuh"
 
 namespace xnc {
 
@@ -103,105 +104,12 @@ constexpr int kProfSlots = 16;
 // 10 epilogue (warp 4) TMEM load + constants, 11 epilogue math + stores.
 __device__ unsigned long long g_umma_prof[1024][kProfSlots];
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// K-major, SWIZZLE_128B UMMA shared-memory descriptor (sm_100 version 1): rows
-// 128 B apart, 8-row groups 1024 B apart (SBO).  The swizzle is a function of the
-// absolute smem address, so row-shifted starts need no base offset.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t addr) {
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-
-// shared::cluster address of the same variable in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t map_to_rank(uint32_t local, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
-  return r;
-}
-
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-  }
-}
-
-// try_wait with a suspend-time hint (ns): the thread sleeps until the phase
-// completes or the hint elapses instead of re-polling
-__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_addr(bar)), "r"(parity), "r"(hint_ns)
-        : "memory");
-  }
-}
-
 #ifndef XNC_EPI_HINT
 #define XNC_EPI_HINT 0
 #endif
 #ifndef XNC_PROD_HINT
 #define XNC_PROD_HINT 0
 #endif
-
-__device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, bool prof,
-                                               unsigned long long& acc, uint32_t hint_ns = 0) {
-  const unsigned long long t0 = prof ? clock64() : 0ull;
-  if (hint_ns) mbar_wait_hint(bar, parity, hint_ns);
-  else mbar_wait(bar, parity);
-  if (prof) acc += clock64() - t0;
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-}
-
-// arrive on an mbarrier given by its shared::cluster address (possibly the peer's).
-// Default (.release.cta) semantics: a .cluster release would compile to
-// MEMBAR.ALL.GPU + CCTL.IVALL, stalling each epilogue warp until its streaming
-// stores drain (ncu: 10% 'membar' stalls).  Only the TMEM reads must be ordered
-// before the arrive, and tcgen05.fence::before_thread_sync does that.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-
-// TMA tile loads into this CTA's shared memory, completing on the mbarrier at a
-// shared::cluster address (the leader CTA's): .cta_group::2 lets the barrier
-// live in the peer CTA.
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
-                                                 uint32_t bar_cluster) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
-      : "memory");
-}
 
 __device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                                  int c3, uint32_t bar_cluster) {
@@ -274,35 +182,6 @@ __device__ __forceinline__ void umma_chunk_pair(uint32_t d0, int np, uint32_t a_
 }
 #undef XNC_MMA1
 
-__device__ __forceinline__ void umma_commit_pair_elect(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-          smem_addr(bar)),
-      "h"((uint16_t)0x3)
-      : "memory");
-}
-
-// arrive (once MMAs issued so far complete) on the mbarrier at this offset in
-// both CTAs of the pair
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_addr(bar)),
-      "h"((uint16_t)0x3)
-      : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
-      " [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-        "=r"(v[15])
-      : "r"(addr));
-}
-
 #ifndef XNC_ST_HINT
 #define XNC_ST_HINT ".cs"
 #endif
@@ -324,57 +203,6 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
                "f"(v), "r"((int)pred)
                : "memory");
 }
-
-// ---- staged epilogue stores: registers -> shared memory -> bulk async copies
-// (cp.async.bulk, the TMA engine's non-tensor form) of whole 16-byte-aligned output
-// row segments.  Each output costs one STS with an immediate offset instead of a
-// 64-bit address computation and a predicated STG.
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-// bytes (a multiple of 16, 16-byte aligned src and dst) shared::cta -> global, in
-// this thread's bulk group; pred = 0: nothing issued
-__device__ __forceinline__ void bulk_store_pred(float* dst, uint32_t src, uint32_t bytes, uint64_t pol, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
-      "@q cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %4;\n\t}" ::"l"(dst),
-      "r"(src), "r"(bytes), "r"((int)pred), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// this thread's bulk copies have finished READING shared memory (the buffer may be rewritten)
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
-}
-
-__device__ __forceinline__ void named_bar_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-// wait for this thread's TMEM loads with the destination registers as operands, so
-// the compiler cannot hoist their uses above the wait
-#define XNC_R16(v) "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), \
-    "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
-__device__ __forceinline__ void tmem_wait_ld_regs(uint32_t (&v)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" : XNC_R16(v)::"memory");
-}
-// orders later uses of v after the preceding (volatile) wait
-__device__ __forceinline__ void reg_dep16(uint32_t (&v)[16]) { asm volatile("" : XNC_R16(v)); }
-#undef XNC_R16
 
 struct PairGeom {
   int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NP, MH, taps, Cw;
@@ -1285,20 +1113,6 @@ bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) 
   PairGeom g;
   size_t smem;
   return pair_plan(N, C, H, W, O, kh, kw, pad, g, smem);
-}
-
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  // a function-local static: initialised once, thread-safe (the driver entry point
-  // is process-wide, not per device)
-  static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    return nullptr;
-  }();
-  return fn;
 }
 
 int umma_profile_read(unsigned long long* host, int n_ctas) {

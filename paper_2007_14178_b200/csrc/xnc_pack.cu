@@ -245,9 +245,23 @@ __global__ void __launch_bounds__(128) k_pack_small(const float* __restrict__ x,
   __syncthreads();
   if (!in) return;
   if (warp == 0) {
+    // sequential chain per pixel; the next 16 channels' LDS issued before this 16's adds
     float s = 0.0f;
-#pragma unroll 8
-    for (int c = 0; c < C; ++c) s = __fadd_rn(s, fabsf(tile[c * 32 + lane]));
+    float cur[16], nxt[16];
+    const int nb = C >> 4;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) cur[u] = nb > 0 ? tile[u * 32 + lane] : 0.0f;
+    for (int k = 0; k < nb; ++k) {
+      if (k + 1 < nb) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) nxt[u] = tile[((k + 1) * 16 + u) * 32 + lane];
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s = __fadd_rn(s, fabsf(cur[u]));
+#pragma unroll
+      for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
+    }
+    for (int c = nb << 4; c < C; ++c) s = __fadd_rn(s, fabsf(tile[c * 32 + lane]));
     if (A) A[q] = __fmul_rn(s, inv);
   } else {
     for (int j = warp - 1; j < Cw; j += 3) {
@@ -271,7 +285,7 @@ constexpr int kAbsChunk = 1024;
 __global__ void __launch_bounds__(128) k_absmean_wide(const float* __restrict__ x, int C, long npix, float inv,
                                                       float* __restrict__ A, const float* __restrict__ in_scale,
                                                       const float* __restrict__ in_shift) {
-  __shared__ float buf[4][kAbsChunk];
+  __shared__ __align__(16) float buf[4][kAbsChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long q = (long)blockIdx.x * 4 + warp;
   if (q >= npix) return;
@@ -291,8 +305,28 @@ __global__ void __launch_bounds__(128) k_absmean_wide(const float* __restrict__ 
     for (int u = 0; u < kAbsChunk / 32; ++u) b[u * 32 + lane] = v[u];
     __syncwarp();
     if (lane == 0) {
-#pragma unroll 16
-      for (int i = 0; i < n; ++i) s = __fadd_rn(s, b[i]);
+      // the chain is one FADD per channel (4 cycles); shared-memory reads are
+      // batched 32 channels ahead (8 x LDS.128 of the next batch issued before the
+      // adds of this one), else every add waits out an LDS latency (~25 cycles)
+      const float4* b4 = reinterpret_cast<const float4*>(b);
+      const int nb = n >> 5;  // whole 32-channel batches
+      float4 cur[8], nxt[8];
+      if (nb > 0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur[u] = b4[u];
+      }
+      for (int k = 0; k < nb; ++k) {
+        if (k + 1 < nb) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) nxt[u] = b4[(k + 1) * 8 + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, cur[u].x), cur[u].y), cur[u].z), cur[u].w);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+      }
+      for (int i = nb << 5; i < n; ++i) s = __fadd_rn(s, b[i]);
     }
   }
   if (lane == 0) A[q] = __fmul_rn(s, inv);

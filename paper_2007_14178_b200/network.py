@@ -66,7 +66,7 @@ class XnorNetAlexNet:
     """Random-init XNOR-Net AlexNet resident on one device."""
 
     def __init__(self, device: torch.device | str = "cuda", num_classes: int = 1000, seed: int = 0,
-                 variant: str = "auto", emit_signs: bool = True):
+                 variant: str = "auto", emit_signs: bool = True, conv1: str = "tcgen05"):
         dev = torch.device(device)
         g = torch.Generator().manual_seed(seed)
 
@@ -85,6 +85,12 @@ class XnorNetAlexNet:
         self.conv1_w_s2d = (w12.view(96, 3, 3, 4, 3, 4).permute(0, 1, 3, 5, 2, 4)
                             .reshape(96, 48, 3, 3).contiguous())
         self.conv1_w_s2d_cl = self.conv1_w_s2d.contiguous(memory_format=torch.channels_last)
+        # conv1 engine: 'tcgen05' = our kind::tf32 kernel on the raw images (no
+        # space-to-depth pass; csrc/xnc_conv1.cu), 'cudnn' = the s2d + cuDNN TF32 path
+        if conv1 not in ("tcgen05", "cudnn"):
+            raise ValueError(f"conv1 must be 'tcgen05' or 'cudnn', got {conv1!r}")
+        self.conv1 = conv1
+        self.conv1_wq = ops.conv1_pack_weights(self.conv1_w) if conv1 == "tcgen05" else None
         # XNOR-Net's binary block is BatchNorm -> BinActiv -> BinConv (-> Pool); the
         # batch norms are folded to a per-channel affine (scale, shift), random-init
         # like everything else.  After a pool it runs inside K1 of the next layer
@@ -132,8 +138,11 @@ class XnorNetAlexNet:
             # kernels, same values as F.pad / F.pixel_unshuffle and F.relu / F.max_pool2d),
             # channels-last end to end: cuDNN's NHWC TF32 conv is 0.39 vs 0.60 ms NCHW, and
             # conv2's K1 reads the channels-last map directly (tools/front_probe.py)
-            xs = ops.pad_space_to_depth(x, 2, 4, channels_last=True)
-            h = F.conv2d(xs, self.conv1_w_s2d_cl)  # bias folded into the pool (exact: see max_pool)
+            if self.conv1 == "tcgen05" and tuple(x.shape[1:]) == (3, 224, 224):
+                h = ops.conv1_forward(x, self.conv1_wq)  # TF32 tensor cores, channels-last out
+            else:
+                xs = ops.pad_space_to_depth(x, 2, 4, channels_last=True)
+                h = F.conv2d(xs, self.conv1_w_s2d_cl)  # bias folded into the pool (exact: see max_pool)
             return ops.max_pool(h, 3, 2, relu=True, bias=self.conv1_b)
 
     def _forward(self, x: torch.Tensor, return_features: bool):

@@ -107,6 +107,38 @@ def pad_space_to_depth(x: torch.Tensor, pad: int, r: int, channels_last: bool = 
     return out
 
 
+def conv1_pack_weights(w: torch.Tensor) -> torch.Tensor:
+    """XNOR-Net AlexNet conv1 weights f32 [96, 3, 11, 11] -> the tcgen05 TF32 kernel's
+    B operand (27 (c, tap) blocks x 96 filters x 16 space-to-depth phases, TF32-rounded)."""
+    _need_cuda(w, "w", torch.float32)
+    if tuple(w.shape) != (96, 3, 11, 11):
+        raise ValueError(f"conv1 weights must be [96, 3, 11, 11], got {tuple(w.shape)}")
+    wq = torch.empty(lib().xnc_conv1_weight_bytes() // 4, dtype=torch.float32, device=w.device)
+    check(lib().xnc_conv1_pack_weights(w.contiguous().data_ptr(), wq.data_ptr(), _stream(w.device)),
+          "xnc_conv1_pack_weights")
+    return wq
+
+
+def conv1_forward(x: torch.Tensor, wq: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """conv1 (11x11, stride 4, pad 2, no bias) of x f32 [N, 3, 224, 224] on the tcgen05
+    TF32 kernel -> f32 [N, 96, 55, 55] stored channels-last (the layout the network's
+    bias + ReLU + pool pass and conv2's K1 read)."""
+    _need_cuda(x, "x", torch.float32)
+    x = x.contiguous()
+    if x.shape[1:] != (3, 224, 224):
+        raise ValueError(f"conv1 input must be [N, 3, 224, 224], got {tuple(x.shape)}")
+    N = x.shape[0]
+    if out is None:
+        out = torch.empty((N, 96, 55, 55), dtype=torch.float32, device=x.device,
+                          memory_format=torch.channels_last)
+    elif (tuple(out.shape) != (N, 96, 55, 55) or out.dtype != torch.float32 or out.device != x.device
+          or not out.is_contiguous(memory_format=torch.channels_last)):
+        raise ValueError("out must be a channels-last f32 [N, 96, 55, 55] tensor on x's device")
+    check(lib().xnc_conv1_forward(x.data_ptr(), N, wq.data_ptr(), out.data_ptr(), _stream(x.device)),
+          "xnc_conv1_forward")
+    return out
+
+
 def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None, in_pool=None):
     """K1: x f32 [N,C,H,W] -> (bits i32 [N,H,W,Cw] (u32 payload), A f32 [N,H,W]).
 

@@ -131,3 +131,39 @@ def test_network_emitted_signs_match_float_chain(batch):
     b = XnorNetAlexNet("cuda", seed=5, emit_signs=False)
     x = torch.rand((batch, 3, 224, 224), device="cuda") * 2 - 1
     assert torch.equal(a.forward(x), b.forward(x))
+
+
+@pytest.mark.parametrize("batch", [1, 5, 37])
+def test_conv1_tcgen05_tf32_matches_fp64(batch):
+    """conv1 on our kind::tf32 tensor-core kernel (csrc/xnc_conv1.cu) vs an fp64
+    conv: TF32-rounded operands, f32 accumulation over 363 terms.  Tolerance: 2e-3
+    max-norm relative (TF32 keeps 10 mantissa bits; measured ~3e-4), and no worse
+    than 2x cuDNN's own TF32 error on the same data.  Batches 5 / 37 put pair tiles
+    across image boundaries (tiles are linear over the batch)."""
+    from paper_2007_14178_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(batch)
+    x = torch.rand((batch, 3, 224, 224), device="cuda", generator=g) * 2 - 1
+    w = (torch.rand((96, 3, 11, 11), device="cuda", generator=g) * 2 - 1) * (3 * 121) ** -0.5
+    y = ops.conv1_forward(x, ops.conv1_pack_weights(w))
+    assert y.is_contiguous(memory_format=torch.channels_last) and y.shape == (batch, 96, 55, 55)
+    ref = F.conv2d(x.double(), w.double(), stride=4, padding=2)
+    err = ((y.double() - ref).abs().max() / ref.abs().max()).item()
+    saved = torch.backends.cudnn.allow_tf32
+    torch.backends.cudnn.allow_tf32 = True
+    try:
+        cud = F.conv2d(x, w, stride=4, padding=2)
+    finally:
+        torch.backends.cudnn.allow_tf32 = saved
+    err_cudnn = ((cud.double() - ref).abs().max() / ref.abs().max()).item()
+    assert err <= 2e-3 and err <= 2 * err_cudnn + 1e-6, (err, err_cudnn)
+
+
+def test_network_front_end_engines_agree():
+    """front_end on the tcgen05 conv1 vs the s2d + cuDNN path: both TF32, same layer."""
+    from paper_2007_14178_b200.network import XnorNetAlexNet
+    torch.manual_seed(1)
+    x = torch.rand((4, 3, 224, 224), device="cuda") * 2 - 1
+    a = XnorNetAlexNet("cuda", seed=2, conv1="tcgen05").front_end(x)
+    b = XnorNetAlexNet("cuda", seed=2, conv1="cudnn").front_end(x)
+    assert a.shape == b.shape == (4, 96, 27, 27)
+    assert ((a - b).abs().max() / b.abs().max()).item() <= 4e-3
