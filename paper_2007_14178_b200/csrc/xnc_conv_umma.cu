@@ -221,9 +221,6 @@ struct PairGeom {
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
   int cst_O;    // > 0: sw / alpha staged in shared memory (cst_O entries each, after the B ring)
-  int stages;      // B ring stages in use (<= kPStages; fewer when the bulk staging needs the room)
-  int bulk;        // 1: the float epilogue stages each warp's 16 x 32 chunk in shared memory and
-                   // writes it with bulk copies of aligned row segments (IC and W' multiples of 4)
   int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
                    // epilogue carries a pixel's running |.| sum and sign words across the blocks)
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
@@ -276,11 +273,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
   uint8_t* b_s = a_s + (size_t)g.NA * g.plane_bytes;     // stages x NP/2 rows x 128 B
-  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)g.stages * kPCPS * g.b_half_bytes);  // [cst_O]
+  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)kPStages * kPCPS * g.b_half_bytes);  // [cst_O]
   float* al_s = reinterpret_cast<float*>(sw_s + g.cst_O);                                           // [cst_O]
   float* sc_s = al_s + g.cst_O;  // out affine scale (1 when none)                                   // [cst_O]
   float* sh_s = sc_s + g.cst_O;  // out affine shift (0 when none)                                   // [cst_O]
-  float* stg_s = sh_s + g.cst_O;  // bulk epilogue staging: [epilogue warp][MH][16 filters][32 px]
   __shared__ __align__(8) uint64_t b_full[kPStages], b_empty[kPStages];
   __shared__ __align__(8) uint64_t a_full[kPMaxA], a_empty[kPMaxA];
   __shared__ __align__(8) uint64_t t_full[2], t_empty[2];
@@ -300,6 +296,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], 2 * kPEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();  // barrier inits complete before any role starts (and before the TMEM alloc)
   if (warp == 0 && lane == 0)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&b_map)) : "memory");
   if (warp == 3) {
@@ -322,7 +319,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
       const int my_units = units_of(g, cluster, n_clusters);
       const uint32_t total = (uint32_t)my_units * g.KBu * g.taps;
-      const uint32_t n_st = (uint32_t)g.stages;
       uint32_t step = 0;
       for (int iu = 0;; ++iu) {
         const int u = unit_at(g, cluster, n_clusters, iu);
@@ -330,12 +326,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         const int nb = (u / g.S) % g.n_nb, kbu0 = (u % g.S) * g.KBu;
           for (int kb = kbu0; kb < kbu0 + g.KBu; ++kb)
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
-              const uint32_t sidx = step / kPCPS, st = sidx % n_st, j = step % kPCPS;
+              const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
               if (j == 0) {
-                if (sidx >= n_st) mbar_wait_prof(&b_empty[st], ((sidx / n_st) - 1) & 1, prof, w_be, XNC_PROD_HINT);
+                if (sidx >= kPStages) mbar_wait_prof(&b_empty[st], ((sidx / kPStages) - 1) & 1, prof, w_be, XNC_PROD_HINT);
                 const uint32_t n_in = min((uint32_t)kPCPS, total - step);
-                if ((dbg & 256) && sidx >= n_st) break;  // profiling: no B protocol after the fill
-                if ((dbg & 2) && sidx >= n_st) {  // profiling: reuse resident chunks, no traffic
+                if ((dbg & 256) && sidx >= kPStages) break;  // profiling: no B protocol after the fill
+                if ((dbg & 2) && sidx >= kPStages) {  // profiling: reuse resident chunks, no traffic
                   if (leader) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&b_full[st])) : "memory");
                   step += kPCPS - 1 - j;
                   tap += kPCPS - 1;
@@ -499,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           int kx = 0;
           for (int tap = 0; tap < g.taps; ++tap, ++step) {
             const unsigned long long tw0 = trace ? clock64() : 0ull;
-            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)g.stages);
+            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)kPStages);
             if (j == 0 && b_proto) {
               mbar_wait_prof(&b_full[st], ph, prof, w_bf);
               asm volatile("tcgen05.fence::after_thread_sync;");
@@ -518,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               if (b_proto) umma_commit_pair_elect(&b_empty[st]);
               j = 0;
               ++stages;
-              if (++st == (uint32_t)g.stages) { st = 0; ph ^= 1u; }
+              if (++st == (uint32_t)kPStages) { st = 0; ph ^= 1u; }
             }
           }
           if (!g.a_unit) umma_commit_pair_elect(&a_empty[sl]);
@@ -574,12 +570,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       }
       named_bar_sync(6, 32 * kPEpiWarps);
     }
-    // staged bulk-store epilogue (g.bulk): lane (jf, sg) copies row segment sg of filter
-    // jf of the warp's 32 pixels; set up once per unit, issued once per chunk
-    const bool bulk = fast && g.bulk;
-    const uint64_t bulk_pol = bulk ? l2_evict_first_policy() : 0ull;
-    const uint32_t stg_warp = smem_addr(stg_s) + (uint32_t)(e_w * MH * 2048);
-    const int jf = lane & 15, sg = lane >> 4;
     float emit_sA[MH];  // sign-emitting epilogue: running |.| sum of each pixel across filter blocks
 #pragma unroll
     for (int h = 0; h < MH; ++h) emit_sA[h] = 0.0f;
@@ -777,46 +767,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           }
           continue;
         }
-        if (bulk && obase + 16 <= g.O) {
-          // staged: one STS per output (immediate offsets), then one bulk copy per lane
-          bulk_wait_read0();  // this lane's previous copies have read the staging buffer
-          __syncwarp();
-#pragma unroll
-          for (int h = 0; h < MH; ++h) {
-            float* stp = stg_s + (e_w * MH + h) * 512 + lane;  // [16 filters][32 px]
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
-              if (out_scale != nullptr) {
-                const float sc = g.cst_O > 0 ? sc_s[obase + j] : __ldg(out_scale + obase + j);
-                const float sh = g.cst_O > 0 ? sh_s[obase + j] : __ldg(out_shift + obase + j);
-                val = __fadd_rn(__fmul_rn(val, sc), sh);
-              }
-              stp[j * 32] = val;
-            }
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          // the warp's 32 extended pixels e0 .. e0+31 of row block h are at most two
-          // output row segments (IC >= 32); with IC, W' and e0 multiples of 4 both start
-          // and end on 16-byte boundaries (host-checked).  Lane (jf, sg) copies segment
-          // sg of filter obase + jf.
-#pragma unroll
-          for (int h = 0; h < MH; ++h) {
-            const int e0 = m0 + h * 128 + quad * 32;
-            const int r0 = e0 / g.IC, c0 = e0 - r0 * g.IC;
-            const int rr = r0 + sg, cc = sg ? 0 : c0, off = sg ? g.IC - c0 : 0;
-            int len = sg ? (c0 + 32 > g.IC ? min(c0 + 32 - g.IC, g.ow) : 0) : min(c0 + 32, g.ow) - c0;
-            if (rr >= g.oh) len = 0;
-            const int o = obase + jf;
-            float* dst = y + (size_t)n * g.O * plane_out + (size_t)(o * plane_out32 + rr * g.ow + cc);
-            bulk_store_pred(dst, stg_warp + (uint32_t)(h * 2048 + jf * 128 + off * 4), (uint32_t)len * 4u,
-                            bulk_pol, len > 0);
-          }
-          bulk_commit();
-          if (prof) w_st += clock64() - tc1;
-          continue;
-        }
         if (fast && obase + 16 <= g.O) {
           // hot path: float output only, all 16 filters valid (IADD3, I2F, 2 FMUL,
           // address, predicated STG per output); the optional per-filter affine
@@ -889,7 +839,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(t_empty0 + buf * 8);
     }
-    if (bulk) bulk_wait_all();  // the staging buffers stay valid until the copies land
     if (prof) {
       g_umma_prof[blockIdx.x][5] = clock64() - t_start;
       g_umma_prof[blockIdx.x][6] = w_tf;
@@ -978,14 +927,10 @@ int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int
 }
 
 static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int pad, int MH, PairGeom& g,
-                         size_t& smem, int S = 1, bool bulk = false, int stages = kPStages) {
-  g.stages = stages;
+                         size_t& smem, int S = 1) {
   g.C = C; g.H = H; g.W = W; g.O = O; g.kh = kh; g.kw = kw; g.pad = pad; g.MH = MH;
   g.oh = H + 2 * pad - kh + 1; g.ow = W + 2 * pad - kw + 1;
-  // bulk epilogue: the extended row padded to a multiple of 4 pixels (the extra
-  // columns are zero-padding pixels whose outputs are discarded, like the last kw-1)
-  g.IC = bulk ? round_up(W + 2 * pad, 4) : W + 2 * pad;
-  g.bulk = bulk ? 1 : 0;
+  g.IC = W + 2 * pad;
   g.KBn = cdiv(C, 128);
   g.Cw = cdiv(C, 32);
   g.NP = pair_np(O);
@@ -1007,8 +952,7 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   // its per-chunk constant loads were L1/L2 misses under the store stream (ncu: the
   // first use after them was the epilogue's top stall, 12 % of samples)
   g.cst_O = O <= 1024 ? round_up(O, 16) : 0;
-  const size_t b_bytes = (size_t)g.stages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 16 +
-                         (bulk ? (size_t)kPEpiWarps * MH * 2048 : 0);
+  const size_t b_bytes = (size_t)kPStages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 16;
   // A plane ring: two units' planes when they fit (the next unit's planes are
   // built during this unit's MMAs), else fewer; long K (fully connected layers
   // viewed as 1 x N images) streams through the ring.
@@ -1028,34 +972,12 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
 // K step), 1 for wider ones; fall back to MH = 1 when the rows do not fit shared
 // memory.  XNC_UMMA_MH overrides (tuning knob).
 static bool pair_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad, PairGeom& g, size_t& smem,
-                      int S = 1, bool bulk = false) {
+                      int S = 1) {
   static const int mh_env = getenv("XNC_UMMA_MH") ? atoi(getenv("XNC_UMMA_MH")) : 0;
   int mh = pair_np(O) > 128 ? 1 : 2;
   if (mh_env == 1 || (mh_env == 2 && pair_np(O) <= 128)) mh = mh_env;
   for (; mh >= 1; mh /= 2)
-    if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem, S, bulk)) return true;
-  return false;
-}
-
-// The staged bulk-store epilogue for a plain float output (no acc / split / emitted
-// signs): when W' is a multiple of 4, y is 16-byte aligned, the padded extended row
-// is >= 32 pixels and the staging buffers fit beside the same MH / A ring plan.
-// XNC_UMMA_BULK=0 turns it off (A/B runs).
-static bool bulk_plan(const PairGeom& g0, int N, int C, int H, int W, int O, int kh, int kw, int pad,
-                      const float* y, PairGeom& g, size_t& smem) {
-  static const int env = getenv("XNC_UMMA_BULK") ? atoi(getenv("XNC_UMMA_BULK")) : 1;
-  if (!env || (g0.ow & 3) || (reinterpret_cast<uintptr_t>(y) & 15) || round_up(W + 2 * pad, 4) < 32) return false;
-  // the staging buffers may take up to two B stages (deeper rings measured no faster
-  // once the A producers are latency-tolerant)
-  for (int st = kPStages; st >= kPStages - 2 && st >= 3; --st) {
-    PairGeom gb;
-    size_t sb;
-    if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, g0.MH, gb, sb, 1, true, st) && gb.NA >= g0.NA) {
-      g = gb;
-      smem = sb;
-      return true;
-    }
-  }
+    if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem, S)) return true;
   return false;
 }
 
@@ -1171,12 +1093,6 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   int32_t* part = g.S > 1 && (long)N * O * g.oh * g.ow < 0x7fffffffL ? split_ws : nullptr;
   if (g.S > 1 && part == nullptr) {  // no buffer usable: run unsplit
     if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
-  }
-  if (y != nullptr && acc == nullptr && next_bits == nullptr && part == nullptr && g.S == 1 &&
-      bulk_plan(g, N, C, H, W, O, kh, kw, pad, y, g, smem)) {
-    static const int dbg = getenv("XNC_UMMA_DEBUG") ? atoi(getenv("XNC_UMMA_DEBUG")) : 0;
-    g.debug = dbg;
-    if (int rc = smem_opt_in(kern, smem)) return rc;
   }
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
   g.tile_major = next_bits != nullptr && g.n_nb > 1;

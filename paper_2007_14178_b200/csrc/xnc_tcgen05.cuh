@@ -139,32 +139,10 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]
       : "r"(addr));
 }
 
-// ---- staged epilogue stores: registers -> shared memory -> bulk async copies
-// (cp.async.bulk, the TMA engine's non-tensor form) of whole 16-byte-aligned output
-// row segments.  Each output costs one STS with an immediate offset instead of a
-// 64-bit address computation and a predicated STG.
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
+// generic-proxy shared-memory writes -> visible to the async proxy (tensor core, TMA)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// bytes (a multiple of 16, 16-byte aligned src and dst) shared::cta -> global, in
-// this thread's bulk group; pred = 0: nothing issued
-__device__ __forceinline__ void bulk_store_pred(float* dst, uint32_t src, uint32_t bytes, uint64_t pol, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
-      "@q cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %4;\n\t}" ::"l"(dst),
-      "r"(src), "r"(bytes), "r"((int)pred), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// this thread's bulk copies have finished READING shared memory (the buffer may be rewritten)
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),

@@ -13,9 +13,9 @@ out=gpurun_out
 mkdir -p $out
 for t in $tools; do
   extra="--print-limit 100"
-  [ "$t" = "memcheck" ] && extra="--print-limit 100 --leak-check full --padding 32"
+  [ "$t" = "memcheck" ] && extra="--print-limit 100 --padding 32"
   [ "$t" = "racecheck" ] && extra="--print-limit 0 --racecheck-report hazard"
-  timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool $t $extra --kernel-name regex=xnc \
+  timeout ${SAN_TIMEOUT:-1200} /usr/local/cuda/bin/compute-sanitizer --tool $t $extra --kernel-name regex=xnc \
       --target-processes application-only python tools/sanitize_cases.py > $out/sanitize_${t}_${tag}.log 2>&1
   rc=$?
   echo "$t rc=$rc $(grep -h 'SUMMARY' $out/sanitize_${t}_${tag}.log | tail -1) cases_ok=$(grep -c ': ok' $out/sanitize_${t}_${tag}.log)"

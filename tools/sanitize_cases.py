@@ -3,7 +3,7 @@
 kernel, so a run that the tool slows down still proves the results.
 
     compute-sanitizer --tool racecheck --kernel-name regex=xnc python tools/sanitize_cases.py [group ...]
-groups: pack scale popc b1mma umma umma_bulk umma_emit umma_split network interop verify (default: all)
+groups: pack scale popc b1mma umma umma_bulk umma_emit umma_split network conv1 interop verify (default: all)
 """
 import os
 import sys
@@ -67,7 +67,7 @@ def case_umma(rng):
 
 
 def case_umma_bulk(rng):
-    # float output only, W' % 4 == 0: the staged bulk-store epilogue (MH = 2 and MH = 1)
+    # float output only (the plain fast epilogue), MH = 2 and MH = 1
     for (N, C, H, W, O_, k) in ((2, 128, 12, 32, 128, 3), (1, 256, 8, 36, 256, 3)):
         x, w = O.f32_exact(rng, (N, C, H, W)), O.f32_exact(rng, (O_, C, k, k))
         layer, xd = _layer(x, w, 1, "umma")
@@ -104,6 +104,16 @@ def case_network(rng):
     ops.max_pool(xc, 3, 2)
     ops.pack_input(xc)
     torch.cuda.synchronize()
+
+
+def case_conv1(rng):
+    # the network's TF32 conv1 on the tensor cores vs an fp64 conv (TF32 tolerance)
+    import torch.nn.functional as F
+    x = torch.from_numpy(O.f32_exact(rng, (3, 3, 224, 224))).cuda()
+    w = torch.from_numpy(O.f32_exact(rng, (96, 3, 11, 11)) * 0.05).cuda()
+    y = ops.conv1_forward(x, ops.conv1_pack_weights(w))
+    ref = F.conv2d(x.double(), w.double(), stride=4, padding=2)
+    assert ((y.double() - ref).abs().max() / ref.abs().max()).item() < 2e-3
 
 
 def case_interop(rng):
