@@ -162,44 +162,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
       }
       uint8_t* plane = a_s + buf * kC1Plane;
       const long m0 = (long)t * 256 + (long)rank * 128;  // this CTA's first extended pixel
-      constexpr int kItems = 3 * 256;                    // (c, p) with p < 256; p >= kC1P idle
-      for (int i0 = 0; i0 < kItems; i0 += 2 * n_pt) {
-        float2 v[2][8];
-        int cs[2], ps[2];
+      // every (c, p) item of the tile is loaded before any is converted: all of a
+      // thread's 8-byte loads (4 items x 4 rows x 2) are in flight at once, one memory
+      // latency per tile (a two-item batch loop waited out two and the producers, not
+      // the tensor core, set the pace)
+      constexpr int kItems = 3 * 256;  // (c, p) with p < 256; p >= kC1P idle
+      constexpr int kPer = (kItems + kC1ProdWarps * 32 - 1) / (kC1ProdWarps * 32);
+      float2 v[kPer][8];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int idx = i0 + k * n_pt + pt;
-          const int c = idx >> 8, p = idx & 255;
-          cs[k] = c;
-          ps[k] = p;
-          const long e = m0 + p;
-          const long img = e / kC1Ext;
-          const int r = (int)(e - img * kC1Ext);
-          const int Y = r / kC1SG, X = r - (r / kC1SG) * kC1SG;
-          const bool live = idx < kItems && p < kC1P && img < N;
-          const float* xc = x + ((size_t)(live ? img : 0) * 3 + (live ? c : 0)) * (kC1In * kC1In);
+      for (int k = 0; k < kPer; ++k) {
+        const int idx = k * n_pt + pt;
+        const int c = idx >> 8, p = idx & 255;
+        const long e = m0 + p;
+        const long img = e / kC1Ext;
+        const int r = (int)(e - img * kC1Ext);
+        const int Y = r / kC1SG, X = r - (r / kC1SG) * kC1SG;
+        const bool live = idx < kItems && p < kC1P && img < N;
+        const float* xc = x + ((size_t)(live ? img : 0) * 3 + (live ? c : 0)) * (kC1In * kC1In);
 #pragma unroll
-          for (int dy = 0; dy < 4; ++dy) {
-            const int row = 4 * Y + dy - 2;
-            const bool rok = live && row >= 0 && row < kC1In;
-            const float* src = xc + (size_t)(rok ? row : 0) * kC1In + 4 * X;
-            v[k][2 * dy] = (rok && X >= 1) ? __ldg(reinterpret_cast<const float2*>(src - 2)) : make_float2(0.f, 0.f);
-            v[k][2 * dy + 1] = (rok && X < kC1SG - 1) ? __ldg(reinterpret_cast<const float2*>(src))
-                                                      : make_float2(0.f, 0.f);
-          }
+        for (int dy = 0; dy < 4; ++dy) {
+          const int row = 4 * Y + dy - 2;
+          const bool rok = live && row >= 0 && row < kC1In;
+          const float* src = xc + (size_t)(rok ? row : 0) * kC1In + 4 * X;
+          v[k][2 * dy] = (rok && X >= 1) ? __ldg(reinterpret_cast<const float2*>(src - 2)) : make_float2(0.f, 0.f);
+          v[k][2 * dy + 1] = (rok && X < kC1SG - 1) ? __ldg(reinterpret_cast<const float2*>(src))
+                                                    : make_float2(0.f, 0.f);
         }
+      }
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int idx = i0 + k * n_pt + pt;
-          if (idx >= kItems || ps[k] >= kC1P) continue;
-          const int p = ps[k];
-          uint8_t* row = plane + cs[k] * kC1Sub + p * 64;
+      for (int k = 0; k < kPer; ++k) {
+        const int idx = k * n_pt + pt;
+        const int c = idx >> 8, p = idx & 255;
+        if (idx >= kItems || p >= kC1P) continue;
+        uint8_t* row = plane + c * kC1Sub + p * 64;
 #pragma unroll
-          for (int dy = 0; dy < 4; ++dy) {
-            const float4 q = make_float4(to_tf32(v[k][2 * dy].x), to_tf32(v[k][2 * dy].y),
-                                         to_tf32(v[k][2 * dy + 1].x), to_tf32(v[k][2 * dy + 1].y));
-            *reinterpret_cast<float4*>(row + ((dy ^ ((p >> 1) & 3)) << 4)) = q;  // SWIZZLE_64B
-          }
+        for (int dy = 0; dy < 4; ++dy) {
+          const float4 q4 = make_float4(to_tf32(v[k][2 * dy].x), to_tf32(v[k][2 * dy].y),
+                                        to_tf32(v[k][2 * dy + 1].x), to_tf32(v[k][2 * dy + 1].y));
+          *reinterpret_cast<float4*>(row + ((dy ^ ((p >> 1) & 3)) << 4)) = q4;  // SWIZZLE_64B
         }
       }
       fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
