@@ -282,16 +282,21 @@ __global__ void __launch_bounds__(128) k_pack_small(const float* __restrict__ x,
 // order; the folded BN, if any, is applied by the loading lanes, the same two
 // roundings).
 constexpr int kAbsChunk = 1024;
+constexpr int kAbsWideMax = 4096;  // channels staged whole per warp (16 KB)
 __global__ void __launch_bounds__(128) k_absmean_wide(const float* __restrict__ x, int C, long npix, float inv,
                                                       float* __restrict__ A, const float* __restrict__ in_scale,
                                                       const float* __restrict__ in_shift) {
-  __shared__ __align__(16) float buf[4][kAbsChunk];
+  // The pixel's whole channel vector is staged first (all lanes' loads, chunk after
+  // chunk, no chain in between), then lane 0 runs the one sequential chain with its
+  // shared-memory reads a batch ahead.  Interleaving per 1024-channel chunk made
+  // the warp wait out a load latency per chunk on top of the chain (ncu: 70 %
+  // long-scoreboard stalls, 50 us for fc7's 256 x 4096 input).
+  extern __shared__ __align__(16) float absw_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long q = (long)blockIdx.x * 4 + warp;
   if (q >= npix) return;
   const float* xp = x + q * C;
-  float* b = buf[warp];
-  float s = 0.0f;
+  float* b = absw_smem + (size_t)warp * C;
   for (int c0 = 0; c0 < C; c0 += kAbsChunk) {
     const int n = min(kAbsChunk, C - c0);
     float v[kAbsChunk / 32];
@@ -300,36 +305,34 @@ __global__ void __launch_bounds__(128) k_absmean_wide(const float* __restrict__ 
       const int c = u * 32 + lane;
       v[u] = c < n ? fabsf(affine_in(__ldg(xp + c0 + c), in_scale, in_shift, c0 + c)) : 0.0f;
     }
-    __syncwarp();  // lane 0 is done with the previous chunk
 #pragma unroll
-    for (int u = 0; u < kAbsChunk / 32; ++u) b[u * 32 + lane] = v[u];
-    __syncwarp();
-    if (lane == 0) {
-      // the chain is one FADD per channel (4 cycles); shared-memory reads are
-      // batched 32 channels ahead (8 x LDS.128 of the next batch issued before the
-      // adds of this one), else every add waits out an LDS latency (~25 cycles)
-      const float4* b4 = reinterpret_cast<const float4*>(b);
-      const int nb = n >> 5;  // whole 32-channel batches
-      float4 cur[8], nxt[8];
-      if (nb > 0) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) cur[u] = b4[u];
-      }
-      for (int k = 0; k < nb; ++k) {
-        if (k + 1 < nb) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) nxt[u] = b4[(k + 1) * 8 + u];
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, cur[u].x), cur[u].y), cur[u].z), cur[u].w);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
-      }
-      for (int i = nb << 5; i < n; ++i) s = __fadd_rn(s, b[i]);
-    }
+    for (int u = 0; u < kAbsChunk / 32; ++u)
+      if (u * 32 + lane < n) b[c0 + u * 32 + lane] = v[u];
   }
-  if (lane == 0) A[q] = __fmul_rn(s, inv);
+  __syncwarp();
+  if (lane == 0) {
+    float s = 0.0f;
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    const int nb = C >> 5;  // whole 32-channel batches
+    float4 cur[8], nxt[8];
+    if (nb > 0) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cur[u] = b4[u];
+    }
+    for (int k = 0; k < nb; ++k) {
+      if (k + 1 < nb) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nxt[u] = b4[(k + 1) * 8 + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, cur[u].x), cur[u].y), cur[u].z), cur[u].w);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+    }
+    for (int i = nb << 5; i < C; ++i) s = __fadd_rn(s, b[i]);
+    A[q] = __fmul_rn(s, inv);
+  }
 }
 
 // The two-kernel form of K1 (sign words, then the sequential |.| means): no shared
@@ -341,9 +344,12 @@ static int launch_pack_2d(const float* x, int N, int C, int H, int W, uint32_t* 
   const int Cw = cdiv(C, 32);
   const long words = npix * Cw;
   k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, in_scale, in_shift);
-  if (A && H * W == 1 && C >= 1024)
-    k_absmean_wide<<<(unsigned)cdivl(npix, 4), 128, 0, s>>>(x, C, npix, (float)(1.0 / (double)C), A, in_scale,
-                                                            in_shift);
+  if (A && H * W == 1 && C >= 1024 && C <= kAbsWideMax && (C & 3) == 0) {
+    const size_t sm = (size_t)4 * C * sizeof(float);
+    if (int rc = smem_opt_in(k_absmean_wide, sm)) return rc;  // per device (xnc_runtime.cu)
+    k_absmean_wide<<<(unsigned)cdivl(npix, 4), 128, sm, s>>>(x, C, npix, (float)(1.0 / (double)C), A, in_scale,
+                                                             in_shift);
+  }
   else if (A)
     k_absmean<<<(unsigned)cdivl(npix, 128), 128, 0, s>>>(x, C, H * W, npix, (float)(1.0 / (double)C), A,
                                                          in_scale, in_shift);

@@ -133,7 +133,7 @@ def test_pack_input_bits_and_absmean(C, HW):
         assert np.array_equal(A[n].cpu().numpy().view(np.uint32), A_ref.view(np.uint32))
 
 
-@pytest.mark.parametrize("C", [1024, 2500, 4096])
+@pytest.mark.parametrize("C", [1024, 1030, 2500, 4096, 6000])
 def test_pack_input_long_channel_vectors(C):
     """1x1 images with long channel vectors (the fc7 input): A from the warp-per-pixel
     kernel is the oracle's sequential f32 sum, bit for bit; bits exact."""
