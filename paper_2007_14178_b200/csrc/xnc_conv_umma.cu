@@ -197,12 +197,6 @@ __device__ __forceinline__ void st_cs_pred_v2(const float* p, float a, float b, 
                : "memory");
 }
 
-__device__ __forceinline__ void st_cs_pred_v4(const float* p, float4 v, bool pred) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global" XNC_ST_HINT ".v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
-               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"((int)pred)
-               : "memory");
-}
-
 // streaming (evict-first) store, predicated without a branch
 __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global" XNC_ST_HINT ".f32 [%0], %1;\n\t}" ::"l"(p),
@@ -227,9 +221,6 @@ struct PairGeom {
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
   int cst_O;    // > 0: sw / alpha staged in shared memory (cst_O entries each, after the B ring)
-  int stages;      // B ring stages in use (<= kPStages; one fewer when the v4 staging needs the room)
-  int v4;          // 1: the float epilogue transposes each warp's 16 filters x 32 pixels through
-                   // shared memory and stores 16-byte runs of 4 pixels (IC and W' multiples of 4)
   int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
                    // epilogue carries a pixel's running |.| sum and sign words across the blocks)
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
@@ -282,11 +273,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
   uint8_t* b_s = a_s + (size_t)g.NA * g.plane_bytes;     // stages x NP/2 rows x 128 B
-  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)g.stages * kPCPS * g.b_half_bytes);  // [cst_O]
+  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)kPStages * kPCPS * g.b_half_bytes);  // [cst_O]
   float* al_s = reinterpret_cast<float*>(sw_s + g.cst_O);                                           // [cst_O]
   float* sc_s = al_s + g.cst_O;  // out affine scale (1 when none)                                   // [cst_O]
   float* sh_s = sc_s + g.cst_O;  // out affine shift (0 when none)                                   // [cst_O]
-  float* stg_s = sh_s + g.cst_O;  // v4 epilogue staging: [epilogue warp][MH][16 filters][32 px]
   __shared__ __align__(8) uint64_t b_full[kPStages], b_empty[kPStages];
   __shared__ __align__(8) uint64_t a_full[kPMaxA], a_empty[kPMaxA];
   __shared__ __align__(8) uint64_t t_full[2], t_empty[2];
@@ -329,7 +319,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
       const int my_units = units_of(g, cluster, n_clusters);
       const uint32_t total = (uint32_t)my_units * g.KBu * g.taps;
-      const uint32_t n_st = (uint32_t)g.stages;
       uint32_t step = 0;
       for (int iu = 0;; ++iu) {
         const int u = unit_at(g, cluster, n_clusters, iu);
@@ -337,12 +326,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         const int nb = (u / g.S) % g.n_nb, kbu0 = (u % g.S) * g.KBu;
           for (int kb = kbu0; kb < kbu0 + g.KBu; ++kb)
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
-              const uint32_t sidx = step / kPCPS, st = sidx % n_st, j = step % kPCPS;
+              const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
               if (j == 0) {
-                if (sidx >= n_st) mbar_wait_prof(&b_empty[st], ((sidx / n_st) - 1) & 1, prof, w_be, XNC_PROD_HINT);
+                if (sidx >= kPStages) mbar_wait_prof(&b_empty[st], ((sidx / kPStages) - 1) & 1, prof, w_be, XNC_PROD_HINT);
                 const uint32_t n_in = min((uint32_t)kPCPS, total - step);
-                if ((dbg & 256) && sidx >= n_st) break;  // profiling: no B protocol after the fill
-                if ((dbg & 2) && sidx >= n_st) {  // profiling: reuse resident chunks, no traffic
+                if ((dbg & 256) && sidx >= kPStages) break;  // profiling: no B protocol after the fill
+                if ((dbg & 2) && sidx >= kPStages) {  // profiling: reuse resident chunks, no traffic
                   if (leader) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&b_full[st])) : "memory");
                   step += kPCPS - 1 - j;
                   tap += kPCPS - 1;
@@ -506,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           int kx = 0;
           for (int tap = 0; tap < g.taps; ++tap, ++step) {
             const unsigned long long tw0 = trace ? clock64() : 0ull;
-            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)g.stages);
+            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)kPStages);
             if (j == 0 && b_proto) {
               mbar_wait_prof(&b_full[st], ph, prof, w_bf);
               asm volatile("tcgen05.fence::after_thread_sync;");
@@ -525,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               if (b_proto) umma_commit_pair_elect(&b_empty[st]);
               j = 0;
               ++stages;
-              if (++st == (uint32_t)g.stages) { st = 0; ph ^= 1u; }
+              if (++st == (uint32_t)kPStages) { st = 0; ph ^= 1u; }
             }
           }
           if (!g.a_unit) umma_commit_pair_elect(&a_empty[sl]);
@@ -581,11 +570,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       }
       named_bar_sync(6, 32 * kPEpiWarps);
     }
-    // v4 epilogue (g.v4): after the transpose lane L owns pixels 4*(L & 7) .. +3 of the
-    // warp's 32 and filters (L >> 3) + 4k of the chunk, k = 0..3
-    const bool v4 = fast && g.v4;
-    float* stg_w = stg_s + e_w * MH * 512;
-    const int g4 = lane & 7, f4 = lane >> 3;
     float emit_sA[MH];  // sign-emitting epilogue: running |.| sum of each pixel across filter blocks
 #pragma unroll
     for (int h = 0; h < MH; ++h) emit_sA[h] = 0.0f;
@@ -606,19 +590,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         qix[h] = (size_t)n * plane_out + (size_t)rr * g.ow + cc;  // output pixel (n, rr, cc)
         pix[h] = (size_t)n * g.O * plane_out + (size_t)rr * g.ow + cc;
         kv[h] = (ok[h] && (y || next_bits)) ? __ldg(Kmap + qix[h]) : 0.0f;
-      }
-      // v4: this lane's 4-pixel group of each row block -- whole groups are valid or not,
-      // and 16-byte aligned in y (IC, W' multiples of 4, host-checked)
-      int q4off[MH];
-      bool q4ok[MH];
-      if (v4) {
-#pragma unroll
-        for (int h = 0; h < MH; ++h) {
-          const int e = m0 + h * 128 + quad * 32 + 4 * g4;
-          const int rr = e / g.IC, cc = e - (e / g.IC) * g.IC;
-          q4ok[h] = rr < g.oh && cc < g.ow;
-          q4off[h] = q4ok[h] ? rr * g.ow + cc : 0;
-        }
       }
       const uint32_t buf = item & 1;
       mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
@@ -796,39 +767,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           }
           continue;
         }
-        if (v4 && obase + 16 <= g.O) {
-          // transpose through shared memory: one STS per output (immediate offsets), then
-          // per lane four 16-byte loads and stores of 4 consecutive pixels of one filter
-          // (a warp store covers 4 filters x 128 contiguous bytes)
-          __syncwarp();  // the previous chunk's reads of the staging rows are done
-#pragma unroll
-          for (int h = 0; h < MH; ++h) {
-            float* stp = stg_w + h * 512 + lane;  // [16 filters][32 px]
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
-              if (out_scale != nullptr) {
-                const float sc = g.cst_O > 0 ? sc_s[obase + j] : __ldg(out_scale + obase + j);
-                const float sh = g.cst_O > 0 ? sh_s[obase + j] : __ldg(out_shift + obase + j);
-                val = __fadd_rn(__fmul_rn(val, sc), sh);
-              }
-              stp[j * 32] = val;
-            }
-          }
-          __syncwarp();
-#pragma unroll
-          for (int h = 0; h < MH; ++h) {
-            const float* src = stg_w + h * 512 + f4 * 32 + 4 * g4;
-            float* dst = y + (size_t)n * g.O * plane_out + (size_t)(obase + f4) * plane_out + q4off[h];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float4 q = *reinterpret_cast<const float4*>(src + k * 128);
-              st_cs_pred_v4(dst + (size_t)k * 4 * plane_out, q, q4ok[h]);
-            }
-          }
-          if (prof) w_st += clock64() - tc1;
-          continue;
-        }
         if (fast && obase + 16 <= g.O) {
           // hot path: float output only, all 16 filters valid (IADD3, I2F, 2 FMUL,
           // address, predicated STG per output); the optional per-filter affine
@@ -989,14 +927,10 @@ int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int
 }
 
 static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int pad, int MH, PairGeom& g,
-                         size_t& smem, int S = 1, bool v4 = false, int stages = kPStages) {
+                         size_t& smem, int S = 1) {
   g.C = C; g.H = H; g.W = W; g.O = O; g.kh = kh; g.kw = kw; g.pad = pad; g.MH = MH;
   g.oh = H + 2 * pad - kh + 1; g.ow = W + 2 * pad - kw + 1;
-  // v4 epilogue: the extended row padded to a multiple of 4 pixels (the extra columns
-  // are zero-padding pixels whose outputs are discarded, like the last kw - 1)
-  g.IC = v4 ? round_up(W + 2 * pad, 4) : W + 2 * pad;
-  g.v4 = v4 ? 1 : 0;
-  g.stages = stages;
+  g.IC = W + 2 * pad;
   g.KBn = cdiv(C, 128);
   g.Cw = cdiv(C, 32);
   g.NP = pair_np(O);
@@ -1018,8 +952,7 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   // its per-chunk constant loads were L1/L2 misses under the store stream (ncu: the
   // first use after them was the epilogue's top stall, 12 % of samples)
   g.cst_O = O <= 1024 ? round_up(O, 16) : 0;
-  const size_t b_bytes = (size_t)g.stages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 16 +
-                         (v4 ? (size_t)kPEpiWarps * MH * 2048 : 0);
+  const size_t b_bytes = (size_t)kPStages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 16;
   // A plane ring: two units' planes when they fit (the next unit's planes are
   // built during this unit's MMAs), else fewer; long K (fully connected layers
   // viewed as 1 x N images) streams through the ring.
@@ -1045,26 +978,6 @@ static bool pair_plan(int N, int C, int H, int W, int O, int kh, int kw, int pad
   if (mh_env == 1 || (mh_env == 2 && pair_np(O) <= 128)) mh = mh_env;
   for (; mh >= 1; mh /= 2)
     if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, mh, g, smem, S)) return true;
-  return false;
-}
-
-// The v4 epilogue for a plain float output (no acc / split / emitted signs): when W'
-// is a multiple of 4 and y 16-byte aligned, with the same MH and A ring as the plain
-// plan and at most one B stage fewer (5 instead of 6 measured equal).
-// XNC_UMMA_V4=0 turns it off (A/B runs).
-static bool v4_plan(const PairGeom& g0, int N, int C, int H, int W, int O, int kh, int kw, int pad,
-                    const float* y, PairGeom& g, size_t& smem) {
-  static const int env = getenv("XNC_UMMA_V4") ? atoi(getenv("XNC_UMMA_V4")) : 1;
-  if (!env || (g0.ow & 3) || (reinterpret_cast<uintptr_t>(y) & 15)) return false;
-  for (int st = kPStages; st >= kPStages - 1; --st) {
-    PairGeom gb;
-    size_t sb;
-    if (pair_plan_mh(N, C, H, W, O, kh, kw, pad, g0.MH, gb, sb, 1, true, st) && gb.NA >= g0.NA) {
-      g = gb;
-      smem = sb;
-      return true;
-    }
-  }
   return false;
 }
 
@@ -1180,13 +1093,6 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   int32_t* part = g.S > 1 && (long)N * O * g.oh * g.ow < 0x7fffffffL ? split_ws : nullptr;
   if (g.S > 1 && part == nullptr) {  // no buffer usable: run unsplit
     if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
-  }
-  if (y != nullptr && acc == nullptr && next_bits == nullptr && part == nullptr && g.S == 1) {
-    const int dbg = g.debug;
-    if (v4_plan(g, N, C, H, W, O, kh, kw, pad, y, g, smem)) {
-      g.debug = dbg;
-      if (int rc = smem_opt_in(kern, smem)) return rc;
-    }
   }
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
   g.tile_major = next_bits != nullptr && g.n_nb > 1;

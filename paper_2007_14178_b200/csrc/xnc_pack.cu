@@ -299,15 +299,26 @@ __global__ void __launch_bounds__(128) k_absmean_wide(const float* __restrict__ 
   float* b = absw_smem + (size_t)warp * C;
   for (int c0 = 0; c0 < C; c0 += kAbsChunk) {
     const int n = min(kAbsChunk, C - c0);
+    // the chunk's 32 loads per lane are all issued before any is used: with the
+    // optional affine's loads interleaved the compiler issued them one at a time and
+    // the warp waited out 32 load latencies per chunk (ncu: 70 % long-scoreboard
+    // stalls on the first use; 57 us for fc7's 256 x 4096 input)
     float v[kAbsChunk / 32];
 #pragma unroll
     for (int u = 0; u < kAbsChunk / 32; ++u) {
       const int c = u * 32 + lane;
-      v[u] = c < n ? fabsf(affine_in(__ldg(xp + c0 + c), in_scale, in_shift, c0 + c)) : 0.0f;
+      v[u] = c < n ? __ldg(xp + c0 + c) : 0.0f;
+    }
+    if (in_scale != nullptr) {
+#pragma unroll
+      for (int u = 0; u < kAbsChunk / 32; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (u * 32 + lane < n) v[u] = __fadd_rn(__fmul_rn(v[u], __ldg(in_scale + c)), __ldg(in_shift + c));
+      }
     }
 #pragma unroll
     for (int u = 0; u < kAbsChunk / 32; ++u)
-      if (u * 32 + lane < n) b[c0 + u * 32 + lane] = v[u];
+      if (u * 32 + lane < n) b[c0 + u * 32 + lane] = fabsf(v[u]);
   }
   __syncwarp();
   if (lane == 0) {
