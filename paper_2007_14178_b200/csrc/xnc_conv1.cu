@@ -19,8 +19,8 @@
 // stay inside one image (13 pair tiles of 256 cells per 57 x 57 image).
 //   warp 0      B (once: this CTA's 48 filter rows of all 27 (c, tap) blocks, TMA,
 //               SWIZZLE_64B), then the MMA issuer on the leader CTA
-//   warp 1      TMA of the raw rows a CTA tile reads (3 channels x 24 rows x 224,
-//               zero-filled outside the image) into a staging buffer; TMEM owner
+//   warp 1      TMA of the raw rows a CTA tile reads (24 rows x 224 per channel,
+//               zero-filled outside the image) through a 2-slot staging ring; TMEM owner
 //   warps 2-3, 8-11  A producers: staging -> TF32 (round to nearest) -> the tile's
 //               three 64-byte-row SWIZZLE_64B sub-planes (c = 0, 1, 2), 244 rows each
 //   warps 4-7   epilogue: TMEM -> registers -> y, one pixel per thread, its 96
@@ -50,8 +50,9 @@ constexpr int kC1BBlock = kC1Half * 64;     // one block, this CTA's rows (3,072
 constexpr int kC1BBytes = kC1Blocks * kC1BBlock;
 constexpr int kC1Tiles = (kC1Ext + 255) / 256;  // pair tiles per image (13)
 constexpr int kC1StRows = 24;               // raw rows a CTA tile spans: 6 cell rows x 4
-constexpr int kC1Stage = 3 * kC1StRows * kC1In * 4;  // 64,512 B
-constexpr int kC1Smem = kC1Plane + kC1BBytes + kC1Stage + 1024;
+constexpr int kC1Stage = kC1StRows * kC1In * 4;  // one channel's rows (21,504 B)
+constexpr int kC1Slots = 2;                       // staging ring
+constexpr int kC1Smem = 2 * kC1Plane + kC1BBytes + kC1Slots * kC1Stage + 1024;
 constexpr int kC1ProdWarps = 6;
 constexpr int kC1Threads = 12 * 32;
 constexpr int kC1TmemCols = 256;            // two 96-column accumulators
@@ -80,10 +81,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
                       float* __restrict__ y, int tiles) {
   extern __shared__ __align__(1024) uint8_t c1_smem_raw[];
   uint8_t* smem = c1_smem_raw + ((1024u - (smem_addr(c1_smem_raw) & 1023u)) & 1023u);
-  uint8_t* a_s = smem;                                   // one tile's 3 sub-planes
-  uint8_t* b_s = smem + kC1Plane;                        // 27 blocks x 48 rows x 64 B
-  float* st_s = reinterpret_cast<float*>(b_s + kC1BBytes);  // raw rows [3][24][224]
-  __shared__ __align__(8) uint64_t b_full, a_full, a_empty, s_full, s_empty, t_full[2], t_empty[2];
+  uint8_t* a_s = smem;                                   // two tiles x 3 sub-planes
+  uint8_t* b_s = smem + 2 * kC1Plane;                    // 27 blocks x 48 rows x 64 B
+  float* st_s = reinterpret_cast<float*>(b_s + kC1BBytes);  // raw rows ring [slot][24][224]
+  __shared__ __align__(8) uint64_t b_full, a_full[2], a_empty[2], s_full[kC1Slots], s_empty[kC1Slots],
+      t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -92,11 +94,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   if (tid == 0) {
     mbar_init(&b_full, 1);
-    mbar_init(&a_full, 2 * kC1ProdWarps);
-    mbar_init(&a_empty, 1);
-    mbar_init(&s_full, 1);
-    mbar_init(&s_empty, kC1ProdWarps);
+    for (int b = 0; b < kC1Slots; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], kC1ProdWarps);
+    }
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&a_full[b], 2 * kC1ProdWarps);
+      mbar_init(&a_empty[b], 1);
       mbar_init(&t_full[b], 1);
       mbar_init(&t_empty[b], 2 * 4);
     }
@@ -138,10 +142,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
           mbar_wait(&t_empty[buf], ((item >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
         }
-        mbar_wait(&a_full, item & 1);
+        mbar_wait(&a_full[buf], (item >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t d = tmem + buf * kC1N;
-        const uint32_t a_plane = a_lo0;
+        const uint32_t a_plane = a_lo0 + buf * (kC1Plane >> 4);
         uint32_t acc = 0;
 #pragma unroll 1
         for (int c = 0; c < 3; ++c) {
@@ -154,66 +158,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
             acc = 1;
           }
         }
-        umma_commit_pair_elect(&a_empty);
+        umma_commit_pair_elect(&a_empty[buf]);
         umma_commit_pair_elect(&t_full[buf]);
       }
     }
   } else if (warp == 1) {
-    // ---- raw-row TMA: rows 4*Y0 - 2 .. 4*Y0 + 21 of all 3 channels of the tile's image
+    // ---- raw-row TMA, one channel per slot: rows 4*Y0 - 2 .. 4*Y0 + 21 of channel c
     if (lane == 0) {
-      uint32_t item = 0;
-      for (int t = cluster; t < tiles; t += n_clusters, ++item) {
-        if (item >= 1) mbar_wait(&s_empty, (item - 1) & 1);
+      uint32_t use = 0;
+      for (int t = cluster; t < tiles; t += n_clusters) {
         const int img = t / kC1Tiles, e0 = (t - img * kC1Tiles) * 256 + (int)rank * 128;
         const int Y0 = e0 / kC1SG;
-        mbar_expect_tx(&s_full, (uint32_t)kC1Stage);
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_addr(st_s)),
-            "l"(reinterpret_cast<uint64_t>(&x_map)), "r"(0), "r"(4 * Y0 - 2), "r"(0), "r"(img),
-            "r"(smem_addr(&s_full))
-            : "memory");
+        for (int c = 0; c < 3; ++c, ++use) {
+          const uint32_t sl = use % kC1Slots;
+          if (use >= kC1Slots) mbar_wait(&s_empty[sl], ((use / kC1Slots) - 1) & 1);
+          mbar_expect_tx(&s_full[sl], (uint32_t)kC1Stage);
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_addr(st_s) + sl * kC1Stage),
+              "l"(reinterpret_cast<uint64_t>(&x_map)), "r"(0), "r"(4 * Y0 - 2), "r"(c), "r"(img),
+              "r"(smem_addr(&s_full[sl]))
+              : "memory");
+        }
       }
     }
   } else if (warp < 4 || warp >= 8) {
-    // ---- A producers: item (c, p) = raw channel c of plane row p, from the staged rows
+    // ---- A producers: row p of sub-plane c from the staged rows of channel c; a
+    // warp's lanes take consecutive rows (cells)
     const int pw = warp < 4 ? warp - 2 : warp - 6;
     const int pt = pw * 32 + lane, n_pt = kC1ProdWarps * 32;
-    const uint32_t full0 = map_to_rank(smem_addr(&a_full), 0);
-    uint32_t item = 0;
+    const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
+    uint32_t item = 0, use = 0;
     for (int t = cluster; t < tiles; t += n_clusters, ++item) {
+      const uint32_t buf = item & 1;
       const int img = t / kC1Tiles, e0 = (t - img * kC1Tiles) * 256 + (int)rank * 128;
       const int Y0 = e0 / kC1SG;
-      if (lane == 0) {
-        mbar_wait(&s_full, item & 1);                          // the tile's raw rows landed
-        if (item >= 1) mbar_wait(&a_empty, (item - 1) & 1);    // the previous tile's MMAs are done
+      if (item >= 2) {  // the MMAs of the tile two back (same A buffer) are done
+        if (lane == 0) mbar_wait(&a_empty[buf], ((item >> 1) - 1) & 1);
+        __syncwarp();
       }
-      __syncwarp();
-      constexpr int kItems = 3 * 256;  // (c, p) with p < 256; p >= kC1P idle
-      for (int idx = pt; idx < kItems; idx += n_pt) {
-        const int c = idx >> 8, p = idx & 255;
-        if (p >= kC1P) continue;
-        const int e = e0 + p;
-        const int Y = e / kC1SG, X = e - (e / kC1SG) * kC1SG;
-        const bool live = e < kC1Ext;
-        const float* src = st_s + ((size_t)c * kC1StRows + 4 * (Y - Y0)) * kC1In + 4 * X;
-        uint8_t* row = a_s + c * kC1Sub + p * 64;
+      uint8_t* plane = a_s + buf * kC1Plane;
+      for (int c = 0; c < 3; ++c, ++use) {
+        const uint32_t sl = use % kC1Slots;
+        if (lane == 0) mbar_wait(&s_full[sl], (use / kC1Slots) & 1);  // channel c's rows landed
+        __syncwarp();
+        const float* st = st_s + (size_t)sl * (kC1Stage / 4);
+        for (int p = pt; p < kC1P; p += n_pt) {
+          const int e = e0 + p;
+          const int Y = e / kC1SG, X = e - (e / kC1SG) * kC1SG;
+          const bool live = e < kC1Ext;
+          const float* src = st + (4 * (Y - Y0)) * kC1In + 4 * X;
+          uint8_t* row = plane + c * kC1Sub + p * 64;
 #pragma unroll
-        for (int dy = 0; dy < 4; ++dy) {
-          const float2 lo = (live && X >= 1) ? *reinterpret_cast<const float2*>(src + dy * kC1In - 2)
-                                             : make_float2(0.f, 0.f);
-          const float2 hi = (live && X < kC1SG - 1) ? *reinterpret_cast<const float2*>(src + dy * kC1In)
-                                                    : make_float2(0.f, 0.f);
-          const float4 q4 = make_float4(to_tf32(lo.x), to_tf32(lo.y), to_tf32(hi.x), to_tf32(hi.y));
-          *reinterpret_cast<float4*>(row + ((dy ^ ((p >> 1) & 3)) << 4)) = q4;  // SWIZZLE_64B
+          for (int dy = 0; dy < 4; ++dy) {
+            const float2 lo = (live && X >= 1) ? *reinterpret_cast<const float2*>(src + dy * kC1In - 2)
+                                               : make_float2(0.f, 0.f);
+            const float2 hi = (live && X < kC1SG - 1) ? *reinterpret_cast<const float2*>(src + dy * kC1In)
+                                                      : make_float2(0.f, 0.f);
+            const float4 q4 = make_float4(to_tf32(lo.x), to_tf32(lo.y), to_tf32(hi.x), to_tf32(hi.y));
+            *reinterpret_cast<float4*>(row + ((dy ^ ((p >> 1) & 3)) << 4)) = q4;  // SWIZZLE_64B
+          }
         }
+        __syncwarp();
+        if (lane == 0)  // this warp is done reading the slot
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&s_empty[sl])) : "memory");
       }
       fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_cluster(full0);                                          // A ready (leader)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&s_empty)) : "memory");
-      }
+      if (lane == 0) mbar_arrive_cluster(full0 + buf * 8);  // A ready (leader)
     }
   } else {
     // ---- epilogue: warp 4 + q reads TMEM lanes 32q .. 32q+31 (pixels), 96 columns
@@ -306,7 +318,7 @@ int xnc_conv1_forward(const float* x, int N, const float* wq, float* y, void* st
   {
     cuuint64_t xd[4] = {(cuuint64_t)kC1In, (cuuint64_t)kC1In, 3u, (cuuint64_t)N};
     cuuint64_t xs[3] = {(cuuint64_t)kC1In * 4, (cuuint64_t)kC1In * kC1In * 4, (cuuint64_t)3 * kC1In * kC1In * 4};
-    cuuint32_t xb[4] = {(cuuint32_t)kC1In, (cuuint32_t)kC1StRows, 3u, 1u};
+    cuuint32_t xb[4] = {(cuuint32_t)kC1In, (cuuint32_t)kC1StRows, 1u, 1u};
     cuuint32_t xe[4] = {1u, 1u, 1u, 1u};
     if (encode(&x_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), xd, xs, xb, xe,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
