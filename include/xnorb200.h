@@ -137,6 +137,14 @@ int xnc_plane_affine(float* y, int N, int O, long plane, const float* scale, con
  * nhwc != 0 (xnc_max_pool too): the map is stored channels-last, [N][H][W][C]. */
 int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, int r, int nhwc,
                            float* out, void* stream);
+/* K1 of max_pool(x) without materialising it: x f32 [N][C][Hin][Win] is the
+ * PRE-pool map; bits / A describe the pooled map [N][Ho][Wo] (Ho = (Hin - pool_k) /
+ * pool_s + 1), bit-identical to xnc_max_pool followed by xnc_pack_input_affine
+ * (in_scale / in_shift may be NULL).  Returns XNC_ENOTSUP for shapes the fused
+ * kernel does not take (pool_k != 3, fewer than 32 pooled pixels per image,
+ * C outside 32..768): pool, then pack. */
+int xnc_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s,
+                        const float* in_scale, const float* in_shift, uint32_t* bits, float* A, void* stream);
 /* K1 (xnc_pack_input_affine) for a channels-last input x f32 [N][H][W][C]: same
  * bits / A, a thread per pixel walking its contiguous channels. */
 int xnc_pack_input_nhwc(const float* x, int N, int C, int H, int W, const float* in_scale,

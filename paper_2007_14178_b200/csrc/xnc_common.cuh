@@ -76,6 +76,8 @@ int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk,
                          const float* bias, float* out, cudaStream_t s);
 int launch_plane_affine(float* y, int N, int O, long plane, const float* scale, const float* shift,
                         cudaStream_t s);
+int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, uint32_t* bits,
+                           float* A, cudaStream_t s, const float* in_scale, const float* in_shift);
 int launch_pack_input_nhwc(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A, cudaStream_t s,
                            const float* in_scale, const float* in_shift);
 }  // namespace xnc

@@ -20,7 +20,12 @@
 //   warp 0      B (once: this CTA's 48 filter rows of all 27 (c, tap) blocks, TMA,
 //               SWIZZLE_64B), then the MMA issuer on the leader CTA
 //   warp 1      TMA of the raw rows a CTA tile reads (24 rows x 224 per channel,
-//               zero-filled outside the image) through a 2-slot staging ring; TMEM owner
+//               zero-filled outside the image) through a 4-slot staging ring; TMEM owner
+// The A operand is one tile's three per-channel sub-planes, each with its own
+// full / empty barriers: the MMAs of channel c start as soon as its sub-plane is
+// built, and the next tile's channel c is built while channels c+1.. are multiplied
+// (a whole-tile double buffer does not fit beside the 83 KB of resident B and the
+// staging ring; with a 2-slot ring the TMA latency was exposed once per tile).
 //   warps 2-3, 8-11  A producers: staging -> TF32 (round to nearest) -> the tile's
 //               three 64-byte-row SWIZZLE_64B sub-planes (c = 0, 1, 2), 244 rows each
 //   warps 4-7   epilogue: TMEM -> registers -> y, one pixel per thread, its 96
@@ -51,8 +56,8 @@ constexpr int kC1BBytes = kC1Blocks * kC1BBlock;
 constexpr int kC1Tiles = (kC1Ext + 255) / 256;  // pair tiles per image (13)
 constexpr int kC1StRows = 24;               // raw rows a CTA tile spans: 6 cell rows x 4
 constexpr int kC1Stage = kC1StRows * kC1In * 4;  // one channel's rows (21,504 B)
-constexpr int kC1Slots = 2;                       // staging ring
-constexpr int kC1Smem = 2 * kC1Plane + kC1BBytes + kC1Slots * kC1Stage + 1024;
+constexpr int kC1Slots = 4;                       // staging ring
+constexpr int kC1Smem = kC1Plane + kC1BBytes + kC1Slots * kC1Stage + 1024;
 constexpr int kC1ProdWarps = 6;
 constexpr int kC1Threads = 12 * 32;
 constexpr int kC1TmemCols = 256;            // two 96-column accumulators
@@ -81,10 +86,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
                       float* __restrict__ y, int tiles) {
   extern __shared__ __align__(1024) uint8_t c1_smem_raw[];
   uint8_t* smem = c1_smem_raw + ((1024u - (smem_addr(c1_smem_raw) & 1023u)) & 1023u);
-  uint8_t* a_s = smem;                                   // two tiles x 3 sub-planes
-  uint8_t* b_s = smem + 2 * kC1Plane;                    // 27 blocks x 48 rows x 64 B
+  uint8_t* a_s = smem;                                   // one tile's 3 sub-planes
+  uint8_t* b_s = smem + kC1Plane;                        // 27 blocks x 48 rows x 64 B
   float* st_s = reinterpret_cast<float*>(b_s + kC1BBytes);  // raw rows ring [slot][24][224]
-  __shared__ __align__(8) uint64_t b_full, a_full[2], a_empty[2], s_full[kC1Slots], s_empty[kC1Slots],
+  __shared__ __align__(8) uint64_t b_full, a_full[3], a_empty[3], s_full[kC1Slots], s_empty[kC1Slots],
       t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base_s;
 
@@ -98,9 +103,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
       mbar_init(&s_full[b], 1);
       mbar_init(&s_empty[b], kC1ProdWarps);
     }
+    for (int c = 0; c < 3; ++c) {
+      mbar_init(&a_full[c], 2 * kC1ProdWarps);
+      mbar_init(&a_empty[c], 1);
+    }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&a_full[b], 2 * kC1ProdWarps);
-      mbar_init(&a_empty[b], 1);
       mbar_init(&t_full[b], 1);
       mbar_init(&t_empty[b], 2 * 4);
     }
@@ -142,13 +149,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
           mbar_wait(&t_empty[buf], ((item >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
         }
-        mbar_wait(&a_full[buf], (item >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t d = tmem + buf * kC1N;
-        const uint32_t a_plane = a_lo0 + buf * (kC1Plane >> 4);
+        const uint32_t a_plane = a_lo0;
         uint32_t acc = 0;
 #pragma unroll 1
         for (int c = 0; c < 3; ++c) {
+          mbar_wait(&a_full[c], item & 1);  // sub-plane c of this tile built (both CTAs)
+          asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const int ky = tap / 3, kx = tap - 3 * (tap / 3);
@@ -157,8 +164,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
             umma_tf32_tap(d, a_lo, b_lo, hi, idesc, acc);
             acc = 1;
           }
+          umma_commit_pair_elect(&a_empty[c]);  // sub-plane c free once these MMAs finish
         }
-        umma_commit_pair_elect(&a_empty[buf]);
         umma_commit_pair_elect(&t_full[buf]);
       }
     }
@@ -190,17 +197,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
     const uint32_t full0 = map_to_rank(smem_addr(&a_full[0]), 0);
     uint32_t item = 0, use = 0;
     for (int t = cluster; t < tiles; t += n_clusters, ++item) {
-      const uint32_t buf = item & 1;
       const int img = t / kC1Tiles, e0 = (t - img * kC1Tiles) * 256 + (int)rank * 128;
       const int Y0 = e0 / kC1SG;
-      if (item >= 2) {  // the MMAs of the tile two back (same A buffer) are done
-        if (lane == 0) mbar_wait(&a_empty[buf], ((item >> 1) - 1) & 1);
-        __syncwarp();
-      }
-      uint8_t* plane = a_s + buf * kC1Plane;
+      uint8_t* plane = a_s;
       for (int c = 0; c < 3; ++c, ++use) {
         const uint32_t sl = use % kC1Slots;
-        if (lane == 0) mbar_wait(&s_full[sl], (use / kC1Slots) & 1);  // channel c's rows landed
+        if (lane == 0) {
+          mbar_wait(&s_full[sl], (use / kC1Slots) & 1);                // channel c's rows landed
+          if (item >= 1) mbar_wait(&a_empty[c], (item - 1) & 1);        // previous tile's c MMAs done
+        }
         __syncwarp();
         const float* st = st_s + (size_t)sl * (kC1Stage / 4);
         for (int p = pt; p < kC1P; p += n_pt) {
@@ -219,13 +224,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
             *reinterpret_cast<float4*>(row + ((dy ^ ((p >> 1) & 3)) << 4)) = q4;  // SWIZZLE_64B
           }
         }
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
-        if (lane == 0)  // this warp is done reading the slot
+        if (lane == 0) {
+          // this warp is done reading the slot, and its rows of sub-plane c are ready
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&s_empty[sl])) : "memory");
+          mbar_arrive_cluster(full0 + c * 8);
+        }
       }
-      fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(full0 + buf * 8);  // A ready (leader)
     }
   } else {
     // ---- epilogue: warp 4 + q reads TMEM lanes 32q .. 32q+31 (pixels), 96 columns

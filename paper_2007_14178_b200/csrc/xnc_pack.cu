@@ -274,6 +274,104 @@ __global__ void __launch_bounds__(128) k_pack_small(const float* __restrict__ x,
   }
 }
 
+// K1 of a max-pooled map without materialising it (XNOR-Net's pool -> BN -> sign in
+// front of conv3 and fc6): x is the PRE-pool map [N][C][Hin][Win]; the value staged
+// for (channel c, pooled pixel (oy, ox)) is the max over its pk x pk window at
+// stride ps with xnc_max_pool's rule (row-major window order, NaN propagates), then
+// the optional affine -- exactly K1 of xnc_max_pool's output.  Otherwise the block
+// is k_pack_small: 32 pooled pixels x all C channels in shared memory, warp 0 runs
+// the sequential |.| chains, warps 1-3 the sign words.  Saves the pooled map's
+// write and re-read and one launch.
+template <bool AFF, int PK>
+__global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict__ x, int C, int Hin, int Win,
+                                                         int Ho, int Wo, int ps, int Cw, long npix, float inv,
+                                                         uint32_t* __restrict__ bits, float* __restrict__ A,
+                                                         const float* __restrict__ in_scale,
+                                                         const float* __restrict__ in_shift) {
+  extern __shared__ float tile[];  // [C][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long q = (long)blockIdx.x * 32 + lane;
+  const bool in = q < npix;
+  const int HWo = Ho * Wo;
+  const long n = in ? q / HWo : 0;
+  const int p = in ? (int)(q - n * HWo) : 0;
+  const int oy = p / Wo, ox = p - (p / Wo) * Wo;
+  const float* xp = x + n * C * (long)Hin * Win + (long)(oy * ps) * Win + ox * ps;
+  const long plane = (long)Hin * Win;
+  constexpr int kU = 4;  // channels per thread per batch: kU * PK * PK loads in flight
+  for (int c0 = warp; c0 < C; c0 += 4 * kU) {
+    float v[kU][PK * PK];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = c0 + 4 * u;
+      const float* b = xp + (long)c * plane;
+#pragma unroll
+      for (int dy = 0; dy < PK; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < PK; ++dx) v[u][dy * PK + dx] = (in && c < C) ? __ldg(b + dy * Win + dx) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = c0 + 4 * u;
+      if (c < C) {
+        float m = v[u][0];
+#pragma unroll
+        for (int k = 1; k < PK * PK; ++k)
+          if (v[u][k] > m || v[u][k] != v[u][k]) m = v[u][k];
+        if (AFF) m = __fadd_rn(__fmul_rn(m, __ldg(in_scale + c)), __ldg(in_shift + c));
+        tile[c * 32 + lane] = m;
+      }
+    }
+  }
+  __syncthreads();
+  if (!in) return;
+  if (warp == 0) {
+    float s = 0.0f;
+    float cur[16], nxt[16];
+    const int nb = C >> 4;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) cur[u] = nb > 0 ? tile[u * 32 + lane] : 0.0f;
+    for (int k = 0; k < nb; ++k) {
+      if (k + 1 < nb) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) nxt[u] = tile[((k + 1) * 16 + u) * 32 + lane];
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s = __fadd_rn(s, fabsf(cur[u]));
+#pragma unroll
+      for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
+    }
+    for (int c = nb << 4; c < C; ++c) s = __fadd_rn(s, fabsf(tile[c * 32 + lane]));
+    if (A) A[q] = __fmul_rn(s, inv);
+  } else {
+    for (int j = warp - 1; j < Cw; j += 3) {
+      const int cend = min(32, C - 32 * j);
+      uint32_t word = 0u;
+#pragma unroll 8
+      for (int u = 0; u < cend; ++u) word |= (tile[(32 * j + u) * 32 + lane] >= 0.0f ? 1u : 0u) << u;
+      bits[q * Cw + j] = word;
+    }
+  }
+}
+
+// xnc_pack_input_pool: the fused form when the pooled map takes the small-map path
+// (>= 32 pooled pixels per image, C <= kSmallMaxC) and the window is 3 x 3;
+// XNC_ENOTSUP otherwise (the caller pools, then packs).
+int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, uint32_t* bits,
+                           float* A, cudaStream_t s, const float* in_scale, const float* in_shift) {
+  if (pk != 3 || ps < 1 || Hin < pk || Win < pk) return XNC_ENOTSUP;
+  const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
+  const long npix = (long)N * Ho * Wo;
+  if (Ho * Wo < 32 || C < 32 || C > kSmallMaxC) return XNC_ENOTSUP;
+  const int Cw = cdiv(C, 32);
+  const size_t sm = (size_t)C * 32 * sizeof(float);
+  auto kern = in_scale ? k_pack_small_pool<true, 3> : k_pack_small_pool<false, 3>;
+  if (int rc = smem_opt_in(kern, sm)) return rc;  // per device (xnc_runtime.cu)
+  kern<<<(unsigned)cdivl(npix, 32), 128, sm, s>>>(x, C, Hin, Win, Ho, Wo, ps, Cw, npix, (float)(1.0 / (double)C),
+                                                  bits, A, in_scale, in_shift);
+  return launch_status();
+}
+
 // A for 1x1 images with long channel vectors (the fc7 input, 4096 channels): the
 // sum is one sequential chain per pixel, so one thread per pixel left all but a
 // couple of SMs idle and waited out a memory latency per few channels.  Here a

@@ -11,7 +11,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import check, lib
+from ._lib import XNC_ENOTSUP, check, lib
 
 ABI_VERSION = 1
 
@@ -148,6 +148,20 @@ def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None, in_pool=Non
     padding; xnc_max_pool) -- XNOR-Net's pool -> BN -> sign; bits / A then have the
     pooled spatial shape."""
     _need_cuda(x, "x", torch.float32, channels_last_ok=True)
+    if in_pool is not None and not _channels_last(x):
+        # pool fused into K1 (xnc_pack_input_pool) when the pooled map takes its path
+        xc = x.contiguous()
+        N, C, Hin, Win = xc.shape
+        H, W = pool_dims(Hin, Win, in_pool)
+        bits = torch.empty((N, H, W, words(C)), dtype=torch.int32, device=x.device)
+        A = torch.empty((N, H, W), dtype=torch.float32, device=x.device) if want_A else None
+        sc, sh = _affine(in_affine, C, x.device, "in_affine")
+        rc = lib().xnc_pack_input_pool(xc.data_ptr(), N, C, Hin, Win, int(in_pool[0]), int(in_pool[1]), _ptr(sc),
+                                       _ptr(sh), bits.data_ptr(), _ptr(A), _stream(x.device))
+        if rc == 0:
+            return bits, A
+        if rc != XNC_ENOTSUP:
+            check(rc, "xnc_pack_input_pool")
     if in_pool is not None:
         x = max_pool(x, *in_pool)
     N, C, H, W = x.shape

@@ -413,9 +413,10 @@ def test_bn_affines_in_k1_and_epilogue(shape, variant):
 @pytest.mark.parametrize("shape", [(3, 256, 27, 27, 3, 2), (2, 70, 13, 13, 3, 2), (2, 64, 9, 12, 2, 2),
                                    (4, 4096, 3, 3, 3, 1)], ids=lambda s: "x".join(map(str, s)))
 def test_pooled_input_k1(shape):
-    """K1 over a max-pooled input (xnc_max_pool): pooled values identical to
-    torch.max_pool2d, bits and A identical to K1 on that map, with and without the
-    folded BN."""
+    """K1 over a max-pooled input: pooled values identical to torch.max_pool2d, bits
+    and A identical to K1 on that map, with and without the folded BN.  The first
+    two shapes take the fused pool + K1 kernel (xnc_pack_input_pool), the last two
+    its fallback (pool, then pack)."""
     import torch.nn.functional as F
     from paper_2007_14178_b200 import ops
     N, C, H, W, k, s = shape
@@ -423,8 +424,12 @@ def test_pooled_input_k1(shape):
     x = torch.from_numpy(O.f32_exact(rng, (N, C, H, W))).to(_dev())
     x[0, 0, 0, :2] = 0.0  # exact zeros and a negative zero inside pooled windows
     x[0, 1, 1, 1] = -0.0
+    x[N - 1, C - 1, H // 2, W // 2] = float("nan")  # NaN propagates through the pool (both paths)
     pooled = F.max_pool2d(x, k, s).contiguous()
-    assert torch.equal(ops.max_pool(x, k, s).view(torch.int32), pooled.view(torch.int32))
+    assert torch.equal(ops.max_pool(x, k, s).isnan(), pooled.isnan())
+    mp = ops.max_pool(x, k, s)
+    assert torch.equal(torch.where(mp.isnan(), 0, mp).view(torch.int32),
+                       torch.where(pooled.isnan(), 0, pooled).view(torch.int32))
     for aff in (None, (torch.rand(C, device=_dev()) + 0.5, torch.rand(C, device=_dev()) - 0.5)):
         b1, a1 = ops.pack_input(x, in_affine=aff, in_pool=(k, s))
         b2, a2 = ops.pack_input(pooled, in_affine=aff)
