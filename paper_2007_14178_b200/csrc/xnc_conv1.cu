@@ -34,6 +34,7 @@
 // long-scoreboard + 10 % lg_throttle stalls, tensor pipe 30 % active, 209 us at C4.)
 // The caller applies bias + ReLU + max-pool (xnc_max_pool, channels-last).
 #include <algorithm>
+#include <cstdlib>
 
 #include "xnc_common.cuh"
 #include "xnc_tcgen05.cuh"
@@ -83,7 +84,9 @@ __device__ __forceinline__ void umma_tf32_tap(uint32_t d, uint32_t a_lo, uint32_
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
     k_conv1_tf32_pair(const __grid_constant__ CUtensorMap x_map, int N, const __grid_constant__ CUtensorMap b_map,
-                      float* __restrict__ y, int tiles) {
+                      float* __restrict__ y, int tiles, int dbg) {
+  // dbg (profiling only, env XNC_CONV1_DEBUG): bit 0 = epilogue skips its stores,
+  // bit 1 = producers build only the first tile's planes, bit 2 = no MMAs issued
   extern __shared__ __align__(1024) uint8_t c1_smem_raw[];
   uint8_t* smem = c1_smem_raw + ((1024u - (smem_addr(c1_smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // one tile's 3 sub-planes
@@ -161,7 +164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
             const int ky = tap / 3, kx = tap - 3 * (tap / 3);
             const uint32_t a_lo = a_plane + (uint32_t)(c * (kC1Sub >> 4) + (ky * kC1SG + kx) * 4);
             const uint32_t b_lo = b_lo0 + (uint32_t)((c * 9 + tap) * (kC1BBlock >> 4));
-            umma_tf32_tap(d, a_lo, b_lo, hi, idesc, acc);
+            if (!(dbg & 4)) umma_tf32_tap(d, a_lo, b_lo, hi, idesc, acc);
             acc = 1;
           }
           umma_commit_pair_elect(&a_empty[c]);  // sub-plane c free once these MMAs finish
@@ -208,7 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
         }
         __syncwarp();
         const float* st = st_s + (size_t)sl * (kC1Stage / 4);
-        for (int p = pt; p < kC1P; p += n_pt) {
+        for (int p = pt; p < ((dbg & 2) && item > 0 ? 0 : kC1P); p += n_pt) {
           const int e = e0 + p;
           const int Y = e / kC1SG, X = e - (e / kC1SG) * kC1SG;
           const bool live = e < kC1Ext;
@@ -256,7 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
         tmem_wait_ld_regs(v[0]);
         reg_dep16(v[1]);
         reg_dep16(v[2]);
-        if (ok) {
+        if (ok && !(dbg & 1)) {
 #pragma unroll
           for (int j = 0; j < 3; ++j)
 #pragma unroll
@@ -336,7 +339,8 @@ int xnc_conv1_forward(const float* x, int N, const float* wq, float* y, void* st
   const int tiles = (int)tiles_l;
   const int pairs = std::min(tiles, device_sm_count() / 2);
   if (int rc = smem_opt_in(k_conv1_tf32_pair, (size_t)kC1Smem)) return rc;
-  k_conv1_tf32_pair<<<2 * pairs, kC1Threads, kC1Smem, as_stream(stream)>>>(x_map, N, b_map, y, tiles);
+  static const int dbg = getenv("XNC_CONV1_DEBUG") ? atoi(getenv("XNC_CONV1_DEBUG")) : 0;
+  k_conv1_tf32_pair<<<2 * pairs, kC1Threads, kC1Smem, as_stream(stream)>>>(x_map, N, b_map, y, tiles, dbg);
   return launch_status();
 }
 
