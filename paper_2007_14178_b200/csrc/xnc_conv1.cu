@@ -57,8 +57,10 @@ constexpr int kC1BBytes = kC1Blocks * kC1BBlock;
 constexpr int kC1Tiles = (kC1Ext + 255) / 256;  // pair tiles per image (13)
 constexpr int kC1StRows = 24;               // raw rows a CTA tile spans: 6 cell rows x 4
 constexpr int kC1Stage = kC1StRows * kC1In * 4;  // one channel's rows (21,504 B)
-constexpr int kC1Slots = 4;                       // staging ring
-constexpr int kC1Smem = kC1Plane + kC1BBytes + kC1Slots * kC1Stage + 1024;
+constexpr int kC1Slots = 3;                       // staging ring
+constexpr int kC1OutPitch = 52;                   // epilogue staging row: 48 floats + 4 (bank skew)
+constexpr int kC1Out1 = 32 * kC1OutPitch * 4;     // one epilogue warp's staging (6,656 B)
+constexpr int kC1Smem = kC1Plane + kC1BBytes + kC1Slots * kC1Stage + 4 * kC1Out1 + 1024;
 constexpr int kC1ProdWarps = 6;
 constexpr int kC1Threads = 12 * 32;
 constexpr int kC1TmemCols = 256;            // two 96-column accumulators
@@ -92,6 +94,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
   uint8_t* a_s = smem;                                   // one tile's 3 sub-planes
   uint8_t* b_s = smem + kC1Plane;                        // 27 blocks x 48 rows x 64 B
   float* st_s = reinterpret_cast<float*>(b_s + kC1BBytes);  // raw rows ring [slot][24][224]
+  float* out_s = st_s + kC1Slots * (kC1Stage / 4);          // epilogue staging [warp][32 px][52]
   __shared__ __align__(8) uint64_t b_full, a_full[3], a_empty[3], s_full[kC1Slots], s_empty[kC1Slots],
       t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base_s;
@@ -237,21 +240,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
       }
     }
   } else {
-    // ---- epilogue: warp 4 + q reads TMEM lanes 32q .. 32q+31 (pixels), 96 columns
+    // ---- epilogue: warp 4 + q reads TMEM lanes 32q .. 32q+31 (pixels), 96 columns,
+    // in two halves of 48 channels.  Each half is staged in shared memory [pixel][48]
+    // and written back pixel-major: a warp store covers 512 B of consecutive
+    // 192-byte channel runs (whole sectors).  Per-lane stores of a pixel's own
+    // channels hit 32 rows 384 B apart per instruction and took half the kernel
+    // (profiles/conv1_debug_r2k.log: 0.217 ms, 0.111 ms with the stores off).
     const int q = warp & 3;
     const uint32_t t_empty0 = map_to_rank(smem_addr(&t_empty[0]), 0);
+    float* ost = out_s + (size_t)q * (kC1Out1 / 4);
     uint32_t item = 0;
     for (int t = cluster; t < tiles; t += n_clusters, ++item) {
       const uint32_t buf = item & 1;
       const int img = t / kC1Tiles;
-      const int r = (t - img * kC1Tiles) * 256 + (int)rank * 128 + q * 32 + lane;
-      const int Y = r / kC1SG, X = r - (r / kC1SG) * kC1SG;
-      const bool ok = r < kC1Ext && Y < kC1Out && X < kC1Out;
-      float* dst = y + (((size_t)(ok ? img : 0) * kC1Out + (ok ? Y : 0)) * kC1Out + (ok ? X : 0)) * kC1N;
+      const int r0 = (t - img * kC1Tiles) * 256 + (int)rank * 128 + q * 32;  // the warp's first cell
       mbar_wait(&t_full[buf], (item >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + buf * kC1N;
-#pragma unroll
+#pragma unroll 1
       for (int half = 0; half < 2; ++half) {
         uint32_t v[3][16];
 #pragma unroll
@@ -259,14 +265,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kC1Threads, 1)
         tmem_wait_ld_regs(v[0]);
         reg_dep16(v[1]);
         reg_dep16(v[2]);
-        if (ok && !(dbg & 1)) {
+        __syncwarp();  // the previous half's copy-out reads are done
 #pragma unroll
-          for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < 3; ++j)
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              *reinterpret_cast<float4*>(dst + (half * 3 + j) * 16 + 4 * u) =
-                  make_float4(__uint_as_float(v[j][4 * u]), __uint_as_float(v[j][4 * u + 1]),
-                              __uint_as_float(v[j][4 * u + 2]), __uint_as_float(v[j][4 * u + 3]));
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<float4*>(ost + lane * kC1OutPitch + j * 16 + 4 * u) =
+                make_float4(__uint_as_float(v[j][4 * u]), __uint_as_float(v[j][4 * u + 1]),
+                            __uint_as_float(v[j][4 * u + 2]), __uint_as_float(v[j][4 * u + 3]));
+        __syncwarp();
+        if (!(dbg & 1)) {
+          // 32 pixels x 12 float4 = 384 chunks; chunk g -> pixel g / 12, float4 g % 12
+#pragma unroll 4
+          for (int g = lane; g < 32 * 12; g += 32) {
+            const int i = g / 12, f4 = g - (g / 12) * 12;
+            const int r = r0 + i;
+            const int Y = r / kC1SG, X = r - (r / kC1SG) * kC1SG;
+            if (r < kC1Ext && Y < kC1Out && X < kC1Out) {
+              float* dst = y + (((size_t)img * kC1Out + Y) * kC1Out + X) * kC1N + half * 48 + f4 * 4;
+              *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(ost + i * kC1OutPitch + f4 * 4);
+            }
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
