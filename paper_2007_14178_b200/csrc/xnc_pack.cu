@@ -14,6 +14,7 @@
 // channel (fully coalesced), and x is read exactly once.  The bits for 32
 // channels are built in registers and written as one word per pixel.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "xnc_common.cuh"
@@ -359,7 +360,8 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
 // XNC_ENOTSUP otherwise (the caller pools, then packs).
 int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, uint32_t* bits,
                            float* A, cudaStream_t s, const float* in_scale, const float* in_shift) {
-  if (pk != 3 || ps < 1 || Hin < pk || Win < pk) return XNC_ENOTSUP;
+  static const int env = getenv("XNC_POOL_K1") ? atoi(getenv("XNC_POOL_K1")) : 1;
+  if (!env || pk != 3 || ps < 1 || Hin < pk || Win < pk) return XNC_ENOTSUP;
   const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
   const long npix = (long)N * Ho * Wo;
   if (Ho * Wo < 32 || C < 32 || C > kSmallMaxC) return XNC_ENOTSUP;

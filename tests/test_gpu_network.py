@@ -74,7 +74,8 @@ def test_pad_space_to_depth_matches_torch(shape, pad, r):
     assert cl.is_contiguous(memory_format=torch.channels_last) and torch.equal(cl, want)
 
 
-@pytest.mark.parametrize("shape,k,s", [((2, 96, 55, 55), 3, 2), ((3, 7, 9, 12), 2, 2), ((1, 4, 11, 11), 5, 3)])
+@pytest.mark.parametrize("shape,k,s", [((2, 96, 55, 55), 3, 2), ((3, 7, 9, 12), 2, 2), ((1, 4, 11, 11), 5, 3),
+                                       ((2, 256, 27, 27), 3, 2), ((3, 40, 13, 13), 3, 2), ((1, 5, 39, 39), 3, 1)])
 def test_relu_max_pool_matches_torch(shape, k, s):
     from paper_2007_14178_b200 import ops
     x = torch.randn(shape, device="cuda")
