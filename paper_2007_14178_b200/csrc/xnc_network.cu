@@ -131,70 +131,12 @@ int launch_max_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk,
   return launch_status();
 }
 
-// The same pool with one warp per (n, c) plane for planes that fit shared memory
-// (the network's 27 x 27 and 13 x 13 maps): the warp first stages its whole plane
-// with coalesced loads, 8 in flight per lane, then takes every window from shared
-// memory.  The per-output form above reads each window from L1/L2 with stride-2
-// lanes and one load round trip per window row (ncu: 50 % long-scoreboard stalls,
-// 2.5-2.9 TB/s on conv2's 191 MB output).
-constexpr int kPoolPlaneMax = 1536;  // floats per staged plane (6 KB)
-constexpr int kPoolWarps = 8;
-template <int PK>
-__global__ void __launch_bounds__(kPoolWarps * 32) k_max_pool_plane(const float* __restrict__ x, int planes, int C,
-                                                                    int Hin, int Win, int Ho, int Wo, int ps,
-                                                                    int relu, const float* __restrict__ bias,
-                                                                    float* __restrict__ out) {
-  __shared__ float pl[kPoolWarps][kPoolPlaneMax];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = blockIdx.x * kPoolWarps + warp;
-  if (p >= planes) return;
-  const int hw = Hin * Win;
-  const float* xp = x + (long)p * hw;
-  float* t = pl[warp];
-  for (int i0 = 0; i0 < hw; i0 += 32 * 8) {
-    float v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + u * 32 + lane;
-      v[u] = i < hw ? __ldcs(xp + i) : 0.0f;  // read once: streamed
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + u * 32 + lane;
-      if (i < hw) t[i] = v[u];
-    }
-  }
-  __syncwarp();
-  const float b = bias != nullptr ? __ldg(bias + p % C) : 0.0f;
-  float* op = out + (long)p * Ho * Wo;
-  for (int o = lane; o < Ho * Wo; o += 32) {
-    const int oy = o / Wo, ox = o - (o / Wo) * Wo;
-    const float* w = t + (oy * ps) * Win + ox * ps;
-    float m = w[0];
-#pragma unroll
-    for (int dy = 0; dy < PK; ++dy)
-#pragma unroll
-      for (int dx = 0; dx < PK; ++dx) {
-        const float v = w[dy * Win + dx];
-        if (v > m || v != v) m = v;
-      }
-    if (bias != nullptr) m = __fadd_rn(m, b);  // max(v + b) == max(v) + b
-    if (relu && m < 0.0f) m = 0.0f;           // clamp_min(0): NaN and -0.0 pass through
-    op[o] = m;
-  }
-}
-
 int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, const float* bias,
                     float* out, cudaStream_t s) {
   if (pk < 1 || pk > 8 || ps < 1 || Hin < pk || Win < pk) return XNC_EINVAL;
   const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
   const long planes = (long)N * C, total = planes * Ho * Wo;
   const unsigned blocks = (unsigned)std::min<long>(cdivl(total, 256), 148L * 16);
-  if (pk == 3 && Hin * Win <= kPoolPlaneMax && planes < 0x7fffffffL) {
-    k_max_pool_plane<3><<<(unsigned)cdivl(planes, kPoolWarps), kPoolWarps * 32, 0, s>>>(
-        x, (int)planes, C, Hin, Win, Ho, Wo, ps, relu, bias, out);
-    return launch_status();
-  }
   if (pk == 3)
     k_max_pool<3><<<blocks, 256, 0, s>>>(x, planes, C, Hin, Win, Ho, Wo, pk, ps, relu, bias, out);
   else if (pk == 2)
