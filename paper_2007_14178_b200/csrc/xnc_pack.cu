@@ -295,8 +295,9 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
   // with coalesced loads, and each lane takes its window maxima from shared memory.
   // (Per-lane window loads straight from global ran L1-bound: 9 loads per value,
   // each spread over three input rows; ncu 62 % L1 throughput, 2.4 TB/s.)
-  extern __shared__ float tile[];  // [C][32], then the band staging [kPCh][R * Win]
+  extern __shared__ float tile[];  // [C][32], then the band staging [2][kPCh][kBandMax]
   constexpr int kPCh = 8;
+  constexpr int kBandMax = 384;  // band floats per channel (host-checked: R * Win <= 384)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int HWo = Ho * Wo;
   const long n = blockIdx.x / bpi;
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
   const int oy0 = p0 / Wo, oy1 = q_hi / Wo;
   const int row0 = oy0 * ps, R = (oy1 - oy0) * ps + PK;      // input band rows
   const int band = R * Win;
-  float* stg = tile + (size_t)C * 32;
+  float* stg = tile + (size_t)C * 32;  // [2 buffers][kPCh][kBandMax]
   const long q = q0 + lane;
   const bool in = lane <= q_hi - p0;
   const int p = p0 + lane;
@@ -314,24 +315,41 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
   const int woff = (oy * ps - row0) * Win + ox * ps;           // window origin in the band
   const float* xb = x + (n * C * (long)Hin + row0) * Win;       // channel 0's band
   const long plane = (long)Hin * Win;
+  // register double buffer: the next chunk's band loads (kPCh channels x kLd per
+  // thread, all in flight) are issued before this chunk's windows are taken
+  constexpr int kLd = kBandMax / 128;
+  float v[kPCh][kLd];
+  auto load = [&](int c0) {
+#pragma unroll
+    for (int ch = 0; ch < kPCh; ++ch)
+#pragma unroll
+      for (int k = 0; k < kLd; ++k) {
+        const int j = threadIdx.x + 128 * k;
+        v[ch][k] = (c0 + ch < C && j < band) ? __ldcs(xb + (long)(c0 + ch) * plane + j) : 0.0f;
+      }
+  };
+  load(0);
   for (int c0 = 0; c0 < C; c0 += kPCh) {
+    float* sb = stg + ((c0 / kPCh) & 1) * (kPCh * kBandMax);
+#pragma unroll
+    for (int ch = 0; ch < kPCh; ++ch)
+#pragma unroll
+      for (int k = 0; k < kLd; ++k) {
+        const int j = threadIdx.x + 128 * k;
+        if (j < band) sb[ch * kBandMax + j] = v[ch][k];
+      }
+    __syncthreads();  // band staged (and, two chunks back, the same buffer's windows taken)
+    if (c0 + kPCh < C) load(c0 + kPCh);
     const int nch = min(kPCh, C - c0);
-    __syncthreads();  // the previous chunk's windows are taken
-    for (int i = threadIdx.x; i < nch * band; i += 128) {
-      const int ch = i / band, j = i - (i / band) * band;
-      stg[i] = __ldcs(xb + (long)(c0 + ch) * plane + j);
-    }
-    __syncthreads();
-    // warp w takes channels c0 + w, c0 + w + 4 of the chunk for its 32 pixels
     for (int ch = warp; ch < nch; ch += 4) {
-      const float* w = stg + ch * band + woff;
+      const float* w = sb + ch * kBandMax + woff;
       float m = w[0];
 #pragma unroll
       for (int dy = 0; dy < PK; ++dy)
 #pragma unroll
         for (int dx = 0; dx < PK; ++dx) {
-          const float v = w[dy * Win + dx];
-          if (v > m || v != v) m = v;
+          const float t = w[dy * Win + dx];
+          if (t > m || t != t) m = t;
         }
       if (AFF) m = __fadd_rn(__fmul_rn(m, __ldg(in_scale + c0 + ch)), __ldg(in_shift + c0 + ch));
       tile[(c0 + ch) * 32 + lane] = m;
@@ -382,8 +400,8 @@ int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int p
   if ((long)N * bpi > 0x7fffffffL) return XNC_ENOTSUP;
   const int Cw = cdiv(C, 32);
   const int rows_max = (cdiv(32, Wo) + 1) * ps + pk;  // band rows of a 32-pixel block, upper bound
-  const size_t sm = ((size_t)C * 32 + (size_t)8 * rows_max * Win) * sizeof(float);
-  if (sm > 200 * 1024) return XNC_ENOTSUP;
+  if (rows_max * Win > 384) return XNC_ENOTSUP;         // kBandMax
+  const size_t sm = ((size_t)C * 32 + (size_t)2 * 8 * 384) * sizeof(float);
   auto kern = in_scale ? k_pack_small_pool<true, 3> : k_pack_small_pool<false, 3>;
   if (int rc = smem_opt_in(kern, sm)) return rc;  // per device (xnc_runtime.cu)
   kern<<<(unsigned)(N * bpi), 128, sm, s>>>(x, C, Hin, Win, Ho, Wo, ps, Cw, bpi, (float)(1.0 / (double)C), bits,
