@@ -14,7 +14,6 @@
 // channel (fully coalesced), and x is read exactly once.  The bits for 32
 // channels are built in registers and written as one word per pixel.
 #include <algorithm>
-#include <cstdlib>
 #include <type_traits>
 
 #include "xnc_common.cuh"
@@ -285,74 +284,43 @@ __global__ void __launch_bounds__(128) k_pack_small(const float* __restrict__ x,
 // write and re-read and one launch.
 template <bool AFF, int PK>
 __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict__ x, int C, int Hin, int Win,
-                                                         int Ho, int Wo, int ps, int Cw, int bpi, float inv,
+                                                         int Ho, int Wo, int ps, int Cw, long npix, float inv,
                                                          uint32_t* __restrict__ bits, float* __restrict__ A,
                                                          const float* __restrict__ in_scale,
                                                          const float* __restrict__ in_shift) {
-  // Block b takes pooled pixels 32 * (b % bpi) .. +31 of image b / bpi (bpi blocks
-  // per image, the last one partial).  The block's 32 pooled pixels (one image) read a band of R consecutive input rows,
-  // contiguous in every channel plane: the band is staged kPCh channels at a time
-  // with coalesced loads, and each lane takes its window maxima from shared memory.
-  // (Per-lane window loads straight from global ran L1-bound: 9 loads per value,
-  // each spread over three input rows; ncu 62 % L1 throughput, 2.4 TB/s.)
-  extern __shared__ float tile[];  // [C][32], then the band staging [2][kPCh][kBandMax]
-  constexpr int kPCh = 8;
-  constexpr int kBandMax = 384;  // band floats per channel (host-checked: R * Win <= 384)
+  extern __shared__ float tile[];  // [C][32]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long q = (long)blockIdx.x * 32 + lane;
+  const bool in = q < npix;
   const int HWo = Ho * Wo;
-  const long n = blockIdx.x / bpi;
-  const int p0 = (int)(blockIdx.x - n * bpi) * 32;
-  const long q0 = n * HWo + p0;
-  const int q_hi = min(HWo - 1, p0 + 31);  // the block's last pooled pixel
-  const int oy0 = p0 / Wo, oy1 = q_hi / Wo;
-  const int row0 = oy0 * ps, R = (oy1 - oy0) * ps + PK;      // input band rows
-  const int band = R * Win;
-  float* stg = tile + (size_t)C * 32;  // [2 buffers][kPCh][kBandMax]
-  const long q = q0 + lane;
-  const bool in = lane <= q_hi - p0;
-  const int p = p0 + lane;
-  const int oy = in ? p / Wo : oy0, ox = in ? p - (p / Wo) * Wo : 0;
-  const int woff = (oy * ps - row0) * Win + ox * ps;           // window origin in the band
-  const float* xb = x + (n * C * (long)Hin + row0) * Win;       // channel 0's band
+  const long n = in ? q / HWo : 0;
+  const int p = in ? (int)(q - n * HWo) : 0;
+  const int oy = p / Wo, ox = p - (p / Wo) * Wo;
+  const float* xp = x + n * C * (long)Hin * Win + (long)(oy * ps) * Win + ox * ps;
   const long plane = (long)Hin * Win;
-  // register double buffer: the next chunk's band loads (kPCh channels x kLd per
-  // thread, all in flight) are issued before this chunk's windows are taken
-  constexpr int kLd = kBandMax / 128;
-  float v[kPCh][kLd];
-  auto load = [&](int c0) {
+  constexpr int kU = 4;  // channels per thread per batch: kU * PK * PK loads in flight
+  for (int c0 = warp; c0 < C; c0 += 4 * kU) {
+    float v[kU][PK * PK];
 #pragma unroll
-    for (int ch = 0; ch < kPCh; ++ch)
-#pragma unroll
-      for (int k = 0; k < kLd; ++k) {
-        const int j = threadIdx.x + 128 * k;
-        v[ch][k] = (c0 + ch < C && j < band) ? __ldcs(xb + (long)(c0 + ch) * plane + j) : 0.0f;
-      }
-  };
-  load(0);
-  for (int c0 = 0; c0 < C; c0 += kPCh) {
-    float* sb = stg + ((c0 / kPCh) & 1) * (kPCh * kBandMax);
-#pragma unroll
-    for (int ch = 0; ch < kPCh; ++ch)
-#pragma unroll
-      for (int k = 0; k < kLd; ++k) {
-        const int j = threadIdx.x + 128 * k;
-        if (j < band) sb[ch * kBandMax + j] = v[ch][k];
-      }
-    __syncthreads();  // band staged (and, two chunks back, the same buffer's windows taken)
-    if (c0 + kPCh < C) load(c0 + kPCh);
-    const int nch = min(kPCh, C - c0);
-    for (int ch = warp; ch < nch; ch += 4) {
-      const float* w = sb + ch * kBandMax + woff;
-      float m = w[0];
+    for (int u = 0; u < kU; ++u) {
+      const int c = c0 + 4 * u;
+      const float* b = xp + (long)c * plane;
 #pragma unroll
       for (int dy = 0; dy < PK; ++dy)
 #pragma unroll
-        for (int dx = 0; dx < PK; ++dx) {
-          const float t = w[dy * Win + dx];
-          if (t > m || t != t) m = t;
-        }
-      if (AFF) m = __fadd_rn(__fmul_rn(m, __ldg(in_scale + c0 + ch)), __ldg(in_shift + c0 + ch));
-      tile[(c0 + ch) * 32 + lane] = m;
+        for (int dx = 0; dx < PK; ++dx) v[u][dy * PK + dx] = (in && c < C) ? __ldg(b + dy * Win + dx) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = c0 + 4 * u;
+      if (c < C) {
+        float m = v[u][0];
+#pragma unroll
+        for (int k = 1; k < PK * PK; ++k)
+          if (v[u][k] > m || v[u][k] != v[u][k]) m = v[u][k];
+        if (AFF) m = __fadd_rn(__fmul_rn(m, __ldg(in_scale + c)), __ldg(in_shift + c));
+        tile[c * 32 + lane] = m;
+      }
     }
   }
   __syncthreads();
@@ -391,21 +359,16 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
 // XNC_ENOTSUP otherwise (the caller pools, then packs).
 int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, uint32_t* bits,
                            float* A, cudaStream_t s, const float* in_scale, const float* in_shift) {
-  static const int env = getenv("XNC_POOL_K1") ? atoi(getenv("XNC_POOL_K1")) : 1;
-  if (!env || pk != 3 || ps < 1 || Hin < pk || Win < pk) return XNC_ENOTSUP;
+  if (pk != 3 || ps < 1 || Hin < pk || Win < pk) return XNC_ENOTSUP;
   const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
-  // blocks of up to 32 pooled pixels of one image (a block's band is one image's rows)
+  const long npix = (long)N * Ho * Wo;
   if (Ho * Wo < 32 || C < 32 || C > kSmallMaxC) return XNC_ENOTSUP;
-  const int bpi = cdiv(Ho * Wo, 32);
-  if ((long)N * bpi > 0x7fffffffL) return XNC_ENOTSUP;
   const int Cw = cdiv(C, 32);
-  const int rows_max = (cdiv(32, Wo) + 1) * ps + pk;  // band rows of a 32-pixel block, upper bound
-  if (rows_max * Win > 384) return XNC_ENOTSUP;         // kBandMax
-  const size_t sm = ((size_t)C * 32 + (size_t)2 * 8 * 384) * sizeof(float);
+  const size_t sm = (size_t)C * 32 * sizeof(float);
   auto kern = in_scale ? k_pack_small_pool<true, 3> : k_pack_small_pool<false, 3>;
   if (int rc = smem_opt_in(kern, sm)) return rc;  // per device (xnc_runtime.cu)
-  kern<<<(unsigned)(N * bpi), 128, sm, s>>>(x, C, Hin, Win, Ho, Wo, ps, Cw, bpi, (float)(1.0 / (double)C), bits,
-                                            A, in_scale, in_shift);
+  kern<<<(unsigned)cdivl(npix, 32), 128, sm, s>>>(x, C, Hin, Win, Ho, Wo, ps, Cw, npix, (float)(1.0 / (double)C),
+                                                  bits, A, in_scale, in_shift);
   return launch_status();
 }
 
