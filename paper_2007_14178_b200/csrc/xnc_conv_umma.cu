@@ -204,6 +204,37 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
                : "memory");
 }
 
+// ---- fused K1 -> K2 -> conv (FUSED kernels, xnc_layer_forward_umma_fused) ------
+// Coherent global loads for data other CTAs write during the same launch (the
+// packed bits and the K map): the read-only (.nc) path may serve stale lines.
+__device__ __forceinline__ uint4 ld_cg_u4(const uint32_t* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+  float r;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int r;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Wait until image n's bits / A / K are published (ready flag 1).  Bounded: a flag
+// that never arrives traps (a kernel error) instead of hanging the device.
+__device__ __forceinline__ void wait_image_ready(const int* ready) {
+  unsigned spins = 0;
+  while (ld_acquire_gpu(ready) == 0) {
+    __nanosleep(128);
+    if (++spins > (1u << 25)) __trap();
+  }
+}
+
 struct PairGeom {
   int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NP, MH, taps, Cw;
   int P;             // extended pixel rows one K-block plane holds
@@ -221,6 +252,8 @@ struct PairGeom {
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
   int cst_O;    // > 0: sw / alpha staged in shared memory (cst_O entries each, after the B ring)
+  int k1_upi;      // FUSED: K1 units (512 pixels of one image) per image
+  float box;       // FUSED: f32(1 / (kh * kw)), the K map scale (_kernels_cy.pyx:259)
   int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
                    // epilogue carries a pixel's running |.| sum and sign words across the blocks)
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
@@ -262,13 +295,22 @@ __device__ __forceinline__ int units_of(const PairGeom& g, int cluster, int n_cl
 // AX = A-producer warps beyond warps 2-3 (after the epilogue warps): at N <= 128 a
 // chunk's four MMAs take half as long as at N = 256 and two producer warps fall
 // behind (C2k3: the issuer waited on a_full for a third of its time).
-template <int MH, bool PROF, int AX>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarps + 32 * AX, 1) k_conv_umma_pair(
+// FUSED: four more warps run K1 (sign bits + A of x, 512 pixels of one image per unit,
+// images in order) and, for each image's last unit, K2 (its K map), publishing a
+// per-image ready flag; the A producers and the epilogue wait for the flag of an
+// image before touching its bits / K.  K1 (HBM reads) then overlaps the convolution
+// (tensor cores + y's HBM writes) instead of preceding it.  fx = the float input,
+// fA = A, fsync = [N] unit counters, [N] ready flags, [1] finished-CTA counter (zero
+// on entry, left zero on exit).
+template <int MH, bool PROF, int AX, bool FUSED = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarps + 32 * AX + (FUSED ? 128 : 0), 1)
+    k_conv_umma_pair(
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
     const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out,
     const float* __restrict__ out_scale, const float* __restrict__ out_shift, int32_t* __restrict__ part,
-    uint32_t* __restrict__ next_bits, float* __restrict__ next_A) {
+    uint32_t* __restrict__ next_bits, float* __restrict__ next_A, const float* __restrict__ fx = nullptr,
+    float* __restrict__ fA = nullptr, int* __restrict__ fsync = nullptr) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
@@ -345,7 +387,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       }
       if (prof) g_umma_prof[blockIdx.x][7] = w_be;
     }
-  } else if ((warp >= kPAWarp0 && warp < kPAWarp0 + 2) || warp >= kPEpiWarp0 + kPEpiWarps) {
+  } else if ((warp >= kPAWarp0 && warp < kPAWarp0 + 2) ||
+             (warp >= kPEpiWarp0 + kPEpiWarps && warp < kPEpiWarp0 + kPEpiWarps + AX)) {
     // ================= A producers: packed bits -> swizzled d-bytes, per K block
     const int a_w = warp < kPEpiWarp0 ? warp - kPAWarp0 : 2 + (warp - kPEpiWarp0 - kPEpiWarps);
     const int pt = a_w * 32 + lane, n_pt = (2 + AX) * 32;
@@ -362,6 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     constexpr int kAR = XNC_A_ROWS;
     const int grp = g.a_unit ? g.KBu : 1;
     uint32_t it = 0;  // units of this pair so far: every unit builds its KBu planes
+    int n_ready = -1;  // FUSED: the last image whose bits were seen published
     for (;; ++it) {
       const int u = unit_at(g, cluster, n_clusters, (int)it);
       if (u < 0) break;
@@ -369,6 +413,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
       const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
+      if (FUSED && n != n_ready) {
+        if (lane == 0) wait_image_ready(fsync + g.tiles / g.n_mt + n);
+        __syncwarp();
+        n_ready = n;
+      }
       for (int kb0 = 0; kb0 < g.KBu; kb0 += grp) {
         const uint32_t use0 = it * g.KBu + kb0;
         // barrier guarding the group's slots: per unit (group it & 1) or per plane
@@ -411,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
                   if (in_img[i] && (k == 0 || two)) {
                     const uint32_t* sk = src + (kbA + k) * 4;
                     if (vec4) {
-                      q[k][i] = __ldg(reinterpret_cast<const uint4*>(sk));
+                      q[k][i] = FUSED ? ld_cg_u4(sk) : __ldg(reinterpret_cast<const uint4*>(sk));
                     } else {
                       const int wl = g.Cw - (kbA + k) * 4;  // words of this block present
                       q[k][i].x = __ldg(sk);
@@ -530,6 +579,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         g_umma_prof[blockIdx.x][4] = n_mma;
       }
     }
+  } else if (FUSED && warp >= kPEpiWarp0 + kPEpiWarps + AX) {
+    // ================= K1 (+ K2) for the images ahead of the convolution
+    // Unit = (image n, pixels 512b .. 512b+511); this CTA takes units blockIdx.x,
+    // blockIdx.x + gridDim.x, ... in image order.  Per thread: 4 consecutive pixels,
+    // the C channels walked in order with 16-byte streaming loads (k_pack_input's
+    // arithmetic: bit = x >= 0, A = sequential f32 sum of |x| * f32(1/C)); the bit
+    // words go straight to global memory.  The CTA that completes an image's last
+    // unit computes its K map (k_scale_map's op order) and raises the image's flag.
+    __shared__ int k1_last;
+    const int kt = tid - (kPEpiWarp0 + kPEpiWarps + AX) * 32;  // 0..127
+    const int N = g.tiles / g.n_mt;
+    const int HW = g.H * g.W;
+    const float inv = (float)(1.0 / (double)g.C);
+    uint32_t* bits_w = const_cast<uint32_t*>(bits);
+    float* K_w = const_cast<float*>(Kmap);
+    int* cnt = fsync;
+    int* ready = fsync + N;
+    for (int u = blockIdx.x; u < N * g.k1_upi; u += gridDim.x) {
+      const int n = u / g.k1_upi, b = u - (u / g.k1_upi) * g.k1_upi;
+      const int p0 = b * 512 + kt * 4;
+      if (p0 < HW) {
+        const float* xp = fx + (size_t)n * g.C * HW + p0;
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < g.Cw; ++j) {
+          uint32_t word[4] = {0u, 0u, 0u, 0u};
+          const int cend = min(32, g.C - 32 * j);
+          for (int c0 = 0; c0 < cend; c0 += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int uu = 0; uu < 8; ++uu)
+              v[uu] = c0 + uu < cend ? __ldcs(reinterpret_cast<const float4*>(xp + (size_t)(32 * j + c0 + uu) * HW))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int uu = 0; uu < 8; ++uu) {
+              if (c0 + uu < cend) {
+                const int cc = c0 + uu;
+                const float e[4] = {v[uu].x, v[uu].y, v[uu].z, v[uu].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  s4[i] = __fadd_rn(s4[i], fabsf(e[i]));
+                  word[i] |= (e[i] >= 0.0f ? 1u : 0u) << cc;
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) bits_w[((size_t)n * HW + p0 + i) * g.Cw + j] = word[i];
+        }
+        *reinterpret_cast<float4*>(fA + (size_t)n * HW + p0) =
+            make_float4(__fmul_rn(s4[0], inv), __fmul_rn(s4[1], inv), __fmul_rn(s4[2], inv), __fmul_rn(s4[3], inv));
+      }
+      __threadfence();  // this thread's bits / A visible device-wide before the count
+      named_bar_sync(8, 128);
+      if (kt == 0) k1_last = atomicAdd(cnt + n, 1) == g.k1_upi - 1;
+      named_bar_sync(8, 128);
+      if (k1_last) {
+        // K2 for image n from every unit's A (k_scale_map's order: kw-wide row sums from
+        // 0, then the kh row sums top to bottom, times f32(1 / (kh * kw)))
+        __threadfence();
+        const float* a = fA + (size_t)n * HW;
+        for (int o = kt; o < g.oh * g.ow; o += 128) {
+          const int yy = o / g.ow, xx = o - (o / g.ow) * g.ow;
+          float acc = 0.0f;
+          for (int d = 0; d < g.kh; ++d) {
+            const int r = yy + d - g.pad;
+            float rs = 0.0f;
+            for (int e2 = 0; e2 < g.kw; ++e2) {
+              const int c = xx + e2 - g.pad;
+              rs = __fadd_rn(rs, (r >= 0 && r < g.H && c >= 0 && c < g.W) ? ld_cg_f32(a + (size_t)r * g.W + c) : 0.0f);
+            }
+            acc = d == 0 ? rs : __fadd_rn(acc, rs);
+          }
+          K_w[(size_t)n * g.oh * g.ow + o] = __fmul_rn(acc, g.box);
+        }
+        __threadfence();
+        named_bar_sync(8, 128);
+        if (kt == 0) st_release_gpu(ready + n, 1);
+      }
+    }
   } else if (warp >= kPEpiWarp0 && warp < kPEpiWarp0 + kPEpiWarps) {
     // ================= epilogue (both CTAs)
     // warp w reads TMEM lane quadrant (w & 3) and the 16-column chunks cg,
@@ -573,12 +701,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     float emit_sA[MH];  // sign-emitting epilogue: running |.| sum of each pixel across filter blocks
 #pragma unroll
     for (int h = 0; h < MH; ++h) emit_sA[h] = 0.0f;
+    int n_ready = -1;  // FUSED: the last image whose K map was seen published
     for (;; ++item) {
       const int u = unit_at(g, cluster, n_clusters, (int)item);
       if (u < 0) break;
       const int t = u / (g.n_nb * g.S), nb = (u / g.S) % g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);
+      if (FUSED && n != n_ready) {
+        if (lane == 0) wait_image_ready(fsync + g.tiles / g.n_mt + n);
+        __syncwarp();
+        n_ready = n;
+      }
       size_t pix[MH], qix[MH];
       bool ok[MH];
       float kv[MH];
@@ -589,7 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         ok[h] = rr < g.oh && cc < g.ow;
         qix[h] = (size_t)n * plane_out + (size_t)rr * g.ow + cc;  // output pixel (n, rr, cc)
         pix[h] = (size_t)n * g.O * plane_out + (size_t)rr * g.ow + cc;
-        kv[h] = (ok[h] && (y || next_bits)) ? __ldg(Kmap + qix[h]) : 0.0f;
+        kv[h] = (ok[h] && (y || next_bits)) ? (FUSED ? ld_cg_f32(Kmap + qix[h]) : __ldg(Kmap + qix[h])) : 0.0f;
       }
       const uint32_t buf = item & 1;
       mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
@@ -852,6 +986,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
   }
+  if (FUSED && tid == 0) {
+    // the last CTA to finish zeroes the counters and flags for the next launch
+    const int N = g.tiles / g.n_mt;
+    __threadfence();
+    if (atomicAdd(fsync + 2 * N, 1) == (int)gridDim.x - 1) {
+      for (int i = 0; i < 2 * N; ++i) fsync[i] = 0;
+      fsync[2 * N] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ---------------------------------------------------------------- weights
@@ -1097,13 +1241,62 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
   g.tile_major = next_bits != nullptr && g.n_nb > 1;
   kern<<<2 * pairs, threads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
-                                          next_bits, next_A);
+                                          next_bits, next_A, nullptr, nullptr, nullptr);
   if (part != nullptr) {
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
     k_split_finalize<<<blocks, 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift, total, O,
                                             (long)g.oh * g.ow, y, acc);
   }
+  return launch_status();
+}
+
+// The fused layer (K1 -> K2 -> conv in one persistent launch, FUSED kernels): for
+// shapes whose plan uses the plain 384-thread launch (filter blocks wider than 128),
+// W*H a multiple of 4 and x 16-byte aligned.  bits / A / K are written by the
+// kernel itself; sync = 2N + 1 ints, zero on entry and left zero.
+bool fused_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
+  PairGeom g;
+  size_t smem;
+  if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return false;
+  return g.NP > 128 && kPAExtra == 0 && (H * W) % 4 == 0 && g.S == 1;
+}
+
+int launch_conv_umma_fused(const float* x, const uint8_t* wq, const int32_t* sw, const float* alpha, int N, int C,
+                           int H, int W, int O, int kh, int kw, int pad, uint32_t* bits, float* A, float* K,
+                           int* sync, float* y, cudaStream_t s) {
+  if (!fused_supported(N, C, H, W, O, kh, kw, pad) || (reinterpret_cast<uintptr_t>(x) & 15) ||
+      (reinterpret_cast<uintptr_t>(A) & 15))
+    return XNC_ENOTSUP;
+  PairGeom g;
+  size_t smem;
+  pair_plan(N, C, H, W, O, kh, kw, pad, g, smem);
+  auto encode = tensor_map_encoder();
+  if (!encode) return XNC_ENOTSUP;
+  CUtensorMap b_map;
+  {
+    const cuuint64_t rows = (cuuint64_t)g.n_nb * g.taps * g.KBn * g.NP;
+    cuuint64_t dims[2] = {128u, rows};
+    cuuint64_t strides[1] = {128u};
+    cuuint32_t box[2] = {128u, (cuuint32_t)(g.NP / 2)};
+    cuuint32_t estr[2] = {1u, 1u};
+    if (encode(&b_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(wq), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return XNC_ENOTSUP;
+  }
+  g.debug = 0;
+  g.inv_O = (float)(1.0 / (double)O);
+  g.tile_major = 0;
+  g.k1_upi = cdiv(H * W, 512);
+  g.box = (float)(1.0 / (double)(kh * kw));  // <real_t> scale, _kernels_cy.pyx:259
+  const int sms = sm_count();
+  const int pairs = g.units < sms / 2 ? g.units : sms / 2;
+  if (g.MH != 1) return XNC_ENOTSUP;  // NP > 128 plans run MH = 1
+  auto kern = k_conv_umma_pair<1, false, 0, true>;
+  if (int rc = smem_opt_in(kern, smem)) return rc;  // per device (xnc_runtime.cu)
+  kern<<<2 * pairs, kPThreads + 128, smem, s>>>(bits, b_map, sw, K, alpha, g, y, nullptr, nullptr, nullptr, nullptr,
+                                                nullptr, nullptr, x, A, sync);
   return launch_status();
 }
 
