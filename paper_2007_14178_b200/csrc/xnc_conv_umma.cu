@@ -205,6 +205,10 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
 }
 
 // ---- fused K1 -> K2 -> conv (FUSED kernels, xnc_layer_forward_umma_fused) ------
+#ifndef XNC_K1U
+#define XNC_K1U 16
+#endif
+constexpr int kK1U = XNC_K1U;
 // Coherent global loads for data other CTAs write during the same launch (the
 // packed bits and the K map): the read-only (.nc) path may serve stale lines.
 __device__ __forceinline__ uint4 ld_cg_u4(const uint32_t* p) {
@@ -605,14 +609,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         for (int j = 0; j < g.Cw; ++j) {
           uint32_t word[4] = {0u, 0u, 0u, 0u};
           const int cend = min(32, g.C - 32 * j);
-          for (int c0 = 0; c0 < cend; c0 += 8) {
-            float4 v[8];
+          // kK1U channel loads per thread in flight: four warps must keep ~32 KB of x in
+          // flight per SM to stream their share of the batch under the conv
+          for (int c0 = 0; c0 < cend; c0 += kK1U) {
+            float4 v[kK1U];
 #pragma unroll
-            for (int uu = 0; uu < 8; ++uu)
+            for (int uu = 0; uu < kK1U; ++uu)
               v[uu] = c0 + uu < cend ? __ldcs(reinterpret_cast<const float4*>(xp + (size_t)(32 * j + c0 + uu) * HW))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int uu = 0; uu < 8; ++uu) {
+            for (int uu = 0; uu < kK1U; ++uu) {
               if (c0 + uu < cend) {
                 const int cc = c0 + uu;
                 const float e[4] = {v[uu].x, v[uu].y, v[uu].z, v[uu].w};
