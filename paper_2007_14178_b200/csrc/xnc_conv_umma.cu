@@ -211,16 +211,9 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
 constexpr int kK1U = XNC_K1U;
 // Coherent global loads for data other CTAs write during the same launch (the
 // packed bits and the K map): the read-only (.nc) path may serve stale lines.
-__device__ __forceinline__ uint4 ld_cg_u4(const uint32_t* p) {
-  uint4 r;
-  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ float ld_cg_f32(const float* p) {
-  float r;
-  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(r) : "l"(p));
-  return r;
-}
+// (the __ldcg intrinsic: ld.global.cg, reorderable, so batches of them stay in flight)
+__device__ __forceinline__ uint4 ld_cg_u4(const uint32_t* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
+__device__ __forceinline__ float ld_cg_f32(const float* p) { return __ldcg(p); }
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int r;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
@@ -645,17 +638,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         // 0, then the kh row sums top to bottom, times f32(1 / (kh * kw)))
         __threadfence();
         const float* a = fA + (size_t)n * HW;
+        // all kh x kw taps of an output loaded before the adds (k <= 3: one round
+        // trip per output instead of one per tap; larger k falls back to a loop)
         for (int o = kt; o < g.oh * g.ow; o += 128) {
           const int yy = o / g.ow, xx = o - (o / g.ow) * g.ow;
           float acc = 0.0f;
-          for (int d = 0; d < g.kh; ++d) {
-            const int r = yy + d - g.pad;
-            float rs = 0.0f;
-            for (int e2 = 0; e2 < g.kw; ++e2) {
-              const int c = xx + e2 - g.pad;
-              rs = __fadd_rn(rs, (r >= 0 && r < g.H && c >= 0 && c < g.W) ? ld_cg_f32(a + (size_t)r * g.W + c) : 0.0f);
+          if (g.kh <= 3 && g.kw <= 3) {
+            float tv[3][3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+              for (int e2 = 0; e2 < 3; ++e2) {
+                const int r = yy + d - g.pad, c = xx + e2 - g.pad;
+                tv[d][e2] = (d < g.kh && e2 < g.kw && r >= 0 && r < g.H && c >= 0 && c < g.W)
+                                ? ld_cg_f32(a + (size_t)r * g.W + c) : 0.0f;
+              }
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              if (d >= g.kh) break;
+              float rs = 0.0f;
+#pragma unroll
+              for (int e2 = 0; e2 < 3; ++e2)
+                if (e2 < g.kw) rs = __fadd_rn(rs, tv[d][e2]);
+              acc = d == 0 ? rs : __fadd_rn(acc, rs);
             }
-            acc = d == 0 ? rs : __fadd_rn(acc, rs);
+          } else {
+            for (int d = 0; d < g.kh; ++d) {
+              const int r = yy + d - g.pad;
+              float rs = 0.0f;
+              for (int e2 = 0; e2 < g.kw; ++e2) {
+                const int c = xx + e2 - g.pad;
+                rs = __fadd_rn(rs, (r >= 0 && r < g.H && c >= 0 && c < g.W) ? ld_cg_f32(a + (size_t)r * g.W + c) : 0.0f);
+              }
+              acc = d == 0 ? rs : __fadd_rn(acc, rs);
+            }
           }
           K_w[(size_t)n * g.oh * g.ow + o] = __fmul_rn(acc, g.box);
         }
