@@ -410,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
       const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
-      if (FUSED && n != n_ready) {
+      if (FUSED && n != n_ready && !(g.debug & 1024)) {  // debug 1024 (profiling): no waits
         if (lane == 0) wait_image_ready(fsync + g.tiles / g.n_mt + n);
         __syncwarp();
         n_ready = n;
@@ -730,7 +730,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const int t = u / (g.n_nb * g.S), nb = (u / g.S) % g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);
-      if (FUSED && n != n_ready) {
+      if (FUSED && n != n_ready && !(g.debug & 1024)) {  // debug 1024 (profiling): no waits
         if (lane == 0) wait_image_ready(fsync + g.tiles / g.n_mt + n);
         __syncwarp();
         n_ready = n;
@@ -1307,13 +1307,18 @@ int launch_conv_umma_fused(const float* x, const uint8_t* wq, const int32_t* sw,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return XNC_ENOTSUP;
   }
-  g.debug = 0;
+  {  // profiling only (env XNC_FUSED_DEBUG): 1024 = conv roles ignore the ready flags
+     // (results undefined), 2048 = no conv units at all (K1 / K2 alone)
+    static const int dbg = getenv("XNC_FUSED_DEBUG") ? atoi(getenv("XNC_FUSED_DEBUG")) : 0;
+    g.debug = dbg & (1024 | 2048);
+  }
+  if (g.debug & 2048) g.units = 0;
   g.inv_O = (float)(1.0 / (double)O);
   g.tile_major = 0;
   g.k1_upi = cdiv(H * W, 512);
   g.box = (float)(1.0 / (double)(kh * kw));  // <real_t> scale, _kernels_cy.pyx:259
   const int sms = sm_count();
-  const int pairs = g.units < sms / 2 ? g.units : sms / 2;
+  const int pairs = (g.debug & 2048) ? sms / 2 : (g.units < sms / 2 ? g.units : sms / 2);
   if (g.MH != 1) return XNC_ENOTSUP;  // NP > 128 plans run MH = 1
   auto kern = k_conv_umma_pair<1, false, 0, true>;
   if (int rc = smem_opt_in(kern, smem)) return rc;  // per device (xnc_runtime.cu)
