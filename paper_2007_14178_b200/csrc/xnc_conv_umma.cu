@@ -209,6 +209,9 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
 #define XNC_K1U 16
 #endif
 constexpr int kK1U = XNC_K1U;
+constexpr int kK1Ch = 4;      // channels per K1 staging slot (4 x 512 px x 4 B = 8 KB)
+constexpr int kK1Slots = 4;   // K1 staging ring: 32 KB of x in flight per SM (bulk copies, not the LSU)
+constexpr int kK1Stage = kK1Ch * 512 * 4;
 // Coherent global loads for data other CTAs write during the same launch (the
 // packed bits and the K map): the read-only (.nc) path may serve stale lines.
 // (the __ldcg intrinsic: ld.global.cg, reorderable, so batches of them stay in flight)
@@ -249,6 +252,7 @@ struct PairGeom {
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
   int cst_O;    // > 0: sw / alpha staged in shared memory (cst_O entries each, after the B ring)
+  int stages;      // B ring stages in use (kPStages; the fused launch gives two of them to K1)
   int k1_upi;      // FUSED: K1 units (512 pixels of one image) per image
   float box;       // FUSED: f32(1 / (kh * kw)), the K map scale (_kernels_cy.pyx:259)
   int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
@@ -312,13 +316,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
   uint8_t* b_s = a_s + (size_t)g.NA * g.plane_bytes;     // stages x NP/2 rows x 128 B
-  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)kPStages * kPCPS * g.b_half_bytes);  // [cst_O]
+  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)g.stages * kPCPS * g.b_half_bytes);  // [cst_O]
   float* al_s = reinterpret_cast<float*>(sw_s + g.cst_O);                                           // [cst_O]
   float* sc_s = al_s + g.cst_O;  // out affine scale (1 when none)                                   // [cst_O]
   float* sh_s = sc_s + g.cst_O;  // out affine shift (0 when none)                                   // [cst_O]
+  float* k1_s = sh_s + g.cst_O;   // FUSED: K1's x staging ring [kK1Slots][kK1Ch][512 px]
   __shared__ __align__(8) uint64_t b_full[kPStages], b_empty[kPStages];
   __shared__ __align__(8) uint64_t a_full[kPMaxA], a_empty[kPMaxA];
   __shared__ __align__(8) uint64_t t_full[2], t_empty[2];
+  __shared__ __align__(8) uint64_t k1_full[kK1Slots], k1_empty[kK1Slots];  // FUSED: K1's x staging ring
   __shared__ uint32_t tmem_base_s;
 
   const int dbg = PROF ? g.debug : 0;  // profiling switches compile away in the production kernel
@@ -333,6 +339,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       mbar_init(&a_empty[k], 1);
     }
     for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], 2 * kPEpiWarps); }
+    if (FUSED)
+      for (int k = 0; k < kK1Slots; ++k) { mbar_init(&k1_full[k], 1); mbar_init(&k1_empty[k], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();  // barrier inits complete before any role starts (and before the TMEM alloc)
@@ -358,6 +366,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
       const int my_units = units_of(g, cluster, n_clusters);
       const uint32_t total = (uint32_t)my_units * g.KBu * g.taps;
+      const uint32_t n_st = (uint32_t)g.stages;
       uint32_t step = 0;
       for (int iu = 0;; ++iu) {
         const int u = unit_at(g, cluster, n_clusters, iu);
@@ -365,12 +374,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         const int nb = (u / g.S) % g.n_nb, kbu0 = (u % g.S) * g.KBu;
           for (int kb = kbu0; kb < kbu0 + g.KBu; ++kb)
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
-              const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
+              const uint32_t sidx = step / kPCPS, st = sidx % n_st, j = step % kPCPS;
               if (j == 0) {
-                if (sidx >= kPStages) mbar_wait_prof(&b_empty[st], ((sidx / kPStages) - 1) & 1, prof, w_be, XNC_PROD_HINT);
+                if (sidx >= n_st) mbar_wait_prof(&b_empty[st], ((sidx / n_st) - 1) & 1, prof, w_be, XNC_PROD_HINT);
                 const uint32_t n_in = min((uint32_t)kPCPS, total - step);
-                if ((dbg & 256) && sidx >= kPStages) break;  // profiling: no B protocol after the fill
-                if ((dbg & 2) && sidx >= kPStages) {  // profiling: reuse resident chunks, no traffic
+                if ((dbg & 256) && sidx >= n_st) break;  // profiling: no B protocol after the fill
+                if ((dbg & 2) && sidx >= n_st) {  // profiling: reuse resident chunks, no traffic
                   if (leader) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&b_full[st])) : "memory");
                   step += kPCPS - 1 - j;
                   tap += kPCPS - 1;
@@ -541,7 +550,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           int kx = 0;
           for (int tap = 0; tap < g.taps; ++tap, ++step) {
             const unsigned long long tw0 = trace ? clock64() : 0ull;
-            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)kPStages);
+            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)g.stages);
             if (j == 0 && b_proto) {
               mbar_wait_prof(&b_full[st], ph, prof, w_bf);
               asm volatile("tcgen05.fence::after_thread_sync;");
@@ -560,7 +569,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               if (b_proto) umma_commit_pair_elect(&b_empty[st]);
               j = 0;
               ++stages;
-              if (++st == (uint32_t)kPStages) { st = 0; ph ^= 1u; }
+              if (++st == (uint32_t)g.stages) { st = 0; ph ^= 1u; }
             }
           }
           if (!g.a_unit) umma_commit_pair_elect(&a_empty[sl]);
@@ -593,42 +602,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     float* K_w = const_cast<float*>(Kmap);
     int* cnt = fsync;
     int* ready = fsync + N;
+    // x streams through a kK1Slots-deep ring of kK1Ch-channel rows of the unit's 512
+    // pixels, filled by bulk copies (the copy engine, not the LSU: the conv's epilogue
+    // already keeps the LSU busy with y) issued by thread 0 a ring ahead
+    const int lanek = kt & 31, wk = kt >> 5;
+    uint32_t fills = 0, uses = 0;  // ring slots filled (thread 0) / consumed, over all units
     for (int u = blockIdx.x; u < N * g.k1_upi; u += gridDim.x) {
       const int n = u / g.k1_upi, b = u - (u / g.k1_upi) * g.k1_upi;
-      const int p0 = b * 512 + kt * 4;
-      if (p0 < HW) {
-        const float* xp = fx + (size_t)n * g.C * HW + p0;
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int j = 0; j < g.Cw; ++j) {
-          uint32_t word[4] = {0u, 0u, 0u, 0u};
-          const int cend = min(32, g.C - 32 * j);
-          // kK1U channel loads per thread in flight: four warps must keep ~32 KB of x in
-          // flight per SM to stream their share of the batch under the conv
-          for (int c0 = 0; c0 < cend; c0 += kK1U) {
-            float4 v[kK1U];
+      const int pb = b * 512;                  // the unit's first pixel
+      const int npx = min(512, HW - pb);       // a multiple of 4 (host-checked HW % 4 == 0)
+      const int p0 = pb + kt * 4;
+      const int nfill = cdiv(g.C, kK1Ch);
+      const float* xu = fx + (size_t)n * g.C * HW + pb;
+      auto issue = [&](int f) {  // thread 0: fill number `fills` = channels f*kK1Ch .. of this unit
+        const uint32_t sl = fills % kK1Slots;
+        if (fills >= (uint32_t)kK1Slots) mbar_wait(&k1_empty[sl], ((fills / kK1Slots) - 1) & 1);
+        const int nch = min(kK1Ch, g.C - f * kK1Ch);
+        mbar_expect_tx(&k1_full[sl], (uint32_t)(nch * npx * 4));
+        for (int ch = 0; ch < nch; ++ch)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_addr(k1_s) + sl * kK1Stage + ch * 2048),
+              "l"(xu + (size_t)(f * kK1Ch + ch) * HW), "r"(npx * 4), "r"(smem_addr(&k1_full[sl]))
+              : "memory");
+        ++fills;
+      };
+      if (kt == 0)
+        for (int f = 0; f < min(kK1Slots - 1, nfill); ++f) issue(f);
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t word[4] = {0u, 0u, 0u, 0u};
+      for (int f = 0; f < nfill; ++f) {
+        if (kt == 0 && f + kK1Slots - 1 < nfill) issue(f + kK1Slots - 1);
+        const uint32_t sl = uses % kK1Slots;
+        mbar_wait(&k1_full[sl], (uses / kK1Slots) & 1);
+        const int nch = min(kK1Ch, g.C - f * kK1Ch);
+        if (p0 < HW) {
 #pragma unroll
-            for (int uu = 0; uu < kK1U; ++uu)
-              v[uu] = c0 + uu < cend ? __ldcs(reinterpret_cast<const float4*>(xp + (size_t)(32 * j + c0 + uu) * HW))
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int ch = 0; ch < kK1Ch; ++ch) {
+            if (ch < nch) {
+              const int c = f * kK1Ch + ch;
+              const float4 v = *reinterpret_cast<const float4*>(k1_s + sl * (kK1Stage / 4) + ch * 512 + kt * 4);
+              const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int uu = 0; uu < kK1U; ++uu) {
-              if (c0 + uu < cend) {
-                const int cc = c0 + uu;
-                const float e[4] = {v[uu].x, v[uu].y, v[uu].z, v[uu].w};
+              for (int i = 0; i < 4; ++i) {
+                s4[i] = __fadd_rn(s4[i], fabsf(e[i]));
+                word[i] |= (e[i] >= 0.0f ? 1u : 0u) << (c & 31);
+              }
+              if ((c & 31) == 31 || c == g.C - 1) {  // a 32-channel word is complete
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  s4[i] = __fadd_rn(s4[i], fabsf(e[i]));
-                  word[i] |= (e[i] >= 0.0f ? 1u : 0u) << cc;
+                  bits_w[((size_t)n * HW + p0 + i) * g.Cw + (c >> 5)] = word[i];
+                  word[i] = 0u;
                 }
               }
             }
           }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) bits_w[((size_t)n * HW + p0 + i) * g.Cw + j] = word[i];
         }
+        __syncwarp();
+        if (lanek == 0) mbar_arrive_local(&k1_empty[sl]);  // this warp is done with the slot
+        ++uses;
+      }
+      (void)wk;
+      if (p0 < HW)
         *reinterpret_cast<float4*>(fA + (size_t)n * HW + p0) =
             make_float4(__fmul_rn(s4[0], inv), __fmul_rn(s4[1], inv), __fmul_rn(s4[2], inv), __fmul_rn(s4[3], inv));
-      }
       __threadfence();  // this thread's bits / A visible device-wide before the count
       named_bar_sync(8, 128);
       if (kt == 0) k1_last = atomicAdd(cnt + n, 1) == g.k1_upi - 1;
@@ -1118,7 +1155,8 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   // its per-chunk constant loads were L1/L2 misses under the store stream (ncu: the
   // first use after them was the epilogue's top stall, 12 % of samples)
   g.cst_O = O <= 1024 ? round_up(O, 16) : 0;
-  const size_t b_bytes = (size_t)kPStages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 16;
+  g.stages = kPStages;
+  const size_t b_bytes = (size_t)g.stages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 16;
   // A plane ring: two units' planes when they fit (the next unit's planes are
   // built during this unit's MMAs), else fewer; long K (fully connected layers
   // viewed as 1 x N images) streams through the ring.
@@ -1313,6 +1351,12 @@ int launch_conv_umma_fused(const float* x, const uint8_t* wq, const int32_t* sw,
     g.debug = dbg & (1024 | 2048);
   }
   if (g.debug & 2048) g.units = 0;
+  // two B stages make room for K1's x staging ring (4 stages measured ... see DESIGN 4b)
+  {
+    const int drop = kPStages - 4;
+    g.stages = kPStages - drop;
+    smem = smem - (size_t)drop * kPCPS * g.b_half_bytes + (size_t)kK1Slots * kK1Stage;
+  }
   g.inv_O = (float)(1.0 / (double)O);
   g.tile_major = 0;
   g.k1_upi = cdiv(H * W, 512);
