@@ -254,22 +254,6 @@ int xnc_channel_abs_mean_f64(const double* x, int C, int H, int W, double* A, vo
 int xnc_apply_scaling_f64(const int32_t* ints, const double* K, double alpha, long n, double* out,
                           void* stream);
 
-/* ---- the fused layer: K1 -> K2 -> tcgen05 conv in ONE persistent launch ------
- * Same result as xnc_layer_forward_umma (bit-identical y), but K1 runs in four
- * extra warps of the conv's own CTAs, image by image ahead of the convolution
- * (per-image ready flags in the workspace), so x's HBM reads overlap the tensor
- * cores and y's writes instead of preceding them.  workspace:
- * xnc_layer_fused_workspace_bytes() bytes = the layer workspace (bits, A, K) + a
- * sync area that must be ZEROED once when the workspace is allocated; every call
- * leaves it zeroed again (CUDA-graph replays included).  XNC_ENOTSUP when
- * xnc_layer_fused_supported() is 0 (filter blocks <= 128, H*W % 4 != 0, a K split);
- * x must be 16-byte aligned. */
-int xnc_layer_fused_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
-size_t xnc_layer_fused_workspace_bytes(int N, int C, int H, int W, int kh, int kw, int pad);
-int xnc_layer_forward_umma_fused(const float* x, const uint8_t* wq, const int32_t* sw, const float* alpha, int N,
-                                 int C, int H, int W, int O, int kh, int kw, int pad, void* workspace, float* y,
-                                 void* stream);
-
 /* ---- XNOR-Net AlexNet conv1 on the tensor cores (network.py front end) -----
  * The network's full-precision first layer (11x11, stride 4, pad 2, 3 -> 96,
  * 224 x 224 -> 55 x 55) as one tcgen05 kind::tf32 kernel on CTA pairs, reading the

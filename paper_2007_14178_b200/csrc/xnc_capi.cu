@@ -250,27 +250,4 @@ int xnc_layer_forward_umma(const float* x, const uint8_t* wq, const int32_t* sw,
   return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, acc, s);
 }
 
-int xnc_layer_fused_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
-  return conv_shape_ok(N, C, H, W, kh, kw, pad) && O >= 1 && fused_supported(N, C, H, W, O, kh, kw, pad) ? 1 : 0;
-}
-
-size_t xnc_layer_fused_workspace_bytes(int N, int C, int H, int W, int kh, int kw, int pad) {
-  return xnc_layer_workspace_bytes(N, C, H, W, kh, kw, pad) + align256((size_t)(2 * N + 1) * sizeof(int));
-}
-
-int xnc_layer_forward_umma_fused(const float* x, const uint8_t* wq, const int32_t* sw, const float* alpha, int N,
-                                 int C, int H, int W, int O, int kh, int kw, int pad, void* workspace, float* y,
-                                 void* stream) {
-  if (!x || !wq || !sw || !alpha || !workspace || !y || O < 1 || !conv_shape_ok(N, C, H, W, kh, kw, pad))
-    return XNC_EINVAL;
-  if (!fused_supported(N, C, H, W, O, kh, kw, pad)) return XNC_ENOTSUP;
-  const size_t Cw = (C + 31) / 32;
-  char* ws = static_cast<char*>(workspace);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(ws);
-  float* A = reinterpret_cast<float*>(ws + align256((size_t)N * H * W * Cw * 4));
-  float* K = reinterpret_cast<float*>(reinterpret_cast<char*>(A) + align256((size_t)N * H * W * 4));
-  int* sync = reinterpret_cast<int*>(ws + xnc_layer_workspace_bytes(N, C, H, W, kh, kw, pad));
-  return launch_conv_umma_fused(x, wq, sw, alpha, N, C, H, W, O, kh, kw, pad, bits, A, K, sync, y, as_stream(stream));
-}
-
 }  // extern "C"

@@ -204,37 +204,6 @@ __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
                : "memory");
 }
 
-// ---- fused K1 -> K2 -> conv (FUSED kernels, xnc_layer_forward_umma_fused) ------
-#ifndef XNC_K1U
-#define XNC_K1U 16
-#endif
-constexpr int kK1U = XNC_K1U;
-constexpr int kK1Ch = 4;      // channels per K1 staging slot (4 x 512 px x 4 B = 8 KB)
-constexpr int kK1Slots = 4;   // K1 staging ring: 32 KB of x in flight per SM (bulk copies, not the LSU)
-constexpr int kK1Stage = kK1Ch * 512 * 4;
-// Coherent global loads for data other CTAs write during the same launch (the
-// packed bits and the K map): the read-only (.nc) path may serve stale lines.
-// (the __ldcg intrinsic: ld.global.cg, reorderable, so batches of them stay in flight)
-__device__ __forceinline__ uint4 ld_cg_u4(const uint32_t* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
-__device__ __forceinline__ float ld_cg_f32(const float* p) { return __ldcg(p); }
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int r;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
-  return r;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// Wait until image n's bits / A / K are published (ready flag 1).  Bounded: a flag
-// that never arrives traps (a kernel error) instead of hanging the device.
-__device__ __forceinline__ void wait_image_ready(const int* ready) {
-  unsigned spins = 0;
-  while (ld_acquire_gpu(ready) == 0) {
-    __nanosleep(128);
-    if (++spins > (1u << 25)) __trap();
-  }
-}
-
 struct PairGeom {
   int C, H, W, O, kh, kw, pad, oh, ow, IC, KBn, NP, MH, taps, Cw;
   int P;             // extended pixel rows one K-block plane holds
@@ -252,9 +221,6 @@ struct PairGeom {
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
   int cst_O;    // > 0: sw / alpha staged in shared memory (cst_O entries each, after the B ring)
-  int stages;      // B ring stages in use (kPStages; the fused launch gives two of them to K1)
-  int k1_upi;      // FUSED: K1 units (512 pixels of one image) per image
-  float box;       // FUSED: f32(1 / (kh * kw)), the K map scale (_kernels_cy.pyx:259)
   int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
                    // epilogue carries a pixel's running |.| sum and sign words across the blocks)
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
@@ -296,35 +262,24 @@ __device__ __forceinline__ int units_of(const PairGeom& g, int cluster, int n_cl
 // AX = A-producer warps beyond warps 2-3 (after the epilogue warps): at N <= 128 a
 // chunk's four MMAs take half as long as at N = 256 and two producer warps fall
 // behind (C2k3: the issuer waited on a_full for a third of its time).
-// FUSED: four more warps run K1 (sign bits + A of x, 512 pixels of one image per unit,
-// images in order) and, for each image's last unit, K2 (its K map), publishing a
-// per-image ready flag; the A producers and the epilogue wait for the flag of an
-// image before touching its bits / K.  K1 (HBM reads) then overlaps the convolution
-// (tensor cores + y's HBM writes) instead of preceding it.  fx = the float input,
-// fA = A, fsync = [N] unit counters, [N] ready flags, [1] finished-CTA counter (zero
-// on entry, left zero on exit).
-template <int MH, bool PROF, int AX, bool FUSED = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarps + 32 * AX + (FUSED ? 128 : 0), 1)
-    k_conv_umma_pair(
+template <int MH, bool PROF, int AX>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarps + 32 * AX, 1) k_conv_umma_pair(
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
     const PairGeom g, float* __restrict__ y, int32_t* __restrict__ acc_out,
     const float* __restrict__ out_scale, const float* __restrict__ out_shift, int32_t* __restrict__ part,
-    uint32_t* __restrict__ next_bits, float* __restrict__ next_A, const float* __restrict__ fx = nullptr,
-    float* __restrict__ fA = nullptr, int* __restrict__ fsync = nullptr) {
+    uint32_t* __restrict__ next_bits, float* __restrict__ next_A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_s = smem;                                   // KBn planes
   uint8_t* b_s = a_s + (size_t)g.NA * g.plane_bytes;     // stages x NP/2 rows x 128 B
-  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)g.stages * kPCPS * g.b_half_bytes);  // [cst_O]
+  int32_t* sw_s = reinterpret_cast<int32_t*>(b_s + (size_t)kPStages * kPCPS * g.b_half_bytes);  // [cst_O]
   float* al_s = reinterpret_cast<float*>(sw_s + g.cst_O);                                           // [cst_O]
   float* sc_s = al_s + g.cst_O;  // out affine scale (1 when none)                                   // [cst_O]
   float* sh_s = sc_s + g.cst_O;  // out affine shift (0 when none)                                   // [cst_O]
-  float* k1_s = sh_s + g.cst_O;   // FUSED: K1's x staging ring [kK1Slots][kK1Ch][512 px]
   __shared__ __align__(8) uint64_t b_full[kPStages], b_empty[kPStages];
   __shared__ __align__(8) uint64_t a_full[kPMaxA], a_empty[kPMaxA];
   __shared__ __align__(8) uint64_t t_full[2], t_empty[2];
-  __shared__ __align__(8) uint64_t k1_full[kK1Slots], k1_empty[kK1Slots];  // FUSED: K1's x staging ring
   __shared__ uint32_t tmem_base_s;
 
   const int dbg = PROF ? g.debug : 0;  // profiling switches compile away in the production kernel
@@ -339,8 +294,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       mbar_init(&a_empty[k], 1);
     }
     for (int b = 0; b < 2; ++b) { mbar_init(&t_full[b], 1); mbar_init(&t_empty[b], 2 * kPEpiWarps); }
-    if (FUSED)
-      for (int k = 0; k < kK1Slots; ++k) { mbar_init(&k1_full[k], 1); mbar_init(&k1_empty[k], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();  // barrier inits complete before any role starts (and before the TMEM alloc)
@@ -366,7 +319,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const uint32_t full0 = map_to_rank(smem_addr(&b_full[0]), 0);
       const int my_units = units_of(g, cluster, n_clusters);
       const uint32_t total = (uint32_t)my_units * g.KBu * g.taps;
-      const uint32_t n_st = (uint32_t)g.stages;
       uint32_t step = 0;
       for (int iu = 0;; ++iu) {
         const int u = unit_at(g, cluster, n_clusters, iu);
@@ -374,12 +326,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         const int nb = (u / g.S) % g.n_nb, kbu0 = (u % g.S) * g.KBu;
           for (int kb = kbu0; kb < kbu0 + g.KBu; ++kb)
             for (int tap = 0; tap < g.taps; ++tap, ++step) {
-              const uint32_t sidx = step / kPCPS, st = sidx % n_st, j = step % kPCPS;
+              const uint32_t sidx = step / kPCPS, st = sidx % kPStages, j = step % kPCPS;
               if (j == 0) {
-                if (sidx >= n_st) mbar_wait_prof(&b_empty[st], ((sidx / n_st) - 1) & 1, prof, w_be, XNC_PROD_HINT);
+                if (sidx >= kPStages) mbar_wait_prof(&b_empty[st], ((sidx / kPStages) - 1) & 1, prof, w_be, XNC_PROD_HINT);
                 const uint32_t n_in = min((uint32_t)kPCPS, total - step);
-                if ((dbg & 256) && sidx >= n_st) break;  // profiling: no B protocol after the fill
-                if ((dbg & 2) && sidx >= n_st) {  // profiling: reuse resident chunks, no traffic
+                if ((dbg & 256) && sidx >= kPStages) break;  // profiling: no B protocol after the fill
+                if ((dbg & 2) && sidx >= kPStages) {  // profiling: reuse resident chunks, no traffic
                   if (leader) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&b_full[st])) : "memory");
                   step += kPCPS - 1 - j;
                   tap += kPCPS - 1;
@@ -393,8 +345,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       }
       if (prof) g_umma_prof[blockIdx.x][7] = w_be;
     }
-  } else if ((warp >= kPAWarp0 && warp < kPAWarp0 + 2) ||
-             (warp >= kPEpiWarp0 + kPEpiWarps && warp < kPEpiWarp0 + kPEpiWarps + AX)) {
+  } else if ((warp >= kPAWarp0 && warp < kPAWarp0 + 2) || warp >= kPEpiWarp0 + kPEpiWarps) {
     // ================= A producers: packed bits -> swizzled d-bytes, per K block
     const int a_w = warp < kPEpiWarp0 ? warp - kPAWarp0 : 2 + (warp - kPEpiWarp0 - kPEpiWarps);
     const int pt = a_w * 32 + lane, n_pt = (2 + AX) * 32;
@@ -411,7 +362,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     constexpr int kAR = XNC_A_ROWS;
     const int grp = g.a_unit ? g.KBu : 1;
     uint32_t it = 0;  // units of this pair so far: every unit builds its KBu planes
-    int n_ready = -1;  // FUSED: the last image whose bits were seen published
     for (;; ++it) {
       const int u = unit_at(g, cluster, n_clusters, (int)it);
       if (u < 0) break;
@@ -419,11 +369,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);  // this CTA's first pixel
       const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
-      if (FUSED && n != n_ready && !(g.debug & 1024)) {  // debug 1024 (profiling): no waits
-        if (lane == 0) wait_image_ready(fsync + g.tiles / g.n_mt + n);
-        __syncwarp();
-        n_ready = n;
-      }
       for (int kb0 = 0; kb0 < g.KBu; kb0 += grp) {
         const uint32_t use0 = it * g.KBu + kb0;
         // barrier guarding the group's slots: per unit (group it & 1) or per plane
@@ -466,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
                   if (in_img[i] && (k == 0 || two)) {
                     const uint32_t* sk = src + (kbA + k) * 4;
                     if (vec4) {
-                      q[k][i] = FUSED ? ld_cg_u4(sk) : __ldg(reinterpret_cast<const uint4*>(sk));
+                      q[k][i] = __ldg(reinterpret_cast<const uint4*>(sk));
                     } else {
                       const int wl = g.Cw - (kbA + k) * 4;  // words of this block present
                       q[k][i].x = __ldg(sk);
@@ -550,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           int kx = 0;
           for (int tap = 0; tap < g.taps; ++tap, ++step) {
             const unsigned long long tw0 = trace ? clock64() : 0ull;
-            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)g.stages);
+            const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)kPStages);
             if (j == 0 && b_proto) {
               mbar_wait_prof(&b_full[st], ph, prof, w_bf);
               asm volatile("tcgen05.fence::after_thread_sync;");
@@ -569,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               if (b_proto) umma_commit_pair_elect(&b_empty[st]);
               j = 0;
               ++stages;
-              if (++st == (uint32_t)g.stages) { st = 0; ph ^= 1u; }
+              if (++st == (uint32_t)kPStages) { st = 0; ph ^= 1u; }
             }
           }
           if (!g.a_unit) umma_commit_pair_elect(&a_empty[sl]);
@@ -583,138 +528,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         g_umma_prof[blockIdx.x][2] = w_af;
         g_umma_prof[blockIdx.x][3] = w_bf;
         g_umma_prof[blockIdx.x][4] = n_mma;
-      }
-    }
-  } else if (FUSED && warp >= kPEpiWarp0 + kPEpiWarps + AX) {
-    // ================= K1 (+ K2) for the images ahead of the convolution
-    // Unit = (image n, pixels 512b .. 512b+511); this CTA takes units blockIdx.x,
-    // blockIdx.x + gridDim.x, ... in image order.  Per thread: 4 consecutive pixels,
-    // the C channels walked in order with 16-byte streaming loads (k_pack_input's
-    // arithmetic: bit = x >= 0, A = sequential f32 sum of |x| * f32(1/C)); the bit
-    // words go straight to global memory.  The CTA that completes an image's last
-    // unit computes its K map (k_scale_map's op order) and raises the image's flag.
-    __shared__ int k1_last;
-    const int kt = tid - (kPEpiWarp0 + kPEpiWarps + AX) * 32;  // 0..127
-    const int N = g.tiles / g.n_mt;
-    const int HW = g.H * g.W;
-    const float inv = (float)(1.0 / (double)g.C);
-    uint32_t* bits_w = const_cast<uint32_t*>(bits);
-    float* K_w = const_cast<float*>(Kmap);
-    int* cnt = fsync;
-    int* ready = fsync + N;
-    // x streams through a kK1Slots-deep ring of kK1Ch-channel rows of the unit's 512
-    // pixels, filled by bulk copies (the copy engine, not the LSU: the conv's epilogue
-    // already keeps the LSU busy with y) issued by thread 0 a ring ahead
-    const int lanek = kt & 31, wk = kt >> 5;
-    uint32_t fills = 0, uses = 0;  // ring slots filled (thread 0) / consumed, over all units
-    for (int u = blockIdx.x; u < N * g.k1_upi; u += gridDim.x) {
-      const int n = u / g.k1_upi, b = u - (u / g.k1_upi) * g.k1_upi;
-      const int pb = b * 512;                  // the unit's first pixel
-      const int npx = min(512, HW - pb);       // a multiple of 4 (host-checked HW % 4 == 0)
-      const int p0 = pb + kt * 4;
-      const int nfill = cdiv(g.C, kK1Ch);
-      const float* xu = fx + (size_t)n * g.C * HW + pb;
-      auto issue = [&](int f) {  // thread 0: fill number `fills` = channels f*kK1Ch .. of this unit
-        const uint32_t sl = fills % kK1Slots;
-        if (fills >= (uint32_t)kK1Slots) mbar_wait(&k1_empty[sl], ((fills / kK1Slots) - 1) & 1);
-        const int nch = min(kK1Ch, g.C - f * kK1Ch);
-        mbar_expect_tx(&k1_full[sl], (uint32_t)(nch * npx * 4));
-        for (int ch = 0; ch < nch; ++ch)
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_addr(k1_s) + sl * kK1Stage + ch * 2048),
-              "l"(xu + (size_t)(f * kK1Ch + ch) * HW), "r"(npx * 4), "r"(smem_addr(&k1_full[sl]))
-              : "memory");
-        ++fills;
-      };
-      if (kt == 0)
-        for (int f = 0; f < min(kK1Slots - 1, nfill); ++f) issue(f);
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t word[4] = {0u, 0u, 0u, 0u};
-      for (int f = 0; f < nfill; ++f) {
-        if (kt == 0 && f + kK1Slots - 1 < nfill) issue(f + kK1Slots - 1);
-        const uint32_t sl = uses % kK1Slots;
-        mbar_wait(&k1_full[sl], (uses / kK1Slots) & 1);
-        const int nch = min(kK1Ch, g.C - f * kK1Ch);
-        if (p0 < HW) {
-#pragma unroll
-          for (int ch = 0; ch < kK1Ch; ++ch) {
-            if (ch < nch) {
-              const int c = f * kK1Ch + ch;
-              const float4 v = *reinterpret_cast<const float4*>(k1_s + sl * (kK1Stage / 4) + ch * 512 + kt * 4);
-              const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                s4[i] = __fadd_rn(s4[i], fabsf(e[i]));
-                word[i] |= (e[i] >= 0.0f ? 1u : 0u) << (c & 31);
-              }
-              if ((c & 31) == 31 || c == g.C - 1) {  // a 32-channel word is complete
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  bits_w[((size_t)n * HW + p0 + i) * g.Cw + (c >> 5)] = word[i];
-                  word[i] = 0u;
-                }
-              }
-            }
-          }
-        }
-        __syncwarp();
-        if (lanek == 0) mbar_arrive_local(&k1_empty[sl]);  // this warp is done with the slot
-        ++uses;
-      }
-      (void)wk;
-      if (p0 < HW)
-        *reinterpret_cast<float4*>(fA + (size_t)n * HW + p0) =
-            make_float4(__fmul_rn(s4[0], inv), __fmul_rn(s4[1], inv), __fmul_rn(s4[2], inv), __fmul_rn(s4[3], inv));
-      __threadfence();  // this thread's bits / A visible device-wide before the count
-      named_bar_sync(8, 128);
-      if (kt == 0) k1_last = atomicAdd(cnt + n, 1) == g.k1_upi - 1;
-      named_bar_sync(8, 128);
-      if (k1_last) {
-        // K2 for image n from every unit's A (k_scale_map's order: kw-wide row sums from
-        // 0, then the kh row sums top to bottom, times f32(1 / (kh * kw)))
-        __threadfence();
-        const float* a = fA + (size_t)n * HW;
-        // all kh x kw taps of an output loaded before the adds (k <= 3: one round
-        // trip per output instead of one per tap; larger k falls back to a loop)
-        for (int o = kt; o < g.oh * g.ow; o += 128) {
-          const int yy = o / g.ow, xx = o - (o / g.ow) * g.ow;
-          float acc = 0.0f;
-          if (g.kh <= 3 && g.kw <= 3) {
-            float tv[3][3];
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-#pragma unroll
-              for (int e2 = 0; e2 < 3; ++e2) {
-                const int r = yy + d - g.pad, c = xx + e2 - g.pad;
-                tv[d][e2] = (d < g.kh && e2 < g.kw && r >= 0 && r < g.H && c >= 0 && c < g.W)
-                                ? ld_cg_f32(a + (size_t)r * g.W + c) : 0.0f;
-              }
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              if (d >= g.kh) break;
-              float rs = 0.0f;
-#pragma unroll
-              for (int e2 = 0; e2 < 3; ++e2)
-                if (e2 < g.kw) rs = __fadd_rn(rs, tv[d][e2]);
-              acc = d == 0 ? rs : __fadd_rn(acc, rs);
-            }
-          } else {
-            for (int d = 0; d < g.kh; ++d) {
-              const int r = yy + d - g.pad;
-              float rs = 0.0f;
-              for (int e2 = 0; e2 < g.kw; ++e2) {
-                const int c = xx + e2 - g.pad;
-                rs = __fadd_rn(rs, (r >= 0 && r < g.H && c >= 0 && c < g.W) ? ld_cg_f32(a + (size_t)r * g.W + c) : 0.0f);
-              }
-              acc = d == 0 ? rs : __fadd_rn(acc, rs);
-            }
-          }
-          K_w[(size_t)n * g.oh * g.ow + o] = __fmul_rn(acc, g.box);
-        }
-        __threadfence();
-        named_bar_sync(8, 128);
-        if (kt == 0) st_release_gpu(ready + n, 1);
       }
     }
   } else if (warp >= kPEpiWarp0 && warp < kPEpiWarp0 + kPEpiWarps) {
@@ -760,18 +573,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     float emit_sA[MH];  // sign-emitting epilogue: running |.| sum of each pixel across filter blocks
 #pragma unroll
     for (int h = 0; h < MH; ++h) emit_sA[h] = 0.0f;
-    int n_ready = -1;  // FUSED: the last image whose K map was seen published
     for (;; ++item) {
       const int u = unit_at(g, cluster, n_clusters, (int)item);
       if (u < 0) break;
       const int t = u / (g.n_nb * g.S), nb = (u / g.S) % g.n_nb;
       const int n = t / g.n_mt;
       const int m0 = (t - n * g.n_mt) * tile_px + (int)rank * (MH * 128);
-      if (FUSED && n != n_ready && !(g.debug & 1024)) {  // debug 1024 (profiling): no waits
-        if (lane == 0) wait_image_ready(fsync + g.tiles / g.n_mt + n);
-        __syncwarp();
-        n_ready = n;
-      }
       size_t pix[MH], qix[MH];
       bool ok[MH];
       float kv[MH];
@@ -782,7 +589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         ok[h] = rr < g.oh && cc < g.ow;
         qix[h] = (size_t)n * plane_out + (size_t)rr * g.ow + cc;  // output pixel (n, rr, cc)
         pix[h] = (size_t)n * g.O * plane_out + (size_t)rr * g.ow + cc;
-        kv[h] = (ok[h] && (y || next_bits)) ? (FUSED ? ld_cg_f32(Kmap + qix[h]) : __ldg(Kmap + qix[h])) : 0.0f;
+        kv[h] = (ok[h] && (y || next_bits)) ? __ldg(Kmap + qix[h]) : 0.0f;
       }
       const uint32_t buf = item & 1;
       mbar_wait_prof(&t_full[buf], (item >> 1) & 1, prof, w_tf, XNC_EPI_HINT);
@@ -1045,16 +852,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
   }
-  if (FUSED && tid == 0) {
-    // the last CTA to finish zeroes the counters and flags for the next launch
-    const int N = g.tiles / g.n_mt;
-    __threadfence();
-    if (atomicAdd(fsync + 2 * N, 1) == (int)gridDim.x - 1) {
-      for (int i = 0; i < 2 * N; ++i) fsync[i] = 0;
-      fsync[2 * N] = 0;
-      __threadfence();
-    }
-  }
 }
 
 // ---------------------------------------------------------------- weights
@@ -1155,8 +952,7 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   // its per-chunk constant loads were L1/L2 misses under the store stream (ncu: the
   // first use after them was the epilogue's top stall, 12 % of samples)
   g.cst_O = O <= 1024 ? round_up(O, 16) : 0;
-  g.stages = kPStages;
-  const size_t b_bytes = (size_t)g.stages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 16;
+  const size_t b_bytes = (size_t)kPStages * kPCPS * g.b_half_bytes + 1024 + (size_t)g.cst_O * 16;
   // A plane ring: two units' planes when they fit (the next unit's planes are
   // built during this unit's MMAs), else fewer; long K (fully connected layers
   // viewed as 1 x N images) streams through the ring.
@@ -1301,73 +1097,13 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
   g.tile_major = next_bits != nullptr && g.n_nb > 1;
   kern<<<2 * pairs, threads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
-                                          next_bits, next_A, nullptr, nullptr, nullptr);
+                                          next_bits, next_A);
   if (part != nullptr) {
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
     k_split_finalize<<<blocks, 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift, total, O,
                                             (long)g.oh * g.ow, y, acc);
   }
-  return launch_status();
-}
-
-// The fused layer (K1 -> K2 -> conv in one persistent launch, FUSED kernels): for
-// shapes whose plan uses the plain 384-thread launch (filter blocks wider than 128),
-// W*H a multiple of 4 and x 16-byte aligned.  bits / A / K are written by the
-// kernel itself; sync = 2N + 1 ints, zero on entry and left zero.
-bool fused_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
-  PairGeom g;
-  size_t smem;
-  if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return false;
-  return g.NP > 128 && kPAExtra == 0 && (H * W) % 4 == 0 && g.S == 1;
-}
-
-int launch_conv_umma_fused(const float* x, const uint8_t* wq, const int32_t* sw, const float* alpha, int N, int C,
-                           int H, int W, int O, int kh, int kw, int pad, uint32_t* bits, float* A, float* K,
-                           int* sync, float* y, cudaStream_t s) {
-  if (!fused_supported(N, C, H, W, O, kh, kw, pad) || (reinterpret_cast<uintptr_t>(x) & 15) ||
-      (reinterpret_cast<uintptr_t>(A) & 15))
-    return XNC_ENOTSUP;
-  PairGeom g;
-  size_t smem;
-  pair_plan(N, C, H, W, O, kh, kw, pad, g, smem);
-  auto encode = tensor_map_encoder();
-  if (!encode) return XNC_ENOTSUP;
-  CUtensorMap b_map;
-  {
-    const cuuint64_t rows = (cuuint64_t)g.n_nb * g.taps * g.KBn * g.NP;
-    cuuint64_t dims[2] = {128u, rows};
-    cuuint64_t strides[1] = {128u};
-    cuuint32_t box[2] = {128u, (cuuint32_t)(g.NP / 2)};
-    cuuint32_t estr[2] = {1u, 1u};
-    if (encode(&b_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(wq), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return XNC_ENOTSUP;
-  }
-  {  // profiling only (env XNC_FUSED_DEBUG): 1024 = conv roles ignore the ready flags
-     // (results undefined), 2048 = no conv units at all (K1 / K2 alone)
-    static const int dbg = getenv("XNC_FUSED_DEBUG") ? atoi(getenv("XNC_FUSED_DEBUG")) : 0;
-    g.debug = dbg & (1024 | 2048);
-  }
-  if (g.debug & 2048) g.units = 0;
-  // two B stages make room for K1's x staging ring (4 stages measured ... see DESIGN 4b)
-  {
-    const int drop = kPStages - 4;
-    g.stages = kPStages - drop;
-    smem = smem - (size_t)drop * kPCPS * g.b_half_bytes + (size_t)kK1Slots * kK1Stage;
-  }
-  g.inv_O = (float)(1.0 / (double)O);
-  g.tile_major = 0;
-  g.k1_upi = cdiv(H * W, 512);
-  g.box = (float)(1.0 / (double)(kh * kw));  // <real_t> scale, _kernels_cy.pyx:259
-  const int sms = sm_count();
-  const int pairs = (g.debug & 2048) ? sms / 2 : (g.units < sms / 2 ? g.units : sms / 2);
-  if (g.MH != 1) return XNC_ENOTSUP;  // NP > 128 plans run MH = 1
-  auto kern = k_conv_umma_pair<1, false, 0, true>;
-  if (int rc = smem_opt_in(kern, smem)) return rc;  // per device (xnc_runtime.cu)
-  kern<<<2 * pairs, kPThreads + 128, smem, s>>>(bits, b_map, sw, K, alpha, g, y, nullptr, nullptr, nullptr, nullptr,
-                                                nullptr, nullptr, x, A, sync);
   return launch_status();
 }
 

@@ -81,10 +81,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
 // arrive on an mbarrier given by its shared::cluster address (possibly the peer's).
 // Default (.release.cta) semantics: a .cluster release would compile to
 // MEMBAR.ALL.GPU + CCTL.IVALL, stalling each epilogue warp until its streaming

@@ -84,11 +84,8 @@ class XnorConv2d:
         ws = self._ws.get(key)
         if ws is None:
             N, C, H, W = x.shape
-            # sized for the fused launch too; its sync area must start zeroed (the kernel
-            # leaves it zeroed), so the whole buffer is zeroed once here
-            nbytes = max(ops.layer_workspace_bytes(N, C, H, W, self.kh, self.kw, self.pad),
-                         ops.layer_fused_workspace_bytes(N, C, H, W, self.kh, self.kw, self.pad))
-            ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=x.device)
+            nbytes = ops.layer_workspace_bytes(N, C, H, W, self.kh, self.kw, self.pad)
+            ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=x.device)
             self._ws[key] = ws
         return ws
 

@@ -7,7 +7,6 @@ layouts documented in include/xnorb200.h.
 """
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass
 
 import torch
@@ -440,20 +439,6 @@ def layer_workspace_bytes(N: int, C: int, H: int, W: int, kh: int, kw: int, pad:
     return int(lib().xnc_layer_workspace_bytes(N, C, H, W, kh, kw, pad))
 
 
-# XNC_FUSED=0: the three-launch layer (K1, K2, conv) instead of the fused one (A/B runs)
-_FUSED = os.environ.get("XNC_FUSED", "1") != "0"
-
-
-def fused_supported(N: int, C: int, H: int, W: int, O: int, kh: int, kw: int, pad: int) -> bool:
-    """The fused K1 -> K2 -> conv launch (xnc_layer_forward_umma_fused) takes this shape."""
-    return bool(lib().xnc_layer_fused_supported(N, C, H, W, O, kh, kw, pad))
-
-
-def layer_fused_workspace_bytes(N: int, C: int, H: int, W: int, kh: int, kw: int, pad: int) -> int:
-    """Layer workspace plus the fused launch's sync area (zeroed once at allocation)."""
-    return int(lib().xnc_layer_fused_workspace_bytes(N, C, H, W, kh, kw, pad))
-
-
 def layer_forward(x: torch.Tensor, filt: PackedFilters, pad: int, workspace: torch.Tensor,
                   y: torch.Tensor | None = None, acc: torch.Tensor | None = None):
     """K1 -> K2 -> K3+K4 in one C-ABI call (xnc_layer_forward)."""
@@ -484,17 +469,6 @@ def layer_forward_umma(x: torch.Tensor, filt: PackedFilters, pad: int, workspace
     _check_layer_bufs(x, filt, pad, workspace, y, acc)
     if y is None:
         y = torch.empty((N, filt.O, oh, ow), dtype=torch.float32, device=x.device)
-    # one persistent launch (K1 overlapped with the conv) when the workspace carries the
-    # zeroed sync area (XnorConv2d.workspace allocates it) and the shape qualifies
-    if (acc is None and _FUSED and workspace.numel() >= layer_fused_workspace_bytes(N, C, H, W, filt.kh, filt.kw, pad)
-            and fused_supported(N, C, H, W, filt.O, filt.kh, filt.kw, pad)):
-        rc = lib().xnc_layer_forward_umma_fused(x.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(),
-                                                filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
-                                                workspace.data_ptr(), y.data_ptr(), _stream(x.device))
-        if rc == 0:
-            return y
-        if rc != XNC_ENOTSUP:
-            check(rc, "xnc_layer_forward_umma_fused")
     check(lib().xnc_layer_forward_umma(x.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(),
                                        filt.alpha.data_ptr(), N, C, H, W, filt.O, filt.kh, filt.kw, pad,
                                        workspace.data_ptr(), _ptr(y), _ptr(acc), _stream(x.device)),

@@ -602,56 +602,3 @@ def test_host_threads_share_the_library():
         want, ints = O.conv_layer(x, w, 1, want_ints=True)
         assert np.array_equal(acc, ints)
         _assert_float_parity(y, want)
-
-
-@pytest.mark.parametrize("shape", [(4, 256, 56, 56, 256, 3), (3, 256, 20, 36, 384, 3), (1, 160, 24, 24, 256, 5),
-                                   (5, 64, 12, 20, 200, 1), (2, 300, 9, 16, 256, 3)],
-                         ids=lambda s: "x".join(map(str, s)))
-def test_fused_layer_matches_three_launch_layer(shape):
-    """The fused launch (K1 in four extra warps of the conv's CTAs, image by image
-    ahead of the convolution, xnc_layer_forward_umma_fused) writes the same y, bit for
-    bit, as K1 -> K2 -> conv, and both match the oracle on sampled pairs; repeated
-    calls and CUDA-graph replays reuse the self-resetting sync area."""
-    from paper_2007_14178_b200 import XnorConv2d, ops
-    N, C, H, W, O_, k = shape
-    pad = (k - 1) // 2
-    assert ops.fused_supported(N, C, H, W, O_, k, k, pad)
-    rng = np.random.default_rng(list(shape))
-    x = O.f32_exact(rng, (N, C, H, W))
-    w = O.f32_exact(rng, (O_, C, k, k))
-    xd = torch.from_numpy(x).to(_dev())
-    layer = XnorConv2d(torch.from_numpy(w).to(_dev()), pad=pad)
-    assert layer.kernel_for(x.shape) == "umma"
-    ws = layer.workspace(xd)
-    y1 = ops.layer_forward_umma(xd, layer.filters, pad, ws)       # fused (default)
-    y1b = ops.layer_forward_umma(xd, layer.filters, pad, ws)      # again: the sync area was reset
-    ws3 = torch.zeros(ops.layer_workspace_bytes(N, C, H, W, k, k, pad), dtype=torch.uint8, device=_dev())
-    y3 = ops.layer_forward_umma(xd, layer.filters, pad, ws3)      # too small for fused: three launches
-    torch.cuda.synchronize()
-    assert torch.equal(y1.view(torch.int32), y3.view(torch.int32))
-    assert torch.equal(y1b.view(torch.int32), y3.view(torch.int32))
-    n_idx, o_idx = [0, N - 1], [0, O_ // 2, O_ - 1]
-    want = O.conv_layer(x[n_idx], w[o_idx], pad)
-    got = y1[n_idx][:, o_idx].cpu().numpy()
-    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
-    # CUDA graph: replays of the captured fused launch
-    yg = torch.empty_like(y1)
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        ops.layer_forward_umma(xd, layer.filters, pad, ws, y=yg)
-    torch.cuda.current_stream().wait_stream(s)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        ops.layer_forward_umma(xd, layer.filters, pad, ws, y=yg)
-    for _ in range(3):
-        yg.zero_()
-        graph.replay()
-        torch.cuda.synchronize()
-        assert torch.equal(yg.view(torch.int32), y3.view(torch.int32))
-
-
-def test_fused_layer_declines_narrow_filter_blocks():
-    from paper_2007_14178_b200 import ops
-    assert not ops.fused_supported(8, 128, 32, 32, 128, 3, 3, 1)   # N = 128 filter blocks: 512-thread plan
-    assert not ops.fused_supported(2, 64, 7, 7, 256, 3, 3, 1)      # H*W % 4 != 0
