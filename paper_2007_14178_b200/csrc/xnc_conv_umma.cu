@@ -988,10 +988,11 @@ static int sm_count() { return device_sm_count(); }
 // (fully connected layers: one 256-image tile, O / 256 blocks, K up to 36 K blocks
 // of 128 channels per split unit).  1 = no split.
 static int split_factor(const PairGeom& g) {
+  static const int cap = getenv("XNC_UMMA_SPLIT_MAX") ? atoi(getenv("XNC_UMMA_SPLIT_MAX")) : 1 << 20;  // tuning
   const int pairs = sm_count() / 2;
   if (2 * g.units > pairs || g.KBn < 2) return 1;
   int best = 1;
-  for (int d = 2; d <= g.KBn; ++d)
+  for (int d = 2; d <= g.KBn && d <= cap; ++d)
     if (g.KBn % d == 0 && (long)g.units * d <= pairs) best = d;
   return best;
 }
