@@ -180,50 +180,6 @@ __device__ __forceinline__ void umma_chunk_pair(uint32_t d0, int np, uint32_t a_
         "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(d1));
   }
 }
-// The same chunk when only its first KS K = 32 steps carry channels (the last K block
-// of a layer with C % 128 in 1..96: its d-bytes past C are all zero, so the
-// remaining steps would multiply zeros; conv2's C = 96 skips a quarter of its MMAs).
-template <int MH, int KS>
-__device__ __forceinline__ void umma_chunk_pair_ks(uint32_t d0, int np, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
-                                                   uint32_t idesc, uint32_t acc) {
-  static_assert(KS >= 1 && KS <= 3, "partial chunk");
-  if constexpr (MH == 1) {
-    if constexpr (KS == 1)
-      asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
-                   "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
-                   XNC_MMA1("%0", 0, 0, "p") "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi));
-    else if constexpr (KS == 2)
-      asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
-                   "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
-                   XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%0", 2, 2, "t")
-                   "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi));
-    else
-      asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
-                   "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
-                   XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%0", 2, 2, "t") XNC_MMA1("%0", 4, 4, "t")
-                   "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi));
-  } else {
-    const uint32_t d1 = d0 + (uint32_t)np;
-    if constexpr (KS == 1)
-      asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
-                   "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
-                   XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%6", 1024, 0, "p")
-                   "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(d1));
-    else if constexpr (KS == 2)
-      asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
-                   "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
-                   XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%6", 1024, 0, "p")
-                   XNC_MMA1("%0", 2, 2, "t") XNC_MMA1("%6", 1026, 2, "t")
-                   "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(d1));
-    else
-      asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
-                   "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
-                   XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%6", 1024, 0, "p")
-                   XNC_MMA1("%0", 2, 2, "t") XNC_MMA1("%6", 1026, 2, "t")
-                   XNC_MMA1("%0", 4, 4, "t") XNC_MMA1("%6", 1028, 4, "t")
-                   "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(d1));
-  }
-}
 #undef XNC_MMA1
 
 #ifndef XNC_ST_HINT
@@ -537,9 +493,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           }
           uint32_t a_tap = a_lo0 + sl * plane16;
           int kx = 0;
-          // K = 32 steps carrying channels in this block (4 except a partial last block)
-          const int gkb = (u % g.S) * g.KBu + kb;
-          const int ksteps = gkb == g.KBn - 1 ? min(4, (g.C - gkb * 128 + 31) / 32) : 4;
           for (int tap = 0; tap < g.taps; ++tap, ++step) {
             const unsigned long long tw0 = trace ? clock64() : 0ull;
             const bool b_proto = !(PROF && (dbg & 256) && stages >= (uint32_t)kPStages);
@@ -552,11 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               g_umma_prof[512 + step / 8][2 * (step % 8)] = tw0 - t_start;
               g_umma_prof[512 + step / 8][2 * (step % 8) + 1] = tw1 - tw0;
             }
-            const uint32_t b_lo = b_lo0 + (st * kPCPS + j) * b16;
-            if (ksteps == 4) umma_chunk_pair<MH>(d0, g.NP, a_tap, b_lo, hi, idesc, acc);
-            else if (ksteps == 3) umma_chunk_pair_ks<MH, 3>(d0, g.NP, a_tap, b_lo, hi, idesc, acc);
-            else if (ksteps == 2) umma_chunk_pair_ks<MH, 2>(d0, g.NP, a_tap, b_lo, hi, idesc, acc);
-            else umma_chunk_pair_ks<MH, 1>(d0, g.NP, a_tap, b_lo, hi, idesc, acc);
+            umma_chunk_pair<MH>(d0, g.NP, a_tap, b_lo0 + (st * kPCPS + j) * b16, hi, idesc, acc);
             acc = 1;
             if (PROF) n_mma += 4 * MH;
             if (++kx == g.kw) { kx = 0; a_tap += row_skip; } else { a_tap += 8u; }
