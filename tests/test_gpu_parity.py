@@ -503,12 +503,12 @@ def test_layer_chain_with_emitted_signs():
     assert torch.equal(got.view(torch.int32), want.view(torch.int32))
 
 
-def _random_shapes(count, seed):
+def _random_shapes(count, seed, kmax=7):
     rng = np.random.default_rng(seed)
     out = []
     while len(out) < count:
-        k = int(rng.integers(1, 8))
-        kh, kw = (k, k) if rng.random() < 0.7 else (k, int(rng.integers(1, 8)))
+        k = int(rng.integers(1, kmax + 1))
+        kh, kw = (k, k) if rng.random() < 0.7 else (k, int(rng.integers(1, kmax + 1)))
         pad = int(rng.integers(0, 4))
         H, W = int(rng.integers(max(1, kh - 2 * pad), 40)), int(rng.integers(max(1, kw - 2 * pad), 40))
         if H + 2 * pad < kh or W + 2 * pad < kw:
@@ -518,7 +518,8 @@ def _random_shapes(count, seed):
     return out
 
 
-@pytest.mark.parametrize("shape", _random_shapes(48, 2026), ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("shape", _random_shapes(48, 2026) + _random_shapes(40, 8, kmax=8),
+                         ids=lambda s: "x".join(map(str, s)))
 def test_random_shapes_umma_matches_popc(shape):
     """Randomised shapes: the tcgen05 kernel (split K, MH = 1/2, odd channel and filter
     tails, every pad) is bit-identical to the POPC kernel, ints and floats; the
