@@ -65,7 +65,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s, const float* out_scale = nullptr,
                      const float* out_shift = nullptr, int32_t* split_ws = nullptr,
-                     uint32_t* next_bits = nullptr, float* next_A = nullptr);
+                     uint32_t* next_bits = nullptr, float* next_A = nullptr, int y_pm = 0);
 bool umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad);
 int launch_max_pool(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu, const float* bias,

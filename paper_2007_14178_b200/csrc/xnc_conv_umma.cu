@@ -221,6 +221,8 @@ struct PairGeom {
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
   int cst_O;    // > 0: sw / alpha staged in shared memory (cst_O entries each, after the B ring)
+  int y_pm;        // 1: y is written pixel-major, y[n][pixel][O] (a fully connected layer's
+                   // [batch][filters] output); float output only
   int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
                    // epilogue carries a pixel's running |.| sum and sign words across the blocks)
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
@@ -767,6 +769,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           }
           continue;
         }
+        if (g.y_pm && fast && obase + 16 <= g.O) {
+          // pixel-major y (fully connected layers): the thread's 16 filters of its pixel
+          // are 64 contiguous bytes -- four 16-byte stores (O % 4 == 0, host-checked)
+#pragma unroll
+          for (int h = 0; h < MH; ++h) {
+            if (!ok[h]) continue;
+            float* dst = y + qix[h] * g.O + obase;
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              float o4[4];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const int j = 4 * q4 + jj;
+                float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
+                if (out_scale != nullptr) {
+                  const float sc = g.cst_O > 0 ? sc_s[obase + j] : __ldg(out_scale + obase + j);
+                  const float sh = g.cst_O > 0 ? sh_s[obase + j] : __ldg(out_shift + obase + j);
+                  val = __fadd_rn(__fmul_rn(val, sc), sh);
+                }
+                o4[jj] = val;
+              }
+              __stcs(reinterpret_cast<float4*>(dst) + q4, make_float4(o4[0], o4[1], o4[2], o4[3]));
+            }
+          }
+          continue;
+        }
         if (fast && obase + 16 <= g.O) {
           // hot path: float output only, all 16 filters valid (IADD3, I2F, 2 FMUL,
           // address, predicated STG per output); the optional per-filter affine
@@ -823,7 +851,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
             const int o = obase + j;
             if (o < g.O) {
               const int accv = swv[j] - 2 * (int)v[h][j];
-              const size_t idx = pix[h] + (size_t)o * plane_out;
+              const size_t idx = g.y_pm ? qix[h] * g.O + o : pix[h] + (size_t)o * plane_out;
               if (y) {
                 float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
                 if (out_scale != nullptr)
@@ -1015,10 +1043,13 @@ size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, in
 __global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __restrict__ sw,
                                  const float* __restrict__ Kmap, const float* __restrict__ alpha,
                                  const float* __restrict__ out_scale, const float* __restrict__ out_shift,
-                                 long total, int O, long plane, float* __restrict__ y, int32_t* __restrict__ acc) {
+                                 long total, int O, long plane, float* __restrict__ y, int32_t* __restrict__ acc,
+                                 int y_pm) {
   // 32-bit index math (the host guarantees total < 2^31): 64-bit divisions made
   // this kernel 10x slower than its 12 bytes per output
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)total; i += gridDim.x * blockDim.x) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < (int)total; k += gridDim.x * blockDim.x) {
+    // y_pm (N = 1, y pixel-major): k walks y [plane][O] in order, part [O][plane] from L2
+    const int i = y_pm ? (k % O) * (int)plane + k / O : k;
     const int np = i / (int)plane, p = i - np * (int)plane;
     const int n = np / O, o = np - n * O;
     const int accv = __ldg(sw + o) - 2 * part[i];
@@ -1027,7 +1058,7 @@ __global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __re
     if (y) {
       float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + (long)n * plane + p)), __ldg(alpha + o));
       if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
-      y[i] = val;
+      y[y_pm ? k : i] = val;
     }
   }
 }
@@ -1047,7 +1078,7 @@ int umma_profile_read(unsigned long long* host, int n_ctas) {
 int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                      const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                      float* y, int32_t* acc, cudaStream_t s, const float* out_scale,
-                     const float* out_shift, int32_t* split_ws, uint32_t* next_bits, float* next_A) {
+                     const float* out_shift, int32_t* split_ws, uint32_t* next_bits, float* next_A, int y_pm) {
   PairGeom g;
   size_t smem;
   if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
@@ -1097,13 +1128,14 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   }
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
   g.tile_major = next_bits != nullptr && g.n_nb > 1;
+  g.y_pm = y_pm;
   kern<<<2 * pairs, threads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
                                           next_bits, next_A);
   if (part != nullptr) {
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
     k_split_finalize<<<blocks, 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift, total, O,
-                                            (long)g.oh * g.ow, y, acc);
+                                            (long)g.oh * g.ow, y, acc, y_pm);
   }
   return launch_status();
 }

@@ -181,6 +181,11 @@ class XnorConv2d:
         bits, A = p.bits, p.A
         K = ops.scale_map(A, self.kh, self.kw, 0)                     # [N, 1, 1]
         fcf = self._fc_filters(umma=variant == "umma-fc")
+        if variant == "umma-fc" and not want_acc and self.O % 4 == 0:
+            # y written [batch][filters] by the kernel itself (xnc_xnor_conv_umma_fc)
+            y = ops.xnor_conv_fc(bits.view(N, H * W * ops.words(C)), fcf, K.view(N), out=out,
+                                 out_affine=self.out_affine)
+            return y
         y1, acc1 = ops.xnor_conv(bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,
                                  want_acc=want_acc, out_affine=self.out_affine,
                                  variant="umma" if variant == "umma-fc" else "popc")  # [1, O, 1, N]

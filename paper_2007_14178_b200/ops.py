@@ -420,6 +420,27 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
     return y, acc
 
 
+def xnor_conv_fc(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor, out: torch.Tensor | None = None,
+                 out_affine=None) -> torch.Tensor:
+    """Fully connected binary layer on the tcgen05 kernel: bits i32 [P, Cw] (P images as
+    one 1 x P image of filt.C channels, 1 x 1 filters), K f32 [P] -> y f32 [P, O, 1, 1]
+    written [batch][filters] by the kernel (xnc_xnor_conv_umma_fc)."""
+    _need_cuda(bits, "bits", torch.int32)
+    P, Cw = bits.shape
+    if words(filt.C) != Cw or filt.kh != 1 or filt.kw != 1 or filt.wq is None:
+        raise ValueError("xnor_conv_fc takes 1x1 tcgen05 filters matching the bits' channel words")
+    _check_out(K, "K", torch.float32, (P,), bits.device)
+    y = torch.empty((P, filt.O, 1, 1), dtype=torch.float32, device=bits.device) if out is None else out
+    _check_out(y, "out", torch.float32, (P, filt.O, 1, 1), bits.device)
+    osc, osh = _affine(out_affine, filt.O, bits.device, "out_affine")
+    ws_bytes = lib().xnc_umma_split_ws_bytes(1, filt.C, 1, P, filt.O, 1, 1, 0)
+    split_ws = _split_ws(ws_bytes, bits.device) if ws_bytes else None
+    check(lib().xnc_xnor_conv_umma_fc(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), K.data_ptr(),
+                                      filt.alpha.data_ptr(), P, filt.C, filt.O, _ptr(osc), _ptr(osh), _ptr(split_ws),
+                                      y.data_ptr(), _stream(bits.device)), "xnc_xnor_conv_umma_fc")
+    return y
+
+
 def _check_layer_bufs(x, filt, pad, workspace, y, acc) -> None:
     N, C, H, W = x.shape
     oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
