@@ -1043,13 +1043,10 @@ size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, in
 __global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __restrict__ sw,
                                  const float* __restrict__ Kmap, const float* __restrict__ alpha,
                                  const float* __restrict__ out_scale, const float* __restrict__ out_shift,
-                                 long total, int O, long plane, float* __restrict__ y, int32_t* __restrict__ acc,
-                                 int y_pm) {
+                                 long total, int O, long plane, float* __restrict__ y, int32_t* __restrict__ acc) {
   // 32-bit index math (the host guarantees total < 2^31): 64-bit divisions made
   // this kernel 10x slower than its 12 bytes per output
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < (int)total; k += gridDim.x * blockDim.x) {
-    // y_pm (N = 1, y pixel-major): k walks y [plane][O] in order, part [O][plane] from L2
-    const int i = y_pm ? (k % O) * (int)plane + k / O : k;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)total; i += gridDim.x * blockDim.x) {
     const int np = i / (int)plane, p = i - np * (int)plane;
     const int n = np / O, o = np - n * O;
     const int accv = __ldg(sw + o) - 2 * part[i];
@@ -1058,8 +1055,37 @@ __global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __re
     if (y) {
       float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + (long)n * plane + p)), __ldg(alpha + o));
       if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
-      y[y_pm ? k : i] = val;
+      y[i] = val;
     }
+  }
+}
+
+// The same for a fully connected layer's pixel-major y ([P][O], N = 1): 32 x 32 tiles
+// staged in shared memory so part [O][P] is read (and re-zeroed) and y written with
+// whole-sector accesses on both sides.
+__global__ void __launch_bounds__(256) k_split_finalize_pm(int32_t* __restrict__ part, const int32_t* __restrict__ sw,
+                                                           const float* __restrict__ Kmap, const float* __restrict__ alpha,
+                                                           const float* __restrict__ out_scale,
+                                                           const float* __restrict__ out_shift, int O, int P,
+                                                           float* __restrict__ y) {
+  __shared__ float t[32][33];
+  const int o0 = blockIdx.y * 32, p0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int o = o0 + r, p = p0 + tx;
+    if (o < O && p < P) {
+      const int idx = o * P + p;
+      const int accv = __ldg(sw + o) - 2 * part[idx];
+      part[idx] = 0;
+      float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + p)), __ldg(alpha + o));
+      if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
+      t[r][tx] = val;
+    }
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int p = p0 + r, o = o0 + tx;
+    if (o < O && p < P) y[(size_t)p * O + o] = t[tx][r];
   }
 }
 
@@ -1134,8 +1160,12 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   if (part != nullptr) {
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
-    k_split_finalize<<<blocks, 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift, total, O,
-                                            (long)g.oh * g.ow, y, acc, y_pm);
+    if (y_pm)
+      k_split_finalize_pm<<<dim3(cdiv(g.ow, 32), cdiv(O, 32)), 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift,
+                                                                          O, g.ow, y);
+    else
+      k_split_finalize<<<blocks, 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift, total, O,
+                                              (long)g.oh * g.ow, y, acc);
   }
   return launch_status();
 }
