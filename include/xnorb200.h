@@ -180,15 +180,16 @@ int xnc_xnor_conv_umma_ws(const uint32_t* bits, const uint8_t* wq, const int32_t
                           int O, int kh, int kw, int pad, const float* out_scale,
                           const float* out_shift, int32_t* split_ws, float* y, int32_t* acc,
                           void* stream);
-/* A fully connected binary layer on the tcgen05 kernel (network.py's fc6 / fc7):
- * the batch viewed as one 1 x P image of C channels (bits u32 [P][ceil(C/32)], K
- * f32 [P], a 1 x 1 kernel), with y written pixel-major, f32 [P][O] -- the layer's
- * [batch][filters] output, no transpose pass.  split_ws as in xnc_xnor_conv_umma_ws
- * (xnc_umma_split_ws_bytes(1, C, 1, P, O, 1, 1, 0) bytes, zeroed; or NULL).
- * O % 4 == 0, y 16-byte aligned. */
-int xnc_xnor_conv_umma_fc(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
-                          const float* alpha, int P, int C, int O, const float* out_scale, const float* out_shift,
-                          int32_t* split_ws, float* y, void* stream);
+/* xnc_xnor_conv_umma_ws with y written CHANNELS-LAST, f32 [N][H'][W'][O] (the
+ * epilogue's 16 filters of a pixel are 64 contiguous bytes; the K-split finalize
+ * transposes through shared memory).  A fully connected layer (network.py's fc6 /
+ * fc7: the batch as one 1 x P image, kernel 1 x 1) gets its [batch][filters]
+ * output without a transpose pass; a conv gets an NHWC map for the channels-last
+ * pool + K1 that follow it.  Float output only; O % 4 == 0, y 16-byte aligned. */
+int xnc_xnor_conv_umma_nhwc(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
+                            const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
+                            const float* out_scale, const float* out_shift, int32_t* split_ws, float* y,
+                            void* stream);
 /* Profiling only: per-CTA cycle counters of the last tcgen05 conv launched with
  * XNC_UMMA_DEBUG bit 7 set (16 u64 slots per CTA, host memory; blocking copy). */
 int xnc_umma_profile(unsigned long long* host_out, int n_ctas);

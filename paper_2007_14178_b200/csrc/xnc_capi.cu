@@ -200,14 +200,15 @@ int xnc_xnor_conv_umma_ws(const uint32_t* bits, const uint8_t* wq, const int32_t
                           out_scale, out_shift, split_ws);
 }
 
-int xnc_xnor_conv_umma_fc(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
-                          const float* alpha, int P, int C, int O, const float* out_scale, const float* out_shift,
-                          int32_t* split_ws, float* y, void* stream) {
-  if (!bits || !wq || !sw || !K || !alpha || !y || P < 1 || C < 1 || O < 1 || (O & 3) ||
+int xnc_xnor_conv_umma_nhwc(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
+                            const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
+                            const float* out_scale, const float* out_shift, int32_t* split_ws, float* y,
+                            void* stream) {
+  if (!bits || !wq || !sw || !K || !alpha || !y || O < 1 || (O & 3) || !conv_shape_ok(N, C, H, W, kh, kw, pad) ||
       (reinterpret_cast<uintptr_t>(y) & 15) || (!out_scale != !out_shift))
     return XNC_EINVAL;
-  return launch_conv_umma(bits, wq, sw, K, alpha, 1, C, 1, P, O, 1, 1, 0, y, nullptr, as_stream(stream), out_scale,
-                          out_shift, split_ws, nullptr, nullptr, 1);
+  return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, nullptr, as_stream(stream),
+                          out_scale, out_shift, split_ws, nullptr, nullptr, 1);
 }
 
 int xnc_umma_profile(unsigned long long* host_out, int n_ctas) {

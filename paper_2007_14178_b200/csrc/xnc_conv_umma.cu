@@ -221,8 +221,8 @@ struct PairGeom {
   uint32_t b_half_bytes, tmem_cols;
   float inv_O;  // f32(1 / O): the next layer's A scale when the epilogue emits its K1 output
   int cst_O;    // > 0: sw / alpha staged in shared memory (cst_O entries each, after the B ring)
-  int y_pm;        // 1: y is written pixel-major, y[n][pixel][O] (a fully connected layer's
-                   // [batch][filters] output); float output only
+  int y_pm;        // 1: y is written channels-last (pixel-major), y[n][pixel][O] (a fully
+                   // connected layer's [batch][filters] output, or an NHWC map); float output only
   int tile_major;  // 1: a pair takes whole tiles, all n_nb filter blocks back to back (the emitting
                    // epilogue carries a pixel's running |.| sum and sign words across the blocks)
   int debug;  // profiling only (env XNC_UMMA_DEBUG): bit 0 = skip epilogue stores, bit 1 = load B once
@@ -1060,8 +1060,8 @@ __global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __re
   }
 }
 
-// The same for a fully connected layer's pixel-major y ([P][O], N = 1): 32 x 32 tiles
-// staged in shared memory so part [O][P] is read (and re-zeroed) and y written with
+// The same for a channels-last y ([N][P][O], P = H'W'): 32 x 32 (filter, pixel) tiles
+// staged in shared memory so part [N][O][P] is read (and re-zeroed) and y written with
 // whole-sector accesses on both sides.
 __global__ void __launch_bounds__(256) k_split_finalize_pm(int32_t* __restrict__ part, const int32_t* __restrict__ sw,
                                                            const float* __restrict__ Kmap, const float* __restrict__ alpha,
@@ -1069,15 +1069,16 @@ __global__ void __launch_bounds__(256) k_split_finalize_pm(int32_t* __restrict__
                                                            const float* __restrict__ out_shift, int O, int P,
                                                            float* __restrict__ y) {
   __shared__ float t[32][33];
-  const int o0 = blockIdx.y * 32, p0 = blockIdx.x * 32;
+  const int o0 = blockIdx.y * 32, p0 = blockIdx.x * 32, n = blockIdx.z;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  int32_t* pn = part + (size_t)n * O * P;
   for (int r = ty; r < 32; r += 8) {
     const int o = o0 + r, p = p0 + tx;
     if (o < O && p < P) {
-      const int idx = o * P + p;
-      const int accv = __ldg(sw + o) - 2 * part[idx];
-      part[idx] = 0;
-      float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + p)), __ldg(alpha + o));
+      const size_t idx = (size_t)o * P + p;
+      const int accv = __ldg(sw + o) - 2 * pn[idx];
+      pn[idx] = 0;
+      float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + (size_t)n * P + p)), __ldg(alpha + o));
       if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
       t[r][tx] = val;
     }
@@ -1085,7 +1086,7 @@ __global__ void __launch_bounds__(256) k_split_finalize_pm(int32_t* __restrict__
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
     const int p = p0 + r, o = o0 + tx;
-    if (o < O && p < P) y[(size_t)p * O + o] = t[tx][r];
+    if (o < O && p < P) y[((size_t)n * P + p) * O + o] = t[tx][r];
   }
 }
 
@@ -1161,8 +1162,8 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
     if (y_pm)
-      k_split_finalize_pm<<<dim3(cdiv(g.ow, 32), cdiv(O, 32)), 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift,
-                                                                          O, g.ow, y);
+      k_split_finalize_pm<<<dim3(cdiv(g.oh * g.ow, 32), cdiv(O, 32), N), 256, 0, s>>>(
+          part, sw, K, alpha, out_scale, out_shift, O, g.oh * g.ow, y);
     else
       k_split_finalize<<<blocks, 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift, total, O,
                                               (long)g.oh * g.ow, y, acc);

@@ -26,7 +26,7 @@ class XnorConv2d:
     """Binary conv layer with packed weights resident on one device."""
 
     def __init__(self, weight: torch.Tensor, pad: int | None = None, variant: str = "auto",
-                 in_affine=None, out_affine=None, in_pool=None):
+                 in_affine=None, out_affine=None, in_pool=None, out_channels_last: bool = False):
         """in_affine = (scale, shift) f32 [C]: the layer binarizes x*scale + shift
         (a folded batch norm in front of the sign, computed inside K1); out_affine =
         (scale, shift) f32 [O]: y*scale + shift is written instead of y (the next
@@ -35,7 +35,9 @@ class XnorConv2d:
         forward() then takes the pre-pool tensor.
 
         variant: 'auto' (default) runs the tcgen05 kernel whenever its plan fits
-        the shape (kernel_for), else popc; 'umma' / 'popc' / 'b1mma' force one."""
+        the shape (kernel_for), else popc; 'umma' / 'popc' / 'b1mma' force one.
+        out_channels_last=True: the tcgen05 epilogue writes y channels-last ([N][H'][W'][O]
+        memory, same values) -- for a map that a channels-last pool / K1 reads next."""
         if weight.dim() != 4:
             raise ValueError(f"weight must be [O, C, kh, kw], got {tuple(weight.shape)}")
         O, C, kh, kw = weight.shape
@@ -61,6 +63,7 @@ class XnorConv2d:
         self.out_affine = None if out_affine is None else tuple(
             t.detach().to(device=dev, dtype=torch.float32).contiguous() for t in out_affine)
         self.in_pool = None if in_pool is None else (int(in_pool[0]), int(in_pool[1]))
+        self.out_channels_last = bool(out_channels_last)
         self._ws: dict[tuple, torch.Tensor] = {}
 
     @property
@@ -117,6 +120,7 @@ class XnorConv2d:
                         want_acc: bool = False, emit_signs: bool = False):
         variant = self.kernel_for(self.conv_in_shape(x.shape))
         plain = (self.in_affine is None and self.out_affine is None and self.in_pool is None
+                 and not self.out_channels_last
                  and x.is_contiguous() and not want_acc and not emit_signs)
         if variant == "popc" and plain:
             return ops.layer_forward(x, self.filters, self.pad, self.workspace(x), y=out)
@@ -144,6 +148,9 @@ class XnorConv2d:
             if variant != "umma":
                 raise ValueError("emit_signs needs the tcgen05 kernel (variant 'umma' or 'auto')")
             return ops.xnor_conv_emit(p.bits, self.filters, K, self.pad, out_affine=self.out_affine)
+        if (self.out_channels_last and variant == "umma" and not want_acc and self.O % 4 == 0
+                and (out is None or out.is_contiguous(memory_format=torch.channels_last))):
+            return ops.xnor_conv_nhwc(p.bits, self.filters, K, self.pad, out=out, out_affine=self.out_affine)
         y, acc = ops.xnor_conv(p.bits, self.filters, K, self.pad, want_acc=want_acc,
                                variant=variant, y=out, out_affine=self.out_affine)
         return (y, acc) if want_acc else y
@@ -181,10 +188,15 @@ class XnorConv2d:
         bits, A = p.bits, p.A
         K = ops.scale_map(A, self.kh, self.kw, 0)                     # [N, 1, 1]
         fcf = self._fc_filters(umma=variant == "umma-fc")
-        if variant == "umma-fc" and not want_acc and self.O % 4 == 0:
-            # y written [batch][filters] by the kernel itself (xnc_xnor_conv_umma_fc)
-            y = ops.xnor_conv_fc(bits.view(N, H * W * ops.words(C)), fcf, K.view(N), out=out,
-                                 out_affine=self.out_affine)
+        if variant == "umma-fc" and not want_acc and self.O % 4 == 0 and (
+                out is None or out.is_contiguous()):
+            # y written [batch][filters] by the kernel itself (channels-last of a 1 x N image)
+            y = ops.xnor_conv_nhwc(bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,
+                                   out_affine=self.out_affine)                   # [1, O, 1, N] channels-last
+            y = y.permute(0, 3, 2, 1).reshape(N, self.O, 1, 1)                   # a view: memory is [N][O]
+            if out is not None:
+                out.copy_(y)
+                return out
             return y
         y1, acc1 = ops.xnor_conv(bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,
                                  want_acc=want_acc, out_affine=self.out_affine,

@@ -420,25 +420,32 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
     return y, acc
 
 
-def xnor_conv_fc(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor, out: torch.Tensor | None = None,
-                 out_affine=None) -> torch.Tensor:
-    """Fully connected binary layer on the tcgen05 kernel: bits i32 [P, Cw] (P images as
-    one 1 x P image of filt.C channels, 1 x 1 filters), K f32 [P] -> y f32 [P, O, 1, 1]
-    written [batch][filters] by the kernel (xnc_xnor_conv_umma_fc)."""
+def xnor_conv_nhwc(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor, pad: int,
+                   out: torch.Tensor | None = None, out_affine=None) -> torch.Tensor:
+    """tcgen05 K3+K4 with y written channels-last: bits i32 [N,H,W,Cw], K f32
+    [N,H',W'] -> y f32 [N,O,H',W'] in channels-last memory (the kernel writes
+    [N][H'][W'][O] directly, xnc_xnor_conv_umma_nhwc).  Fully connected layers pass
+    the batch as a 1 x P image (N = 1, H = 1, W = P) and view y as [P, O]."""
     _need_cuda(bits, "bits", torch.int32)
-    P, Cw = bits.shape
-    if words(filt.C) != Cw or filt.kh != 1 or filt.kw != 1 or filt.wq is None:
-        raise ValueError("xnor_conv_fc takes 1x1 tcgen05 filters matching the bits' channel words")
-    _check_out(K, "K", torch.float32, (P,), bits.device)
-    y = torch.empty((P, filt.O, 1, 1), dtype=torch.float32, device=bits.device) if out is None else out
-    _check_out(y, "out", torch.float32, (P, filt.O, 1, 1), bits.device)
+    N, H, W, Cw = bits.shape
+    if words(filt.C) != Cw or filt.wq is None:
+        raise ValueError("xnor_conv_nhwc takes tcgen05 filters matching the bits' channel words")
+    oh, ow = out_dims(H, W, filt.kh, filt.kw, pad)
+    _check_out(K, "K", torch.float32, (N, oh, ow), bits.device)
+    if out is None:
+        out = torch.empty((N, filt.O, oh, ow), dtype=torch.float32, device=bits.device,
+                          memory_format=torch.channels_last)
+    elif (tuple(out.shape) != (N, filt.O, oh, ow) or out.dtype != torch.float32 or out.device != bits.device
+          or not out.is_contiguous(memory_format=torch.channels_last)):
+        raise ValueError(f"out must be a channels-last f32 {(N, filt.O, oh, ow)} tensor on {bits.device}")
     osc, osh = _affine(out_affine, filt.O, bits.device, "out_affine")
-    ws_bytes = lib().xnc_umma_split_ws_bytes(1, filt.C, 1, P, filt.O, 1, 1, 0)
+    ws_bytes = lib().xnc_umma_split_ws_bytes(N, filt.C, H, W, filt.O, filt.kh, filt.kw, pad)
     split_ws = _split_ws(ws_bytes, bits.device) if ws_bytes else None
-    check(lib().xnc_xnor_conv_umma_fc(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), K.data_ptr(),
-                                      filt.alpha.data_ptr(), P, filt.C, filt.O, _ptr(osc), _ptr(osh), _ptr(split_ws),
-                                      y.data_ptr(), _stream(bits.device)), "xnc_xnor_conv_umma_fc")
-    return y
+    check(lib().xnc_xnor_conv_umma_nhwc(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), K.data_ptr(),
+                                        filt.alpha.data_ptr(), N, filt.C, H, W, filt.O, filt.kh, filt.kw, pad,
+                                        _ptr(osc), _ptr(osh), _ptr(split_ws), out.data_ptr(), _stream(bits.device)),
+          "xnc_xnor_conv_umma_nhwc")
+    return out
 
 
 def _check_layer_bufs(x, filt, pad, workspace, y, acc) -> None:

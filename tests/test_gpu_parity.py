@@ -603,3 +603,22 @@ def test_host_threads_share_the_library():
         want, ints = O.conv_layer(x, w, 1, want_ints=True)
         assert np.array_equal(acc, ints)
         _assert_float_parity(y, want)
+
+
+@pytest.mark.parametrize("shape", [(3, 96, 27, 27, 256, 5, 2), (2, 384, 13, 13, 256, 3, 1), (1, 64, 9, 11, 132, 3, 0)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_channels_last_output_matches_nchw(shape):
+    """out_channels_last=True: the tcgen05 epilogue writes y [N][H'][W'][O]
+    (xnc_xnor_conv_umma_nhwc); same values, bit for bit, as the NCHW output, with and
+    without the fused out affine."""
+    from paper_2007_14178_b200 import XnorConv2d
+    N, C, H, W, O_, k, pad = shape
+    rng = np.random.default_rng(list(shape))
+    x = torch.from_numpy(O.f32_exact(rng, (N, C, H, W))).to(_dev())
+    w = torch.from_numpy(O.f32_exact(rng, (O_, C, k, k))).to(_dev())
+    aff = (torch.rand(O_, device=_dev()) + 0.5, torch.rand(O_, device=_dev()) - 0.5)
+    for out_aff in (None, aff):
+        a = XnorConv2d(w, pad=pad, out_affine=out_aff)(x)
+        b = XnorConv2d(w, pad=pad, out_affine=out_aff, out_channels_last=True)(x)
+        assert b.is_contiguous(memory_format=torch.channels_last)
+        assert torch.equal(a.view(torch.int32), b.contiguous().view(torch.int32))
