@@ -113,12 +113,11 @@ class XnorNetAlexNet:
             out_aff = self.bn[fused_out[name]] if name in fused_out else None
             # the max-pools after conv2 / conv5 are the next layer's in_pool (our pool kernel)
             in_pool = (3, 2) if name in POOLED_INPUT else None
-            # conv2 / conv5 feed a pool: their epilogue writes the map channels-last, so the
-            # pool and the next K1 take the coalesced channels-last path
-            pooled_next = name in ("conv2", "conv5")
+            # (out_channels_last for conv2 / conv5, so their pools and the next K1 run
+            # channels-last, measured no faster: the NHWC epilogue's per-pixel 64-byte runs
+            # cost what the coalesced pool saves; DESIGN 4b)
             self.binary[name] = XnorConv2d(rnd(cout, cin, k, k), pad=pad, variant=variant,
-                                           in_affine=in_aff, out_affine=out_aff, in_pool=in_pool,
-                                           out_channels_last=pooled_next)
+                                           in_affine=in_aff, out_affine=out_aff, in_pool=in_pool)
         self.fc8_w = rnd(num_classes, 4096, scale=4096 ** -0.5)
         self.fc8_b = rnd(num_classes, scale=0.1)
 
