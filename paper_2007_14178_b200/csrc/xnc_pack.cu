@@ -444,6 +444,74 @@ __global__ void __launch_bounds__(128) k_absmean_wide(const float* __restrict__ 
   }
 }
 
+// K1 of 1 x 1 images with long channel vectors (fc7's 4096-channel input) in ONE
+// pass: per pixel a loader warp streams the vector in 1024-channel chunks into
+// shared memory and emits the sign words with ballots (bit = lane), while lane 0 of
+// a chain warp runs the sequential |.| sum over each chunk as soon as it is staged
+// (bar.arrive / bar.sync handshake per chunk).  Replaces k_pack_words +
+// k_absmean_wide (x read once instead of twice; the chain overlaps the loads).
+__global__ void __launch_bounds__(64) k_pack_wide(const float* __restrict__ x, int C, float inv,
+                                                  uint32_t* __restrict__ bits, float* __restrict__ A,
+                                                  const float* __restrict__ in_scale,
+                                                  const float* __restrict__ in_shift) {
+  extern __shared__ __align__(16) float wide_s[];  // [C] |x'|
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long q = blockIdx.x;
+  const int Cw = C >> 5;
+  const int nchunk = (C + kAbsChunk - 1) / kAbsChunk;  // <= 4 (host-checked C <= kAbsWideMax)
+  if (warp == 0) {
+    const float* xp = x + q * C;
+    for (int k = 0; k < nchunk; ++k) {
+      const int c0 = k * kAbsChunk, n = min(kAbsChunk, C - c0);  // n % 32 == 0
+      float v[kAbsChunk / 32];
+#pragma unroll
+      for (int u = 0; u < kAbsChunk / 32; ++u) v[u] = u * 32 < n ? __ldg(xp + c0 + u * 32 + lane) : 0.0f;
+      if (in_scale != nullptr) {
+#pragma unroll
+        for (int u = 0; u < kAbsChunk / 32; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (u * 32 < n) v[u] = __fadd_rn(__fmul_rn(v[u], __ldg(in_scale + c)), __ldg(in_shift + c));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kAbsChunk / 32; ++u) {
+        if (u * 32 < n) {
+          wide_s[c0 + u * 32 + lane] = fabsf(v[u]);
+          const uint32_t word = __ballot_sync(0xffffffffu, v[u] >= 0.0f);  // bit lane = channel c0+32u+lane
+          if (lane == (u & 31)) bits[q * Cw + (c0 >> 5) + u] = word;
+        }
+      }
+      __threadfence_block();
+      asm volatile("bar.arrive %0, 64;" ::"r"(1 + k) : "memory");  // chunk k staged
+    }
+  } else {
+    float s = 0.0f;
+    for (int k = 0; k < nchunk; ++k) {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + k) : "memory");
+      if (lane == 0) {
+        const int c0 = k * kAbsChunk, n = min(kAbsChunk, C - c0);
+        const float4* b4 = reinterpret_cast<const float4*>(wide_s + c0);
+        const int nb = n >> 5;
+        float4 cur[8], nxt[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur[u] = b4[u];
+        for (int b = 0; b < nb; ++b) {
+          if (b + 1 < nb) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nxt[u] = b4[(b + 1) * 8 + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, cur[u].x), cur[u].y), cur[u].z), cur[u].w);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+        }
+      }
+    }
+    if (lane == 0 && A != nullptr) A[q] = __fmul_rn(s, inv);
+  }
+}
+
 // The two-kernel form of K1 (sign words, then the sequential |.| means): no shared
 // word tile, so it serves any channel count; the preferred form for few pixels with
 // long channel loops.
@@ -452,6 +520,12 @@ static int launch_pack_2d(const float* x, int N, int C, int H, int W, uint32_t* 
   const long npix = (long)N * H * W;
   const int Cw = cdiv(C, 32);
   const long words = npix * Cw;
+  if (H * W == 1 && C >= 1024 && C <= kAbsWideMax && (C & 31) == 0 && npix < 0x7fffffffL) {
+    const size_t sm = (size_t)C * sizeof(float);
+    if (int rc = smem_opt_in(k_pack_wide, sm)) return rc;  // per device (xnc_runtime.cu)
+    k_pack_wide<<<(unsigned)npix, 64, sm, s>>>(x, C, (float)(1.0 / (double)C), bits, A, in_scale, in_shift);
+    return launch_status();
+  }
   k_pack_words<<<(unsigned)cdivl(words, 256), 256, 0, s>>>(x, C, H * W, Cw, npix, bits, in_scale, in_shift);
   if (A && H * W == 1 && C >= 1024 && C <= kAbsWideMax && (C & 3) == 0) {
     const size_t sm = (size_t)4 * C * sizeof(float);
