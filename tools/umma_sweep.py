@@ -24,6 +24,10 @@ SHAPES = {
     "C2k3": (64, 128, 64, 64, 128, 3),
     "C2k5": (64, 128, 64, 64, 128, 5),
     "C2k7": (64, 128, 64, 64, 128, 7),
+    # XNOR-Net AlexNet's binary layers at batch 256 (C4)
+    "conv2": (256, 96, 27, 27, 256, 5),
+    "conv3": (256, 256, 13, 13, 384, 3),
+    "conv5": (256, 384, 13, 13, 256, 3),
 }
 
 
