@@ -264,7 +264,10 @@ __device__ __forceinline__ int units_of(const PairGeom& g, int cluster, int n_cl
 // AX = A-producer warps beyond warps 2-3 (after the epilogue warps): at N <= 128 a
 // chunk's four MMAs take half as long as at N = 256 and two producer warps fall
 // behind (C2k3: the issuer waited on a_full for a third of its time).
-template <int MH, bool PROF, int AX>
+// YPM: y written channels-last ([n][pixel][O], fully connected layers / NHWC maps);
+// a separate instantiation, so the NCHW epilogue's hot loop carries no branch for it
+// (a runtime flag there cost C3 ~5 % in ncu cycles).
+template <int MH, bool PROF, int AX, bool YPM = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarps + 32 * AX, 1) k_conv_umma_pair(
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
@@ -769,7 +772,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           }
           continue;
         }
-        if (g.y_pm && fast && obase + 16 <= g.O) {
+        if (YPM && fast && obase + 16 <= g.O) {
           // pixel-major y (fully connected layers): the thread's 16 filters of its pixel
           // are 64 contiguous bytes -- four 16-byte stores (O % 4 == 0, host-checked)
 #pragma unroll
@@ -851,7 +854,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
             const int o = obase + j;
             if (o < g.O) {
               const int accv = swv[j] - 2 * (int)v[h][j];
-              const size_t idx = g.y_pm ? qix[h] * g.O + o : pix[h] + (size_t)o * plane_out;
+              const size_t idx = YPM ? qix[h] * g.O + o : pix[h] + (size_t)o * plane_out;
               if (y) {
                 float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
                 if (out_scale != nullptr)
@@ -1143,8 +1146,11 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   // N <= 128: four more A-producer warps (C2k3 -9 %; at MH = 2 the 128-register cap
   // of 512 threads costs a few spilled registers, outweighed by the faster A ring)
   const bool wide_a = g.NP <= 128 && kPAExtra == 0;
-  auto kern = wide_a ? (g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true, 4> : k_conv_umma_pair<2, false, 4>)
-                                  : (g.debug ? k_conv_umma_pair<1, true, 4> : k_conv_umma_pair<1, false, 4>))
+  auto kern = y_pm ? (wide_a ? (g.MH == 2 ? k_conv_umma_pair<2, false, 4, true> : k_conv_umma_pair<1, false, 4, true>)
+                             : (g.MH == 2 ? k_conv_umma_pair<2, false, kPAExtra, true>
+                                          : k_conv_umma_pair<1, false, kPAExtra, true>))
+              : wide_a ? (g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true, 4> : k_conv_umma_pair<2, false, 4>)
+                                    : (g.debug ? k_conv_umma_pair<1, true, 4> : k_conv_umma_pair<1, false, 4>))
               : g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true, kPAExtra> : k_conv_umma_pair<2, false, kPAExtra>)
                           : (g.debug ? k_conv_umma_pair<1, true, kPAExtra> : k_conv_umma_pair<1, false, kPAExtra>);
   const int threads = kPThreads + (wide_a ? 32 * 4 : 0);
@@ -1155,7 +1161,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   }
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
   g.tile_major = next_bits != nullptr && g.n_nb > 1;
-  g.y_pm = y_pm;
+  g.y_pm = y_pm;  // (informational: the YPM instantiation is selected above)
   kern<<<2 * pairs, threads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
                                           next_bits, next_A);
   if (part != nullptr) {
