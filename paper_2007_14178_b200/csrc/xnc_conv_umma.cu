@@ -197,6 +197,24 @@ __device__ __forceinline__ void st_cs_pred_v2(const float* p, float a, float b, 
                : "memory");
 }
 
+// Two IEEE round-to-nearest f32 multiplies in one FMUL2 (sm_100 packed f32x2): the
+// same bits as two __fmul_rn, half the epilogue's multiply instructions.
+#ifndef XNC_FMUL2
+#define XNC_FMUL2 1
+#endif
+__device__ __forceinline__ void fmul2_rn(float& o0, float& o1, float a0, float a1, float b0, float b1) {
+#if XNC_FMUL2
+  uint64_t a, b, c;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(c) : "l"(a), "l"(b));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o0), "=f"(o1) : "l"(c));
+#else
+  o0 = __fmul_rn(a0, b0);
+  o1 = __fmul_rn(a1, b1);
+#endif
+}
+
 // streaming (evict-first) store, predicated without a branch
 __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global" XNC_ST_HINT ".f32 [%0], %1;\n\t}" ::"l"(p),
@@ -813,8 +831,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               const float* yp = y + (pix[h] - odd) + (size_t)(obase + odd) * plane_out;
 #pragma unroll
               for (int j = 0; j < 16; j += 2) {
-                const float o0 = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
-                const float o1 = __fmul_rn(__fmul_rn((float)(swv[j + 1] - 2 * (int)v[h][j + 1]), kv[h]), av[j + 1]);
+                float o0, o1;
+                fmul2_rn(o0, o1, (float)(swv[j] - 2 * (int)v[h][j]), (float)(swv[j + 1] - 2 * (int)v[h][j + 1]),
+                         kv[h], kv[h]);
+                fmul2_rn(o0, o1, o0, o1, av[j], av[j + 1]);
                 const float recv = __shfl_xor_sync(0xffffffffu, odd ? o0 : o1, 1);
                 st_cs_pred_v2(yp + j * plane_out32, odd ? recv : o0, odd ? o1 : recv, ok[h]);
               }
@@ -824,9 +844,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
             for (int h = 0; h < MH; ++h) {
               const float* yp = y + pix[h] + (size_t)obase * plane_out;
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const int accv = swv[j] - 2 * (int)v[h][j];
-                st_cs_pred(yp + j * plane_out32, __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]), ok[h]);
+              for (int j = 0; j < 16; j += 2) {
+                float o0, o1;
+                fmul2_rn(o0, o1, (float)(swv[j] - 2 * (int)v[h][j]), (float)(swv[j + 1] - 2 * (int)v[h][j + 1]),
+                         kv[h], kv[h]);
+                fmul2_rn(o0, o1, o0, o1, av[j], av[j + 1]);
+                st_cs_pred(yp + j * plane_out32, o0, ok[h]);
+                st_cs_pred(yp + (j + 1) * plane_out32, o1, ok[h]);
               }
             }
           } else {
