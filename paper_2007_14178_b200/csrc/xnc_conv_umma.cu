@@ -215,6 +215,13 @@ __device__ __forceinline__ void fmul2_rn(float& o0, float& o1, float a0, float a
 #endif
 }
 
+// base + J * stride_bytes in ONE IMAD.WIDE.U32 (J an immediate, stride warp-uniform):
+// the epilogue's per-store 64-bit address arithmetic was three instructions
+// (IMAD + LEA + LEA.HI.X) around every store.
+__device__ __forceinline__ const float* addr_j(const float* base, uint32_t stride_bytes, uint32_t j) {
+  return reinterpret_cast<const float*>(reinterpret_cast<uint64_t>(base) + (uint64_t)j * stride_bytes);
+}
+
 // streaming (evict-first) store, predicated without a branch
 __device__ __forceinline__ void st_cs_pred(const float* p, float v, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global" XNC_ST_HINT ".f32 [%0], %1;\n\t}" ::"l"(p),
@@ -576,6 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
                         ((reinterpret_cast<uintptr_t>(alpha) & 15) == 0);
     // 32-bit filter-plane stride for the hot path (host guarantees O*oh*ow < 2^31)
     const int plane_out32 = g.oh * g.ow;
+    const uint32_t plane_bytes32 = (uint32_t)plane_out32 * 4u;
     const bool fast = y != nullptr && acc_out == nullptr;
     // float2 stores from lane pairs: adjacent extended pixels (2i, 2i+1) share an output
     // row and are both valid or both padding when IC and W' are even; 8-byte aligned
@@ -836,7 +844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
                          kv[h], kv[h]);
                 fmul2_rn(o0, o1, o0, o1, av[j], av[j + 1]);
                 const float recv = __shfl_xor_sync(0xffffffffu, odd ? o0 : o1, 1);
-                st_cs_pred_v2(yp + j * plane_out32, odd ? recv : o0, odd ? o1 : recv, ok[h]);
+                st_cs_pred_v2(addr_j(yp, plane_bytes32, j), odd ? recv : o0, odd ? o1 : recv, ok[h]);
               }
             }
           } else if (out_scale == nullptr) {
@@ -849,8 +857,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
                 fmul2_rn(o0, o1, (float)(swv[j] - 2 * (int)v[h][j]), (float)(swv[j + 1] - 2 * (int)v[h][j + 1]),
                          kv[h], kv[h]);
                 fmul2_rn(o0, o1, o0, o1, av[j], av[j + 1]);
-                st_cs_pred(yp + j * plane_out32, o0, ok[h]);
-                st_cs_pred(yp + (j + 1) * plane_out32, o1, ok[h]);
+                st_cs_pred(addr_j(yp, plane_bytes32, j), o0, ok[h]);
+                st_cs_pred(addr_j(yp, plane_bytes32, j + 1), o1, ok[h]);
               }
             }
           } else {
@@ -863,7 +871,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
                 const float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
                 const float sc = g.cst_O > 0 ? sc_s[obase + j] : __ldg(out_scale + obase + j);
                 const float sh = g.cst_O > 0 ? sh_s[obase + j] : __ldg(out_shift + obase + j);
-                st_cs_pred(yp + j * plane_out32, __fadd_rn(__fmul_rn(val, sc), sh), ok[h]);
+                st_cs_pred(addr_j(yp, plane_bytes32, j), __fadd_rn(__fmul_rn(val, sc), sh), ok[h]);
               }
             }
           }
