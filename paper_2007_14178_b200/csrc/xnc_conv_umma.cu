@@ -508,12 +508,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         const int u = unit_at(g, cluster, n_clusters, (int)item);
         if (u < 0) break;
         const uint32_t buf = item & 1;
-        // every accumulator is first preloaded with S_w by the epilogue (phase 0 for the
-        // first two units), then freed again after each unit's epilogue
-        mbar_wait_prof(&t_empty[buf], (item >> 1) & 1, prof, w_te);
-        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (item >= 2) {
+          mbar_wait_prof(&t_empty[buf], ((item >> 1) - 1) & 1, prof, w_te);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
         const uint32_t d0 = tmem + buf * (MH * g.NP);
-        const uint32_t acc = 1;  // accumulate onto the preload from the first MMA on
+        uint32_t acc = 0;
         for (int kb = 0; kb < g.KBu; ++kb) {
           const uint32_t use = item * g.KBu + kb, sl = use % g.NA;
           if (!g.a_unit || kb == 0) {
@@ -536,6 +536,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               g_umma_prof[512 + step / 8][2 * (step % 8) + 1] = tw1 - tw0;
             }
             umma_chunk_pair<MH>(d0, g.NP, a_tap, b_lo0 + (st * kPCPS + j) * b16, hi, idesc, acc);
+            acc = 1;
             if (PROF) n_mma += 4 * MH;
             if (++kx == g.kw) { kx = 0; a_tap += row_skip; } else { a_tap += 8u; }
             --left;
@@ -603,40 +604,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     float emit_sA[MH];  // sign-emitting epilogue: running |.| sum of each pixel across filter blocks
 #pragma unroll
     for (int h = 0; h < MH; ++h) emit_sA[h] = 0.0f;
-    // Accumulator preload: the B operand is -2 * s_w, so an accumulator that starts at
-    // S_w (the filter's sign sum) ends at S_w - 2 * sum(d * s_w) = the XNOR sum, and the
-    // epilogue converts it directly (no S_w - 2 * acc per output).  Each warp writes
-    // S_w into its lane quadrant of the columns it owns for the unit that will next use
-    // the buffer (split units other than the first start at 0).  The emitting epilogue
-    // preloads from group 0 only, after its last reads of the buffer.
-    const bool emit_mode = next_bits != nullptr;
-    auto preload = [&](uint32_t pbuf, int pu) {
-      const int pnb = (pu / g.S) % g.n_nb;
-      const bool first_split = (pu % g.S) == 0;
-      const uint32_t pbase = tmem + ((uint32_t)(quad * 32) << 16) + pbuf * (MH * g.NP);
-      const int c0 = emit_mode ? 0 : cg, c1 = emit_mode ? (cg == 0 ? n_chunks : 0) : n_chunks;
-      const int cs = emit_mode ? 1 : cstep;
-      for (int ch = c0; ch < c1; ch += cs) {
-        const int ob = pnb * g.NP + ch * 16;
-        uint32_t pv[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int o = ob + j;
-          pv[j] = (first_split && o < g.O) ? (uint32_t)(g.cst_O > 0 ? sw_s[o] : __ldg(sw + o)) : 0u;
-        }
-#pragma unroll
-        for (int h = 0; h < MH; ++h) tmem_st16(pbase + h * g.NP + ch * 16, pv);
-      }
-    };
-    for (uint32_t b = 0; b < 2; ++b) {  // the first two units' accumulators
-      const int ub = unit_at(g, cluster, n_clusters, (int)b);
-      if (ub < 0) break;
-      preload(b, ub);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(t_empty0 + b * 8);
-    }
     for (;; ++item) {
       const int u = unit_at(g, cluster, n_clusters, (int)item);
       if (u < 0) break;
@@ -738,7 +705,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
             uint32_t absv[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              float val = __fmul_rn(__fmul_rn((float)(int)v[h][j], kv[h]), av[j]);
+              float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
               if (out_scale != nullptr) val = __fadd_rn(__fmul_rn(val, osc[j]), osh[j]);
               const bool in = obase + j < g.O;
               absv[j] = in ? __float_as_uint(fabsf(val)) : 0u;
@@ -774,13 +741,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
             for (int h = 0; h < MH; ++h)
               if (ok[h] && next_A != nullptr) next_A[qix[h]] = __fmul_rn(sA[h], g.inv_O);
-          }
-        }
-        {
-          const int u2 = unit_at(g, cluster, n_clusters, (int)item + 2);
-          if (u2 >= 0) {
-            preload(buf, u2);  // group 0 only (all chunks), after its reads above
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -851,7 +811,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj) {
                 const int j = 4 * q4 + jj;
-                float val = __fmul_rn(__fmul_rn((float)(int)v[h][j], kv[h]), av[j]);
+                float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
                 if (out_scale != nullptr) {
                   const float sc = g.cst_O > 0 ? sc_s[obase + j] : __ldg(out_scale + obase + j);
                   const float sh = g.cst_O > 0 ? sh_s[obase + j] : __ldg(out_shift + obase + j);
@@ -880,7 +840,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
               for (int j = 0; j < 16; j += 2) {
                 float o0, o1;
-                fmul2_rn(o0, o1, (float)(int)v[h][j], (float)(int)v[h][j + 1],
+                fmul2_rn(o0, o1, (float)(swv[j] - 2 * (int)v[h][j]), (float)(swv[j + 1] - 2 * (int)v[h][j + 1]),
                          kv[h], kv[h]);
                 fmul2_rn(o0, o1, o0, o1, av[j], av[j + 1]);
                 const float recv = __shfl_xor_sync(0xffffffffu, odd ? o0 : o1, 1);
@@ -894,7 +854,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
               for (int j = 0; j < 16; j += 2) {
                 float o0, o1;
-                fmul2_rn(o0, o1, (float)(int)v[h][j], (float)(int)v[h][j + 1],
+                fmul2_rn(o0, o1, (float)(swv[j] - 2 * (int)v[h][j]), (float)(swv[j + 1] - 2 * (int)v[h][j + 1]),
                          kv[h], kv[h]);
                 fmul2_rn(o0, o1, o0, o1, av[j], av[j + 1]);
                 st_cs_pred(addr_j(yp, plane_bytes32, j), o0, ok[h]);
@@ -907,7 +867,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               const float* yp = y + pix[h] + (size_t)obase * plane_out;
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-                const int accv = (int)v[h][j];
+                const int accv = swv[j] - 2 * (int)v[h][j];
                 const float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
                 const float sc = g.cst_O > 0 ? sc_s[obase + j] : __ldg(out_scale + obase + j);
                 const float sh = g.cst_O > 0 ? sh_s[obase + j] : __ldg(out_shift + obase + j);
@@ -925,7 +885,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           for (int j = 0; j < 16; ++j) {
             const int o = obase + j;
             if (o < g.O) {
-              const int accv = (int)v[h][j];
+              const int accv = swv[j] - 2 * (int)v[h][j];
               const size_t idx = YPM ? qix[h] * g.O + o : pix[h] + (size_t)o * plane_out;
               if (y) {
                 float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
@@ -936,13 +896,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               if (acc_out) acc_out[idx] = accv;
             }
           }
-        }
-      }
-      {
-        const int u2 = unit_at(g, cluster, n_clusters, (int)item + 2);
-        if (u2 >= 0) {
-          preload(buf, u2);  // the warp's own chunks, all read above
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -987,9 +940,7 @@ __global__ void k_pack_weights_umma(const T* __restrict__ w, int O, int C, int k
       const int c = kb * 128 + q * 16 + b;
       if (c < C) {
         const T v = w[((long)o * C + c) * kh * kw + tap];
-        // -2 * sign: the accumulator starts at S_w (preloaded by the epilogue), so after
-        // the MMAs it holds S_w - 2 * sum(d * s_w), the XNOR sum itself
-        const uint32_t sgn = v >= T(0) ? 0xFEu : 0x02u;
+        const uint32_t sgn = v >= T(0) ? 0x01u : 0xFFu;
         vals[b >> 2] |= sgn << ((b & 3) * 8);
       }
     }
@@ -1133,7 +1084,7 @@ __global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __re
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)total; i += gridDim.x * blockDim.x) {
     const int np = i / (int)plane, p = i - np * (int)plane;
     const int n = np / O, o = np - n * O;
-    const int accv = part[i];  // the split units' partial accumulators (S_w preloaded in split 0's)
+    const int accv = __ldg(sw + o) - 2 * part[i];
     part[i] = 0;
     if (acc) acc[i] = accv;
     if (y) {
@@ -1160,7 +1111,7 @@ __global__ void __launch_bounds__(256) k_split_finalize_pm(int32_t* __restrict__
     const int o = o0 + r, p = p0 + tx;
     if (o < O && p < P) {
       const size_t idx = (size_t)o * P + p;
-      const int accv = pn[idx];
+      const int accv = __ldg(sw + o) - 2 * pn[idx];
       pn[idx] = 0;
       float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + (size_t)n * P + p)), __ldg(alpha + o));
       if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
