@@ -3,7 +3,7 @@
 kernel, so a run that the tool slows down still proves the results.
 
     compute-sanitizer --tool racecheck --kernel-name regex=xnc python tools/sanitize_cases.py [group ...]
-groups: pack scale popc b1mma umma umma_bulk umma_emit umma_split network conv1 interop verify (default: all)
+groups: pack scale popc b1mma umma umma_bulk umma_emit umma_split fc_nhwc pack_wide pool_k1 network conv1 interop verify (default: all)
 """
 import os
 import sys
@@ -94,6 +94,41 @@ def case_umma_split(rng):
     want = O.conv_layer(x, w, 0)
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy().reshape(want.shape).view(np.uint32), want.view(np.uint32))
+
+
+def case_fc_nhwc(rng):
+    # fully connected layer on the tcgen05 kernel: K split + pixel-major finalize, and the
+    # unsplit channels-last epilogue (out_channels_last)
+    x, w = O.f32_exact(rng, (96, 256, 3, 3)), O.f32_exact(rng, (512, 256, 3, 3))
+    layer, xd = _layer(x, w, 0, "auto")
+    assert layer.kernel_for(x.shape) == "umma-fc"
+    y = layer.forward(xd)
+    want = O.conv_layer(x, w, 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy().reshape(want.shape).view(np.uint32), want.view(np.uint32))
+    x2, w2 = O.f32_exact(rng, (2, 64, 9, 11)), O.f32_exact(rng, (132, 64, 3, 3))
+    a = XnorConv2d(torch.from_numpy(w2).cuda(), pad=1)(torch.from_numpy(x2).cuda())
+    b = XnorConv2d(torch.from_numpy(w2).cuda(), pad=1, out_channels_last=True)(torch.from_numpy(x2).cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(a, b.contiguous())
+
+
+def case_pack_wide(rng):
+    # K1 of 1 x 1 images with 4096 channels (fc7's input): ballot words + overlapped chain
+    x = O.f32_exact(rng, (5, 4096, 1, 1))
+    bits, A = ops.pack_input(torch.from_numpy(x).cuda())
+    A_ref, _ = O.scale_map_f32(x[0], 1, 1, 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(A[0].cpu().numpy().view(np.uint32), A_ref.view(np.uint32))
+
+
+def case_pool_k1(rng):
+    # max-pool fused into K1 (conv3 / fc6 inputs)
+    x = torch.from_numpy(O.f32_exact(rng, (2, 96, 27, 27))).cuda()
+    b1, a1 = ops.pack_input(x, in_pool=(3, 2))
+    b2, a2 = ops.pack_input(ops.max_pool(x, 3, 2))
+    torch.cuda.synchronize()
+    assert torch.equal(b1, b2) and torch.equal(a1, a2)
 
 
 def case_network(rng):
