@@ -1177,7 +1177,10 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   const int pairs = work < sms / 2 ? work : sms / 2;
   // N <= 128: four more A-producer warps (C2k3 -9 %; at MH = 2 the 128-register cap
   // of 512 threads costs a few spilled registers, outweighed by the faster A ring)
-  const bool wide_a = g.NP <= 128 && kPAExtra == 0;
+  // 1 x 1 taps (fully connected layers): each A plane feeds only 4 MMAs instead of 4 per
+  // tap, so the producers need the extra warps there too (XNC_WIDE_A_1X1=0: off, A/B runs)
+  static const int wide_1x1 = getenv("XNC_WIDE_A_1X1") ? atoi(getenv("XNC_WIDE_A_1X1")) : 1;
+  const bool wide_a = (g.NP <= 128 || (wide_1x1 && g.taps == 1)) && kPAExtra == 0;
   auto kern = y_pm ? (wide_a ? (g.MH == 2 ? k_conv_umma_pair<2, false, 4, true> : k_conv_umma_pair<1, false, 4, true>)
                              : (g.MH == 2 ? k_conv_umma_pair<2, false, kPAExtra, true>
                                           : k_conv_umma_pair<1, false, kPAExtra, true>))
