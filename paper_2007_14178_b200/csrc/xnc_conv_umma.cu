@@ -189,7 +189,8 @@ __device__ __forceinline__ void umma_chunk_pair(uint32_t d0, int np, uint32_t a_
 #define XNC_EMIT_SPLIT 8
 #endif
 #ifndef XNC_PAIR_ST
-#define XNC_PAIR_ST 1
+#define XNC_PAIR_ST 0  // lane-pair float2 stores: -5 % at C2k3 in round 1, +5 % since the
+                       // one-instruction store addresses (profiles/umma_pairst_ab_r3.log)
 #endif
 __device__ __forceinline__ void st_cs_pred_v2(const float* p, float a, float b, bool pred) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global" XNC_ST_HINT ".v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p),
