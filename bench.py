@@ -661,7 +661,9 @@ def run_network(args, cfg_name):
         res = {"metric": METRIC, "value": bops / (ms * 1e-3) / 1e9, "unit": "Gbinop/s", "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                "scaling": "strong" if cfg_name == "C5" else "weak", "vs_baseline": None,
-               "dtype": "1-bit signs (binary layers); conv1 / fc8 full precision on cuDNN / cuBLAS with TF32",
+               "dtype": ("1-bit signs (binary layers); conv1 f32 in / TF32 multiply on our tcgen05 kernel; fc8 cuBLAS TF32"
+                         if net.conv1 == "tcgen05" else
+                         "1-bit signs (binary layers); conv1 / fc8 full precision on cuDNN / cuBLAS with TF32"),
                "data": "synthetic U(-1,1), random-init weights",
                "config": {"workload": CONFIG_TEXT[cfg_name], "name": cfg_name, "global_batch": gb,
                           "batch_per_gpu": N, "variant": args.variant,
