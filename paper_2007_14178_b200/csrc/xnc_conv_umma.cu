@@ -89,9 +89,31 @@ constexpr int kPThreads = 128 + 32 * kPEpiWarps + 32 * kPAExtra;
 #ifndef XNC_PCPS
 #define XNC_PCPS 1
 #endif
+// Operand format of the binary GEMM.  1: tcgen05.mma kind::mxf4 -- d and
+// the filter signs as E2M1 nibbles (d: 0 or 1.0, s_w: +-1.0, 0 for tail channels),
+// every UE8M0 block scale 2^0, f32 accumulators.  Every product is 0 or +-1 and
+// every partial sum an integer below 2^24, so the f32 sums are exact: the same
+// integers as kind::i8, at twice the MACs per cycle (16384 vs 8192 per SM per clock,
+// 128-cycle M=256 x N=256 MMAs either way, profiles/mxf4_probe_r3.jsonl) because a
+// 128-byte K row carries 256 channels instead of 128.  0 (default): kind::i8 (u8
+// d-bytes x s8 signs, s32 accumulators).  Both pass every parity test; kind::mxf4 is
+// not the default because the kernel does not get faster with it: the MMAs are not
+// what bounds it.  Measured (profiles/umma_fp4_ab_r4.log): C3 0.39 vs 0.30 ms, C2k3
+// 0.073 vs 0.046 -- the 240-filter cap splits O = 256 into two blocks (A built twice,
+// twice the units), C = 128 fills only half of a 256-channel K row, the B stream has
+// to arrive twice as fast per MMA-cycle, and with B and A resident (debug 6) the
+// epilogue alone still takes 0.29-0.33 ms at C3; conv3 / conv5 of the network are
+// 5-7 % faster (0.042 vs 0.044, 0.043 vs 0.047 ms).  Build with -DXNC_UMMA_FP4=1.
+#ifndef XNC_UMMA_FP4
+#define XNC_UMMA_FP4 0
+#endif
+constexpr int kKBc = XNC_UMMA_FP4 ? 256 : 128;  // channels per K block (one 128-byte operand row)
+constexpr int kKBw = kKBc / 32;                  // sign words per K block
+constexpr int kSfCols = XNC_UMMA_FP4 ? 32 : 0;   // TMEM columns of scale factors (0x7F = 2^0)
+constexpr int kMaxNP = XNC_UMMA_FP4 ? 240 : 256;  // two accumulators + the scale columns <= 512
 constexpr int kPStages = XNC_PSTAGES;  // B pipeline depth (stages)
 constexpr int kPCPS = XNC_PCPS;        // (tap, K block) chunks per B stage: one wait + one commit each
-constexpr int kPMaxKB = 4;       // K blocks (128 channels each) of a tile resident: C <= 512
+constexpr int kPMaxKB = 4;       // K blocks of a tile resident (C <= 4 * kKBc)
 constexpr int kPMaxA = 2 * kPMaxKB;  // A plane ring: two tiles' planes when they fit
 constexpr int kPAWarp0 = 2;      // first A-producer warp
 constexpr int kPEpiWarp0 = 4;    // first epilogue warp
@@ -156,18 +178,24 @@ __device__ __forceinline__ void umma_i8_pair_elect(uint32_t tmem_d, uint64_t ade
 // instructions instead of ~100 (an elect, R2URs and 64-bit adds per MMA).  The
 // issuer shares its SM sub-partition with four busy epilogue warps; every
 // instruction it saves is issue latency the tensor pipe does not wait on.
+#if XNC_UMMA_FP4
+#define XNC_MMA_OP(D, P) "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [" D "], a, b, %3, [%7], [%7], " P ";\n\t"
+#else
+#define XNC_MMA_OP(D, P) "@e tcgen05.mma.cta_group::2.kind::i8 [" D "], a, b, %3, " P ";\n\t"
+#endif
 #define XNC_MMA1(D, AO, BO, P)                                                              \
   "add.u32 al, %1, " #AO ";\n\tadd.u32 bl, %2, " #BO ";\n\tmov.b64 a, {al, %5};\n\t"   \
-  "mov.b64 b, {bl, %5};\n\t@e tcgen05.mma.cta_group::2.kind::i8 [" D "], a, b, %3, " P ";\n\t"
+  "mov.b64 b, {bl, %5};\n\t" XNC_MMA_OP(D, P)
+// sf: TMEM address of the scale-factor columns (kind::mxf4; unused for kind::i8)
 template <int MH>
 __device__ __forceinline__ void umma_chunk_pair(uint32_t d0, int np, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
-                                                uint32_t idesc, uint32_t acc) {
+                                                uint32_t idesc, uint32_t acc, uint32_t sf) {
   if constexpr (MH == 1) {
     asm volatile(
         "{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
         XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%0", 2, 2, "t") XNC_MMA1("%0", 4, 4, "t") XNC_MMA1("%0", 6, 6, "t")
-        "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi));
+        "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(0u), "r"(sf));
   } else {
     const uint32_t d1 = d0 + (uint32_t)np;
     asm volatile(
@@ -177,10 +205,11 @@ __device__ __forceinline__ void umma_chunk_pair(uint32_t d0, int np, uint32_t a_
         XNC_MMA1("%0", 2, 2, "t") XNC_MMA1("%6", 1026, 2, "t")
         XNC_MMA1("%0", 4, 4, "t") XNC_MMA1("%6", 1028, 4, "t")
         XNC_MMA1("%0", 6, 6, "t") XNC_MMA1("%6", 1030, 6, "t")
-        "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(d1));
+        "}" ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(d1), "r"(sf));
   }
 }
 #undef XNC_MMA1
+#undef XNC_MMA_OP
 
 #ifndef XNC_ST_HINT
 #define XNC_ST_HINT ".cs"
@@ -268,6 +297,39 @@ __device__ __forceinline__ uint4 d_bytes16(uint32_t bits16, uint32_t valid16) {
   return r;
 }
 
+// 8 bits -> 8 E2M1 nibbles (kind::mxf4 A operand): bit n -> nibble n = 0x2 (1.0) or
+// 0x0.  Three multiply-and-mask steps, each multiply a disjoint OR of two shifts.
+__device__ __forceinline__ uint32_t spread8_nib(uint32_t b) {
+  uint32_t x = (b * 0x1001u) & 0x000F000Fu;  // bits 0-3 | 4-7 -> 16-19
+  x = (x * 0x41u) & 0x03030303u;             // pairs per byte
+  return (x * 18u) & 0x22222222u;            // bit n -> 4n + 1
+}
+
+// 32 sign bits -> 32 d-nibbles (16 bytes; byte j = channels 2j (low nibble), 2j + 1)
+__device__ __forceinline__ uint4 d_nibbles32(uint32_t bits, uint32_t valid) {
+  const uint32_t d = ~bits & valid;
+  return make_uint4(spread8_nib(d & 0xFFu), spread8_nib((d >> 8) & 0xFFu), spread8_nib((d >> 16) & 0xFFu),
+                    spread8_nib(d >> 24));
+}
+
+// accumulator word -> the integer sum d . s_w (kind::mxf4: an exact f32 integer)
+__device__ __forceinline__ int acc_raw(uint32_t v) {
+#if XNC_UMMA_FP4
+  return __float2int_rz(__uint_as_float(v));
+#else
+  return (int)v;
+#endif
+}
+
+// S_w - 2 * acc as f32 (exact: integers below 2^24)
+__device__ __forceinline__ float acc_val(int sw, uint32_t v) {
+#if XNC_UMMA_FP4
+  return __fmaf_rn(__uint_as_float(v), -2.0f, (float)sw);
+#else
+  return (float)(sw - 2 * (int)v);
+#endif
+}
+
 // The i-th work unit of CTA pair `cluster` (-1 past the end): units strided over the
 // pairs, or, tile-major, whole tiles strided over the pairs with their filter blocks
 // back to back.  Every role walks the same sequence.
@@ -340,6 +402,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_s;
   const int tile_px = 2 * MH * 128;
+#if XNC_UMMA_FP4
+  // every block scale factor = 2^0 (UE8M0 0x7F in every byte of the scale columns, all
+  // 128 lanes of both CTAs): the MMAs then sum plain E2M1 products
+  if (warp >= kPEpiWarp0 && warp < kPEpiWarp0 + 4) {
+    uint32_t ones[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) ones[j] = 0x7F7F7F7Fu;
+    const uint32_t t = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (g.tmem_cols - (uint32_t)kSfCols);
+#pragma unroll
+    for (int c = 0; c < kSfCols; c += 16) tmem_st16(t + c, ones);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+#endif
 
   if (warp == 0) {
     // ================= B producer: this CTA's NP/2 filter rows of every chunk,
@@ -415,18 +493,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
             const int kbA = kbu0 + kb0 + kp;  // global K block of the first plane
             const bool two = kp + 1 < grp;
             uint8_t* planes[2];
-            uint32_t vmask[2][4];  // valid-channel masks of each block's four words
+            constexpr int NQ = kKBw / 4;  // 16-byte loads per pixel and K block
+            uint32_t vmask[2][kKBw];      // valid-channel masks of each block's words
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               planes[k] = a_s + (size_t)((use0 + kp + k) % g.NA) * g.plane_bytes;
 #pragma unroll
-              for (int w = 0; w < 4; ++w) {
-                const int rem = g.C - ((kbA + k) * 128 + w * 32);
+              for (int w = 0; w < kKBw; ++w) {
+                const int rem = g.C - ((kbA + k) * kKBc + w * 32);
                 vmask[k][w] = rem >= 32 ? 0xFFFFFFFFu : rem <= 0 ? 0u : ((1u << rem) - 1u);
               }
             }
             for (int r0 = 0; r0 < g.P; r0 += n_pt * kAR) {
-              uint4 q[2][kAR];
+              uint4 q[2][kAR][NQ];
               bool in_img[kAR];
 #pragma unroll
               for (int i = 0; i < kAR; ++i) {
@@ -437,21 +516,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
                 in_img[i] = p < g.P && r >= 0 && r < g.H && c >= 0 && c < g.W;
                 const uint32_t* src = img + ((size_t)(in_img[i] ? r : 0) * g.W + (in_img[i] ? c : 0)) * g.Cw;
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                  q[k][i] = make_uint4(0u, 0u, 0u, 0u);
-                  if (in_img[i] && (k == 0 || two)) {
-                    const uint32_t* sk = src + (kbA + k) * 4;
-                    if (vec4) {
-                      q[k][i] = __ldg(reinterpret_cast<const uint4*>(sk));
-                    } else {
-                      const int wl = g.Cw - (kbA + k) * 4;  // words of this block present
-                      q[k][i].x = __ldg(sk);
-                      if (wl > 1) q[k][i].y = __ldg(sk + 1);
-                      if (wl > 2) q[k][i].z = __ldg(sk + 2);
-                      if (wl > 3) q[k][i].w = __ldg(sk + 3);
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                  for (int u = 0; u < NQ; ++u) {
+                    q[k][i][u] = make_uint4(0u, 0u, 0u, 0u);
+                    const int wl = g.Cw - (kbA + k) * kKBw - 4 * u;  // words present from this load on
+                    if (in_img[i] && (k == 0 || two) && wl > 0) {
+                      const uint32_t* sk = src + (kbA + k) * kKBw + 4 * u;
+                      if (vec4 && wl >= 4) {
+                        q[k][i][u] = __ldg(reinterpret_cast<const uint4*>(sk));
+                      } else {
+                        q[k][i][u].x = __ldg(sk);
+                        if (wl > 1) q[k][i][u].y = __ldg(sk + 1);
+                        if (wl > 2) q[k][i][u].z = __ldg(sk + 2);
+                        if (wl > 3) q[k][i][u].w = __ldg(sk + 3);
+                      }
                     }
                   }
-                }
               }
 #pragma unroll
               for (int i = 0; i < kAR; ++i) {
@@ -460,14 +541,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                   if (k == 1 && !two) continue;
-                  const uint32_t wd[4] = {q[k][i].x, q[k][i].y, q[k][i].z, q[k][i].w};
+                  uint32_t wd[kKBw];
+#pragma unroll
+                  for (int u = 0; u < NQ; ++u) {
+                    wd[4 * u] = q[k][i][u].x; wd[4 * u + 1] = q[k][i][u].y;
+                    wd[4 * u + 2] = q[k][i][u].z; wd[4 * u + 3] = q[k][i][u].w;
+                  }
                   uint8_t* row = planes[k] + (size_t)p * 128;
 #pragma unroll
                   for (int h = 0; h < 8; ++h) {
+#if XNC_UMMA_FP4
+                    // 16-byte chunk h = word h: 32 channels as nibbles (padding pixel: all d = 0)
+                    const uint4 chunk = d_nibbles32(wd[h], in_img[i] ? vmask[k][h] : 0u);
+#else
+                    // 16-byte chunk h = half word h: 16 channels as bytes
                     const uint32_t b16 = (wd[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
-                    // padding pixel: all d = 0
                     const uint32_t v16 = in_img[i] ? (vmask[k][h >> 1] >> ((h & 1) * 16)) & 0xFFFFu : 0u;
-                    *reinterpret_cast<uint4*>(row + ((h ^ (p & 7)) << 4)) = d_bytes16(b16, v16);
+                    const uint4 chunk = d_bytes16(b16, v16);
+#endif
+                    *reinterpret_cast<uint4*>(row + ((h ^ (p & 7)) << 4)) = chunk;
                   }
                 }
               }
@@ -487,8 +579,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     // Descriptors are built once and advanced by adding (byte offset >> 4) to
     // the start-address field (addresses < 256 KB never carry out of it).
     if (leader) {  // the whole warp runs the loop; one elected lane issues
+#if XNC_UMMA_FP4
+      // block-scaled descriptor: A, B E2M1 (1), K-major, N, UE8M0 scales (bit 23), M = 256,
+      // scale-factor ids 0, K = 64; the accumulator is f32
+      const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(g.NP >> 3) << 17) | (1u << 23) |
+                             ((uint32_t)(256 >> 4) << 24);
+#else
+      // s32 accumulator, A u8, B s8, K-major, N, M = 256
       const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(g.NP >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
+#endif
+      const uint32_t sf_addr = tmem + (g.tmem_cols - (uint32_t)kSfCols);
       // descriptors as (low word, high word): only the start-address field in the
       // low word moves, so the loop runs on 32-bit values
       const uint64_t a_desc0 = umma_desc_sw128(smem_addr(a_s));
@@ -536,7 +637,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               g_umma_prof[512 + step / 8][2 * (step % 8)] = tw0 - t_start;
               g_umma_prof[512 + step / 8][2 * (step % 8) + 1] = tw1 - tw0;
             }
-            umma_chunk_pair<MH>(d0, g.NP, a_tap, b_lo0 + (st * kPCPS + j) * b16, hi, idesc, acc);
+            umma_chunk_pair<MH>(d0, g.NP, a_tap, b_lo0 + (st * kPCPS + j) * b16, hi, idesc, acc, sf_addr);
             acc = 1;
             if (PROF) n_mma += 4 * MH;
             if (++kx == g.kw) { kx = 0; a_tap += row_skip; } else { a_tap += 8u; }
@@ -706,7 +807,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
             uint32_t absv[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
+              float val = __fmul_rn(__fmul_rn(acc_val(swv[j], v[h][j]), kv[h]), av[j]);
               if (out_scale != nullptr) val = __fadd_rn(__fmul_rn(val, osc[j]), osh[j]);
               const bool in = obase + j < g.O;
               absv[j] = in ? __float_as_uint(fabsf(val)) : 0u;
@@ -795,7 +896,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
             if (!ok[h]) continue;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              if (obase + j < g.O) atomicAdd(part + pix[h] + (size_t)(obase + j) * plane_out, (int)v[h][j]);
+              if (obase + j < g.O) atomicAdd(part + pix[h] + (size_t)(obase + j) * plane_out, acc_raw(v[h][j]));
           }
           continue;
         }
@@ -812,7 +913,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj) {
                 const int j = 4 * q4 + jj;
-                float val = __fmul_rn(__fmul_rn((float)(swv[j] - 2 * (int)v[h][j]), kv[h]), av[j]);
+                float val = __fmul_rn(__fmul_rn(acc_val(swv[j], v[h][j]), kv[h]), av[j]);
                 if (out_scale != nullptr) {
                   const float sc = g.cst_O > 0 ? sc_s[obase + j] : __ldg(out_scale + obase + j);
                   const float sh = g.cst_O > 0 ? sh_s[obase + j] : __ldg(out_shift + obase + j);
@@ -841,7 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
               for (int j = 0; j < 16; j += 2) {
                 float o0, o1;
-                fmul2_rn(o0, o1, (float)(swv[j] - 2 * (int)v[h][j]), (float)(swv[j + 1] - 2 * (int)v[h][j + 1]),
+                fmul2_rn(o0, o1, acc_val(swv[j], v[h][j]), acc_val(swv[j + 1], v[h][j + 1]),
                          kv[h], kv[h]);
                 fmul2_rn(o0, o1, o0, o1, av[j], av[j + 1]);
                 const float recv = __shfl_xor_sync(0xffffffffu, odd ? o0 : o1, 1);
@@ -855,7 +956,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
               for (int j = 0; j < 16; j += 2) {
                 float o0, o1;
-                fmul2_rn(o0, o1, (float)(swv[j] - 2 * (int)v[h][j]), (float)(swv[j + 1] - 2 * (int)v[h][j + 1]),
+                fmul2_rn(o0, o1, acc_val(swv[j], v[h][j]), acc_val(swv[j + 1], v[h][j + 1]),
                          kv[h], kv[h]);
                 fmul2_rn(o0, o1, o0, o1, av[j], av[j + 1]);
                 st_cs_pred(addr_j(yp, plane_bytes32, j), o0, ok[h]);
@@ -868,7 +969,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               const float* yp = y + pix[h] + (size_t)obase * plane_out;
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-                const int accv = swv[j] - 2 * (int)v[h][j];
+                const int accv = swv[j] - 2 * acc_raw(v[h][j]);
                 const float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
                 const float sc = g.cst_O > 0 ? sc_s[obase + j] : __ldg(out_scale + obase + j);
                 const float sh = g.cst_O > 0 ? sh_s[obase + j] : __ldg(out_shift + obase + j);
@@ -886,7 +987,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           for (int j = 0; j < 16; ++j) {
             const int o = obase + j;
             if (o < g.O) {
-              const int accv = swv[j] - 2 * (int)v[h][j];
+              const int accv = swv[j] - 2 * acc_raw(v[h][j]);
               const size_t idx = YPM ? qix[h] * g.O + o : pix[h] + (size_t)o * plane_out;
               if (y) {
                 float val = __fmul_rn(__fmul_rn((float)accv, kv[h]), av[j]);
@@ -919,9 +1020,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 }
 
 // ---------------------------------------------------------------- weights
-// wq[nb][tap][kb][row = filter within a block of NP][128 B], s8 signs (+1/-1,
-// 0 for tail channels and filters >= O), plain rows: the B TMA applies the
-// 128-byte swizzle.  CTA r of a pair loads rows [r*NP/2, (r+1)*NP/2) of a chunk.
+// wq[nb][tap][kb][row = filter within a block of NP][128 B], plain rows (the B TMA
+// applies the 128-byte swizzle); CTA r of a pair loads rows [r*NP/2, (r+1)*NP/2) of a
+// chunk.  kind::mxf4: E2M1 nibbles, byte j = channels 2j (low), 2j + 1 (high) of the
+// block: +1.0 (0x2) / -1.0 (0xA), 0 for tail channels and filters >= O.  kind::i8: s8
+// signs +1 / -1, 0 likewise.  Thread = one 16-byte chunk of a row.
 template <typename T>
 __global__ void k_pack_weights_umma(const T* __restrict__ w, int O, int C, int kh, int kw, int NP,
                                     int KBn, uint8_t* __restrict__ wq) {
@@ -935,14 +1038,18 @@ __global__ void k_pack_weights_umma(const T* __restrict__ w, int O, int C, int k
   const int tap = (int)(rest % (kh * kw));
   const int nb = (int)(rest / (kh * kw));
   const int o = nb * NP + row;
+  constexpr int kPer = kKBc / 8;  // channels per 16-byte chunk
   uint32_t vals[4] = {0u, 0u, 0u, 0u};
   if (o < O) {
-    for (int b = 0; b < 16; ++b) {
-      const int c = kb * 128 + q * 16 + b;
+    for (int b = 0; b < kPer; ++b) {
+      const int c = kb * kKBc + q * kPer + b;
       if (c < C) {
         const T v = w[((long)o * C + c) * kh * kw + tap];
-        const uint32_t sgn = v >= T(0) ? 0x01u : 0xFFu;
-        vals[b >> 2] |= sgn << ((b & 3) * 8);
+#if XNC_UMMA_FP4
+        vals[b >> 3] |= (v >= T(0) ? 0x2u : 0xAu) << ((b & 7) * 4);
+#else
+        vals[b >> 2] |= (v >= T(0) ? 0x01u : 0xFFu) << ((b & 3) * 8);
+#endif
       }
     }
   }
@@ -965,19 +1072,23 @@ __global__ void k_weight_sign_sums(const T* __restrict__ w, int O, int C, int kk
 // 16 rows): O = 256 -> 256, 384 -> 2 x 192, 300 -> 2 x 160, 128 -> 128.  Wide
 // MMAs matter: at N = 128 each pipeline wait costs ~2x the MMA time it hides
 // (profiles/umma_pair_rate_r1.jsonl), so 384 filters run as 2 x 192, not 3 x 128.
+// kind::mxf4 leaves 32 TMEM columns for the scale factors, so a block is at most 240
+// filters there (O = 256 -> 2 x 128).
 static int pair_np(int O) {
-  const int blocks = cdiv(O, 256);
-  return round_up(cdiv(O, blocks), 32);
+  for (int blocks = cdiv(O, kMaxNP);; ++blocks) {
+    const int np = round_up(cdiv(O, blocks), 32);
+    if (np <= kMaxNP) return np;
+  }
 }
 
 size_t umma_weight_bytes(int O, int C, int kh, int kw) {
   const int NP = pair_np(O);
-  return (size_t)cdiv(O, NP) * NP * kh * kw * cdiv(C, 128) * 128;
+  return (size_t)cdiv(O, NP) * NP * kh * kw * cdiv(C, kKBc) * 128;
 }
 
 int launch_pack_weights_umma(const void* w, int dtype, int O, int C, int kh, int kw, uint8_t* wq,
                              int32_t* sw, cudaStream_t s) {
-  const int NP = pair_np(O), KBn = cdiv(C, 128);
+  const int NP = pair_np(O), KBn = cdiv(C, kKBc);
   const long total = (long)cdiv(O, NP) * kh * kw * KBn * NP * 8;
   const unsigned blocks = (unsigned)cdivl(total, 256);
   if (dtype == XNC_DTYPE_F64) {
@@ -995,7 +1106,7 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   g.C = C; g.H = H; g.W = W; g.O = O; g.kh = kh; g.kw = kw; g.pad = pad; g.MH = MH;
   g.oh = H + 2 * pad - kh + 1; g.ow = W + 2 * pad - kw + 1;
   g.IC = W + 2 * pad;
-  g.KBn = cdiv(C, 128);
+  g.KBn = cdiv(C, kKBc);
   g.Cw = cdiv(C, 32);
   g.NP = pair_np(O);
   g.taps = kh * kw;
@@ -1010,7 +1121,7 @@ static bool pair_plan_mh(int N, int C, int H, int W, int O, int kh, int kw, int 
   g.KBu = g.KBn / g.S;
   g.units = g.tiles * g.n_nb * g.S;
   g.b_half_bytes = (uint32_t)(g.NP / 2) * 128u;
-  const int cols = 2 * MH * g.NP;  // two accumulators x MH row blocks
+  const int cols = 2 * MH * g.NP + kSfCols;  // two accumulators x MH row blocks (+ scale factors)
   g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   // S_w and alpha of every filter staged in shared memory for the epilogue (O <= 1024):
   // its per-chunk constant loads were L1/L2 misses under the store stream (ncu: the
