@@ -141,10 +141,21 @@ int xnc_pad_space_to_depth(const float* x, int N, int C, int H, int W, int pad, 
  * PRE-pool map; bits / A describe the pooled map [N][Ho][Wo] (Ho = (Hin - pool_k) /
  * pool_s + 1), bit-identical to xnc_max_pool followed by xnc_pack_input_affine
  * (in_scale / in_shift may be NULL).  Returns XNC_ENOTSUP for shapes the fused
- * kernel does not take (pool_k != 3, fewer than 32 pooled pixels per image,
- * C outside 32..768): pool, then pack. */
+ * kernel does not take (pool_k != 3; unless pool_s == 2 and Win <= 32, also
+ * fewer than 32 pooled pixels per image or C outside 32..768): pool, then pack. */
 int xnc_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s,
                         const float* in_scale, const float* in_shift, uint32_t* bits, float* A, void* stream);
+/* The channels-last form with the pool's bias and ReLU: bits / A of
+ * xnc_max_pool(x, pool_k, pool_s, relu, bias, nhwc = 1) followed by
+ * xnc_pack_input_nhwc(in_scale, in_shift), bit-identical, the pooled map never
+ * written (the XNOR-Net front end: conv1 -> bias -> ReLU -> pool -> conv2's BN ->
+ * sign; reference xnor_conv pipeline.py:176-201 takes one image's binarized input,
+ * this is that input's K1 for a whole batch).  x f32 [N][Hin][Win][C], 16-byte
+ * aligned; bias may be NULL.  XNC_ENOTSUP unless pool_k == 3 and C % 32 == 0, C <=
+ * 256: pool, then pack. */
+int xnc_pack_input_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu,
+                             const float* bias, const float* in_scale, const float* in_shift, uint32_t* bits,
+                             float* A, void* stream);
 /* K1 (xnc_pack_input_affine) for a channels-last input x f32 [N][H][W][C]: same
  * bits / A, a thread per pixel walking its contiguous channels. */
 int xnc_pack_input_nhwc(const float* x, int N, int C, int H, int W, const float* in_scale,

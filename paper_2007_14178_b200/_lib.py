@@ -55,6 +55,7 @@ def lib() -> ctypes.CDLL:
         "xnc_plane_affine": ([P, I, I, LG, P, P, P], I),
         "xnc_pack_input_nhwc": ([P, I, I, I, I, P, P, P, P, P], I),
         "xnc_pack_input_pool": ([P, I, I, I, I, I, I, P, P, P, P, P], I),
+        "xnc_pack_input_pool_nhwc": ([P, I, I, I, I, I, I, I, P, P, P, P, P, P], I),
         "xnc_xnor_conv_umma_ws": ([P, P, P, P, P, I, I, I, I, I, I, I, I, P, P, P, P, P, P], I),
         "xnc_layer_forward": ([P, P, P, I, I, I, I, I, I, I, I, P, P, P, P], I),
         "xnc_layer_forward_umma": ([P, P, P, P, I, I, I, I, I, I, I, I, P, P, P, P], I),
@@ -92,7 +93,7 @@ def exported_symbols() -> list[str]:
             "xnc_layer_workspace_bytes", "xnc_layer_forward", "xnc_layer_forward_umma", "xnc_umma_weight_bytes",
             "xnc_umma_supported", "xnc_pack_weights_umma", "xnc_xnor_conv_umma", "xnc_umma_profile", "xnc_pack_input_affine", "xnc_xnor_conv_umma_affine",
             "xnc_umma_split_ws_bytes", "xnc_xnor_conv_umma_ws", "xnc_max_pool", "xnc_pad_space_to_depth", "xnc_plane_affine",
-            "xnc_pack_input_nhwc", "xnc_pack_input_pool", "xnc_umma_emit_supported", "xnc_xnor_conv_umma_emit", "xnc_pack_plane", "xnc_unpack_plane",
+            "xnc_pack_input_nhwc", "xnc_pack_input_pool", "xnc_pack_input_pool_nhwc", "xnc_umma_emit_supported", "xnc_xnor_conv_umma_emit", "xnc_pack_plane", "xnc_unpack_plane",
             "xnc_sign_plane", "xnc_xnor_accumulate", "xnc_filter_words", "xnc_box_mean",
             "xnc_scale_rows", "xnc_scale_join", "xnc_xnor_reconstruct", "xnc_channel_abs_mean_f64",
             "xnc_apply_scaling_f64", "xnc_ref_sign_conv2d", "xnc_ref_conv2d_f64", "xnc_vanilla_conv",

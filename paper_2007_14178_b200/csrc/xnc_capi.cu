@@ -118,6 +118,15 @@ int xnc_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int pool
   return launch_pack_input_pool(x, N, C, Hin, Win, pool_k, pool_s, bits, A, as_stream(stream), in_scale, in_shift);
 }
 
+int xnc_pack_input_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pool_k, int pool_s, int relu,
+                             const float* bias, const float* in_scale, const float* in_shift, uint32_t* bits,
+                             float* A, void* stream) {
+  if (!x || !bits || N < 1 || C < 1 || Hin < 1 || Win < 1 || pool_k < 1 || pool_s < 1 || (!in_scale != !in_shift))
+    return XNC_EINVAL;
+  return launch_pack_input_pool_nhwc(x, N, C, Hin, Win, pool_k, pool_s, relu, bias, bits, A, as_stream(stream),
+                                     in_scale, in_shift);
+}
+
 int xnc_xnor_conv_umma_affine(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
                               const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                               const float* out_scale, const float* out_shift, float* y, int32_t* acc,

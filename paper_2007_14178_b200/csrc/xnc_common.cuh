@@ -80,4 +80,7 @@ int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int p
                            float* A, cudaStream_t s, const float* in_scale, const float* in_shift);
 int launch_pack_input_nhwc(const float* x, int N, int C, int H, int W, uint32_t* bits, float* A, cudaStream_t s,
                            const float* in_scale, const float* in_shift);
+int launch_pack_input_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu,
+                                const float* bias, uint32_t* bits, float* A, cudaStream_t s, const float* in_scale,
+                                const float* in_shift);
 }  // namespace xnc

@@ -274,6 +274,10 @@ __global__ void __launch_bounds__(128) k_pack_small(const float* __restrict__ x,
   }
 }
 
+// max-pool step in xnc_max_pool's order and rule: a later value wins when it
+// is larger or NaN (so a window's result is its last NaN, else its maximum)
+__device__ __forceinline__ float pool_pick(float m, float v) { return (v > m || v != v) ? v : m; }
+
 // K1 of a max-pooled map without materialising it (XNOR-Net's pool -> BN -> sign in
 // front of conv3 and fc6): x is the PRE-pool map [N][C][Hin][Win]; the value staged
 // for (channel c, pooled pixel (oy, ox)) is the max over its pk x pk window at
@@ -282,6 +286,9 @@ __global__ void __launch_bounds__(128) k_pack_small(const float* __restrict__ x,
 // is k_pack_small: 32 pooled pixels x all C channels in shared memory, warp 0 runs
 // the sequential |.| chains, warps 1-3 the sign words.  Saves the pooled map's
 // write and re-read and one launch.
+#ifndef XNC_POOL_KU
+#define XNC_POOL_KU 6  // 2 / 4 / 6 / 8: conv3's input 81 / 73 / 64 / 73 us at batch 256 (tools/pool_probe.py)
+#endif
 template <bool AFF, int PK>
 __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict__ x, int C, int Hin, int Win,
                                                          int Ho, int Wo, int ps, int Cw, long npix, float inv,
@@ -298,9 +305,9 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
   const int oy = p / Wo, ox = p - (p / Wo) * Wo;
   const float* xp = x + n * C * (long)Hin * Win + (long)(oy * ps) * Win + ox * ps;
   const long plane = (long)Hin * Win;
-  constexpr int kU = 4;  // channels per thread per batch: kU * PK * PK loads in flight
+  constexpr int kU = XNC_POOL_KU;  // channels per thread per batch: kU * PK * PK loads in flight
   for (int c0 = warp; c0 < C; c0 += 4 * kU) {
-    float v[kU][PK * PK];
+    float v[kU][PK * PK], sc[kU], sh[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int c = c0 + 4 * u;
@@ -309,6 +316,10 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
       for (int dy = 0; dy < PK; ++dy)
 #pragma unroll
         for (int dx = 0; dx < PK; ++dx) v[u][dy * PK + dx] = (in && c < C) ? __ldg(b + dy * Win + dx) : 0.0f;
+      // the affine's constants in the same batch of loads (loaded after the window
+      // values were used, each was another memory round trip: ncu's top stall)
+      sc[u] = (AFF && c < C) ? __ldg(in_scale + c) : 1.0f;
+      sh[u] = (AFF && c < C) ? __ldg(in_shift + c) : 0.0f;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -316,9 +327,8 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
       if (c < C) {
         float m = v[u][0];
 #pragma unroll
-        for (int k = 1; k < PK * PK; ++k)
-          if (v[u][k] > m || v[u][k] != v[u][k]) m = v[u][k];
-        if (AFF) m = __fadd_rn(__fmul_rn(m, __ldg(in_scale + c)), __ldg(in_shift + c));
+        for (int k = 1; k < PK * PK; ++k) m = pool_pick(m, v[u][k]);
+        if (AFF) m = __fadd_rn(__fmul_rn(m, sc[u]), sh[u]);
         tile[c * 32 + lane] = m;
       }
     }
@@ -369,6 +379,98 @@ int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int p
   if (int rc = smem_opt_in(kern, sm)) return rc;  // per device (xnc_runtime.cu)
   kern<<<(unsigned)cdivl(npix, 32), 128, sm, s>>>(x, C, Hin, Win, Ho, Wo, ps, Cw, npix, (float)(1.0 / (double)C),
                                                   bits, A, in_scale, in_shift);
+  return launch_status();
+}
+
+// K1 of xnc_max_pool_nhwc's output fused with the pool (the network's front end:
+// conv1's channels-last map -> max 3 x 3 / ps -> + bias -> ReLU -> conv2's folded BN
+// -> sign / A).  Laid out like the pool kernel (a thread per 4 channels of one pooled
+// pixel, nine float4 window loads, coalesced along the channels, many warps in flight:
+// that pass runs at HBM speed); a block takes kPoolPx pooled pixels x C/4 threads.
+// The pool's rule in window order, its bias and ReLU, then the affine as K1 applies
+// it; the sign nibbles are OR-reduced over 8-thread groups (one 32-channel word each:
+// C % 32 == 0, so groups never straddle pixels or warps) and the values staged
+// [C][kPoolPx + 1] for the per-pixel sequential |.| chains.  Saves the pooled map's
+// write and re-read (72 MB at batch 256) and one launch.
+constexpr int kPoolPx = 16;
+template <bool AFF>
+__global__ void __launch_bounds__(1024) k_pool_pack_nhwc(const float4* __restrict__ x, int C, int Hin, int Win,
+                                                        int Ho, int Wo, int ps, int relu, const float* __restrict__ bias,
+                                                        long npix, float inv, uint32_t* __restrict__ bits,
+                                                        float* __restrict__ A, const float* __restrict__ in_scale,
+                                                        const float* __restrict__ in_shift) {
+  extern __shared__ float tile[];  // [C][kPoolPx + 1]
+  constexpr int ld = kPoolPx + 1;
+  const int C4 = C >> 2, Cw = C >> 5;
+  const int t = threadIdx.x, lane = t & 31;
+  const int px = t / C4, c4 = t - px * C4;
+  const long q = (long)blockIdx.x * kPoolPx + px;
+  const bool in = q < npix;
+  uint32_t nib = 0u;
+  if (in) {
+    const int HWo = Ho * Wo;
+    const int n = (int)(q / HWo), p = (int)(q - (long)n * HWo);
+    const int oy = p / Wo, ox = p - (p / Wo) * Wo;
+    const float4* b = x + ((size_t)(n * Hin + oy * ps) * Win + ox * ps) * C4 + c4;
+    float4 w[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) w[k] = __ldg(b + ((size_t)(k / 3) * Win + (k % 3)) * C4);
+    float4 m = w[0];
+#pragma unroll
+    for (int k = 1; k < 9; ++k) {
+      m.x = pool_pick(m.x, w[k].x); m.y = pool_pick(m.y, w[k].y);
+      m.z = pool_pick(m.z, w[k].z); m.w = pool_pick(m.w, w[k].w);
+    }
+    float v[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = 4 * c4 + u;
+      if (bias != nullptr) v[u] = __fadd_rn(v[u], __ldg(bias + c));
+      if (relu && v[u] < 0.0f) v[u] = 0.0f;
+      if (AFF) v[u] = __fadd_rn(__fmul_rn(v[u], __ldg(in_scale + c)), __ldg(in_shift + c));
+      tile[c * ld + px] = v[u];
+      nib |= (v[u] >= 0.0f ? 1u : 0u) << u;
+    }
+  }
+  // 32-channel word = 8 consecutive threads (c4 = 8j .. 8j + 7 of one pixel)
+  uint32_t wv = nib << (4 * (lane & 7));
+  wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
+  wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
+  wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
+  if (in && (c4 & 7) == 0) bits[q * Cw + (c4 >> 3)] = wv;
+  __syncthreads();
+  if (t < kPoolPx && A != nullptr) {
+    const long qa = (long)blockIdx.x * kPoolPx + t;
+    if (qa < npix) {
+      float s = 0.0f;
+      int c = 0;
+      for (; c + 8 <= C; c += 8) {
+        float tv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tv[u] = tile[(c + u) * ld + t];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = __fadd_rn(s, fabsf(tv[u]));
+      }
+      for (; c < C; ++c) s = __fadd_rn(s, fabsf(tile[c * ld + t]));
+      A[qa] = __fmul_rn(s, inv);
+    }
+  }
+}
+
+int launch_pack_input_pool_nhwc(const float* x, int N, int C, int Hin, int Win, int pk, int ps, int relu,
+                                const float* bias, uint32_t* bits, float* A, cudaStream_t s, const float* in_scale,
+                                const float* in_shift) {
+  if (pk != 3 || ps < 1 || Hin < pk || Win < pk) return XNC_ENOTSUP;
+  if ((C & 31) != 0 || C / 4 * kPoolPx > 1024 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) return XNC_ENOTSUP;
+  const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
+  const long npix = (long)N * Ho * Wo;
+  if ((long)N * Hin * Win * C >= 0x7fffffffL * 4L) return XNC_ENOTSUP;
+  const size_t sm = (size_t)C * (kPoolPx + 1) * sizeof(float);
+  auto kern = in_scale ? k_pool_pack_nhwc<true> : k_pool_pack_nhwc<false>;
+  if (int rc = smem_opt_in(kern, sm)) return rc;
+  kern<<<(unsigned)cdivl(npix, kPoolPx), (C / 4) * kPoolPx, sm, s>>>(
+      reinterpret_cast<const float4*>(x), C, Hin, Win, Ho, Wo, ps, relu, bias, npix, (float)(1.0 / (double)C), bits, A,
+      in_scale, in_shift);
   return launch_status();
 }
 

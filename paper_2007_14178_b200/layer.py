@@ -137,6 +137,18 @@ class XnorConv2d:
         self.out_shape(p.shape)
         return self._conv_packed(p, self.kernel_for(p.shape), out, want_acc, emit_signs)
 
+    def forward_k1(self, p: "ops.PackedInput", out: torch.Tensor | None = None, emit_signs: bool = False):
+        """The conv on an input whose K1 the caller produced WITH this layer's
+        in_affine / in_pool applied (fused into its own pass, e.g. the network's
+        front end: conv1's pool + this layer's batch norm + sign in one kernel)."""
+        if p.C != self.C:
+            raise ValueError(f"packed input has {p.C} channels, the filters {self.C}")
+        N, C, H, W = p.shape  # already the conv's input shape (pooled, if in_pool)
+        oh, ow = ops.out_dims(H, W, self.kh, self.kw, self.pad)
+        if oh < 1 or ow < 1:
+            raise ValueError("kernel larger than the padded input")
+        return self._conv_packed(p, self.kernel_for(p.shape), out, False, emit_signs)
+
     def _conv_packed(self, p: "ops.PackedInput", variant: str, out, want_acc: bool, emit_signs: bool):
         """K2 -> K3+K4 on a K1-form input."""
         if variant in ("popc-fc", "umma-fc"):

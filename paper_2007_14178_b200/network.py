@@ -141,22 +141,35 @@ class XnorNetAlexNet:
             # kernels, same values as F.pad / F.pixel_unshuffle and F.relu / F.max_pool2d),
             # channels-last end to end: cuDNN's NHWC TF32 conv is 0.39 vs 0.60 ms NCHW, and
             # conv2's K1 reads the channels-last map directly (tools/front_probe.py)
-            if self.conv1 == "tcgen05" and tuple(x.shape[1:]) == (3, 224, 224):
-                h = ops.conv1_forward(x, self.conv1_wq)  # TF32 tensor cores, channels-last out
-            else:
-                xs = ops.pad_space_to_depth(x, 2, 4, channels_last=True)
-                h = F.conv2d(xs, self.conv1_w_s2d_cl)  # bias folded into the pool (exact: see max_pool)
-            return ops.max_pool(h, 3, 2, relu=True, bias=self.conv1_b)
+            return ops.max_pool(self._conv1_map(x), 3, 2, relu=True, bias=self.conv1_b)
+
+    def _conv1_map(self, x: torch.Tensor) -> torch.Tensor:
+        """conv1 without its bias: f32 [N, 96, 55, 55] channels-last."""
+        if self.conv1 == "tcgen05" and tuple(x.shape[1:]) == (3, 224, 224):
+            return ops.conv1_forward(x, self.conv1_wq)  # TF32 tensor cores, channels-last out
+        xs = ops.pad_space_to_depth(x, 2, 4, channels_last=True)
+        return F.conv2d(xs, self.conv1_w_s2d_cl)  # bias folded into the pool (exact: see max_pool)
 
     def _forward(self, x: torch.Tensor, return_features: bool):
-        h = self.front_end(x)
         feats = {}
+        h = None
         for name, *_ in BINARY_LAYERS:
             # conv3 / fc6 take the pre-pool map (their in_pool); conv3 and conv4 hand the
             # next layer its input in packed-sign form (sign-emitting epilogue, exact)
             # unless the float feature maps are asked for
             emit = self.emit_signs and not return_features and name in EMITS_NEXT
-            h = self.binary[name].forward(h, emit_signs=emit)  # NCHW / channels-last / packed
+            layer = self.binary[name]
+            if h is None:
+                # conv2's K1 fused with conv1's bias + ReLU + pool 3/2 and conv2's batch
+                # norm: one pass over conv1's channels-last map, the pooled map never
+                # written (xnc_pack_input_pool_nhwc; same bits / A as front_end() + K1)
+                with _tf32_full_precision_layers():
+                    pre = self._conv1_map(x)
+                bits, A = ops.pack_input(pre, in_affine=layer.in_affine, in_pool=(3, 2), pool_relu=True,
+                                         pool_bias=self.conv1_b)
+                h = layer.forward_k1(ops.PackedInput(bits, A, layer.C), emit_signs=emit)
+            else:
+                h = layer.forward(h, emit_signs=emit)  # NCHW / channels-last / packed
             feats[name] = h
         logits = F.linear(h.flatten(1), self.fc8_w, self.fc8_b)  # full precision
         return (logits, feats) if return_features else logits

@@ -139,16 +139,35 @@ def conv1_forward(x: torch.Tensor, wq: torch.Tensor, out: torch.Tensor | None = 
     return out
 
 
-def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None, in_pool=None):
+def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None, in_pool=None, pool_relu: bool = False,
+               pool_bias: torch.Tensor | None = None):
     """K1: x f32 [N,C,H,W] -> (bits i32 [N,H,W,Cw] (u32 payload), A f32 [N,H,W]).
 
     in_affine = (scale, shift) f32 [C]: binarize and average x*scale + shift (one
     rounding per op) instead of x -- a folded batch norm before the sign.
     in_pool = (kernel, stride): x is the pre-pool tensor, max-pooled first (no
-    padding; xnc_max_pool) -- XNOR-Net's pool -> BN -> sign; bits / A then have the
-    pooled spatial shape."""
+    padding; xnc_max_pool, with its relu / bias = pool_relu / pool_bias) --
+    XNOR-Net's pool -> BN -> sign; bits / A then have the pooled spatial shape."""
     _need_cuda(x, "x", torch.float32, channels_last_ok=True)
-    if in_pool is not None and not _channels_last(x):
+    if pool_bias is not None:
+        _need_cuda(pool_bias, "pool_bias", torch.float32)
+        if pool_bias.numel() != x.shape[1]:
+            raise ValueError(f"pool_bias must have {x.shape[1]} entries")
+    if in_pool is not None and _channels_last(x):
+        # pool (+ bias, ReLU) fused into K1 on the channels-last map (xnc_pack_input_pool_nhwc)
+        N, C, Hin, Win = x.shape
+        H, W = pool_dims(Hin, Win, in_pool)
+        bits = torch.empty((N, H, W, words(C)), dtype=torch.int32, device=x.device)
+        A = torch.empty((N, H, W), dtype=torch.float32, device=x.device) if want_A else None
+        sc, sh = _affine(in_affine, C, x.device, "in_affine")
+        rc = lib().xnc_pack_input_pool_nhwc(x.data_ptr(), N, C, Hin, Win, int(in_pool[0]), int(in_pool[1]),
+                                            int(bool(pool_relu)), _ptr(pool_bias), _ptr(sc), _ptr(sh),
+                                            bits.data_ptr(), _ptr(A), _stream(x.device))
+        if rc == 0:
+            return bits, A
+        if rc != XNC_ENOTSUP:
+            check(rc, "xnc_pack_input_pool_nhwc")
+    elif in_pool is not None and not pool_relu and pool_bias is None:
         # pool fused into K1 (xnc_pack_input_pool) when the pooled map takes its path
         xc = x.contiguous()
         N, C, Hin, Win = xc.shape
@@ -163,7 +182,7 @@ def pack_input(x: torch.Tensor, want_A: bool = True, in_affine=None, in_pool=Non
         if rc != XNC_ENOTSUP:
             check(rc, "xnc_pack_input_pool")
     if in_pool is not None:
-        x = max_pool(x, *in_pool)
+        x = max_pool(x, *in_pool, relu=pool_relu, bias=pool_bias)
     N, C, H, W = x.shape
     bits = torch.empty((N, H, W, words(C)), dtype=torch.int32, device=x.device)
     A = torch.empty((N, H, W), dtype=torch.float32, device=x.device) if want_A else None

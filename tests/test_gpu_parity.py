@@ -410,13 +410,16 @@ def test_bn_affines_in_k1_and_epilogue(shape, variant):
 
 
 
-@pytest.mark.parametrize("shape", [(3, 256, 27, 27, 3, 2), (2, 70, 13, 13, 3, 2), (2, 64, 9, 12, 2, 2),
-                                   (4, 4096, 3, 3, 3, 1)], ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("shape", [(3, 256, 27, 27, 3, 2), (2, 70, 13, 13, 3, 2), (2, 256, 13, 13, 3, 2),
+                                   (2, 33, 31, 32, 3, 2), (1, 2, 7, 7, 3, 2), (2, 40, 29, 33, 3, 2),
+                                   (2, 64, 9, 12, 2, 2), (4, 4096, 3, 3, 3, 1)],
+                         ids=lambda s: "x".join(map(str, s)))
 def test_pooled_input_k1(shape):
     """K1 over a max-pooled input: pooled values identical to torch.max_pool2d, bits
-    and A identical to K1 on that map, with and without the folded BN.  The first
-    two shapes take the fused pool + K1 kernel (xnc_pack_input_pool), the last two
-    its fallback (pool, then pack)."""
+    and A identical to K1 on that map, with and without the folded BN.  The 3 x 3
+    shapes with >= 32 pooled pixels and C >= 32 take the fused kernel
+    (xnc_pack_input_pool: conv3's and fc6's inputs among them); C = 2 and the last two
+    the fallback (pool, then pack)."""
     import torch.nn.functional as F
     from paper_2007_14178_b200 import ops
     N, C, H, W, k, s = shape
@@ -435,6 +438,32 @@ def test_pooled_input_k1(shape):
         b2, a2 = ops.pack_input(pooled, in_affine=aff)
         assert torch.equal(b1, b2)
         assert torch.equal(a1.view(torch.int32), a2.view(torch.int32))
+
+
+@pytest.mark.parametrize("shape", [(3, 96, 55, 55), (2, 64, 12, 11), (2, 32, 7, 9), (2, 40, 9, 9)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_pooled_input_k1_nhwc(shape):
+    """The network front end's fused pass (xnc_pack_input_pool_nhwc): K1 of
+    max_pool(x, 3, 2, relu, bias) on a channels-last map, with conv2's folded BN,
+    identical to pooling first (xnc_max_pool) and packing the pooled map; C = 40 is
+    not a multiple of 32 and takes that two-pass fallback."""
+    from paper_2007_14178_b200 import ops
+    N, C, H, W = shape
+    rng = np.random.default_rng(list(shape))
+    x = torch.from_numpy(O.f32_exact(rng, (N, C, H, W))).to(_dev())
+    x[0, 0, 0, :2] = 0.0
+    x[0, 1, 1, 1] = -0.0
+    x[N - 1, C - 1, H // 2, W // 2] = float("nan")
+    x = x.contiguous(memory_format=torch.channels_last)
+    bias = torch.rand(C, device=_dev()) - 0.5
+    aff = (torch.rand(C, device=_dev()) + 0.5, torch.rand(C, device=_dev()) - 0.5)
+    for relu, b, a in ((True, bias, aff), (False, None, aff), (True, None, None), (False, bias, None)):
+        b1, a1 = ops.pack_input(x, in_affine=a, in_pool=(3, 2), pool_relu=relu, pool_bias=b)
+        pooled = ops.max_pool(x, 3, 2, relu=relu, bias=b)
+        assert pooled.is_contiguous(memory_format=torch.channels_last)
+        b2, a2 = ops.pack_input(pooled, in_affine=a)
+        assert torch.equal(b1, b2), (relu, b is None, a is None)
+        assert torch.equal(a1.view(torch.int32), a2.view(torch.int32)), (relu, b is None, a is None)
 
 
 def test_layer_in_pool_matches_pooled_layer():

@@ -123,10 +123,18 @@ def case_pack_wide(rng):
 
 
 def case_pool_k1(rng):
-    # max-pool fused into K1 (conv3 / fc6 inputs)
-    x = torch.from_numpy(O.f32_exact(rng, (2, 96, 27, 27))).cuda()
-    b1, a1 = ops.pack_input(x, in_pool=(3, 2))
-    b2, a2 = ops.pack_input(ops.max_pool(x, 3, 2))
+    # max-pool fused into K1: conv3 / fc6-like inputs, a 33-wide map, and the
+    # channels-last front end with bias + ReLU
+    for shape in ((2, 96, 27, 27), (2, 64, 13, 13), (1, 40, 11, 33)):
+        x = torch.from_numpy(O.f32_exact(rng, shape)).cuda()
+        b1, a1 = ops.pack_input(x, in_pool=(3, 2))
+        b2, a2 = ops.pack_input(ops.max_pool(x, 3, 2))
+        torch.cuda.synchronize()
+        assert torch.equal(b1, b2) and torch.equal(a1, a2)
+    x = torch.from_numpy(O.f32_exact(rng, (2, 96, 13, 13))).cuda().contiguous(memory_format=torch.channels_last)
+    bias = torch.from_numpy(O.f32_exact(rng, (96,))).cuda()
+    b1, a1 = ops.pack_input(x, in_pool=(3, 2), pool_relu=True, pool_bias=bias)
+    b2, a2 = ops.pack_input(ops.max_pool(x, 3, 2, relu=True, bias=bias))
     torch.cuda.synchronize()
     assert torch.equal(b1, b2) and torch.equal(a1, a2)
 
