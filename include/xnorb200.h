@@ -179,10 +179,11 @@ int xnc_xnor_conv_umma_emit(const uint32_t* bits, const uint8_t* wq, const int32
                             void* stream);
 /* K split for shapes with fewer (pixel tile, 256-filter block) work units than CTA
  * pairs -- fully connected layers viewed as one 1 x N image.  Units of one output
- * tile take disjoint K ranges and add their raw partial sums into split_ws
- * (s32, xnc_umma_split_ws_bytes() bytes, ZEROED by the caller; left zeroed on
- * return); a finalize kernel then writes y / acc with the same arithmetic as the
- * unsplit epilogue (integer sums: exact in any order).  xnc_umma_split_ws_bytes()
+ * tile take disjoint K ranges and store their raw partial sums into their own
+ * slice of split_ws (s32, xnc_umma_split_ws_bytes() bytes = S slices of N*O*H'*W';
+ * any contents on entry -- every slice entry is written); a finalize kernel then
+ * adds the slices and writes y / acc with the same arithmetic as the unsplit
+ * epilogue (integer sums: exact in any order).  xnc_umma_split_ws_bytes()
  * == 0: no split for this shape, split_ws is ignored (may be NULL).  Otherwise
  * the same contract as xnc_xnor_conv_umma_affine (which never splits). */
 size_t xnc_umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad);

@@ -270,6 +270,7 @@ struct PairGeom {
   int n_nb;          // filter blocks
   int tiles;         // N * n_mt
   int units;         // tiles * n_nb * S work units (pair tile, filter block, K split), strided over the pairs
+  long part_slice;   // K split: s32 partial sums per split slice (N * O * oh * ow)
   int S, KBu;        // K splits per (tile, filter block) and K blocks per unit (KBn = S * KBu); S > 1
                      // for shapes with fewer (tile, block) pairs than CTA pairs (fully connected
                      // layers): the units add raw partial sums into a zeroed s32 buffer
@@ -469,7 +470,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     // epilogue's store stream the L2 latency of the bit rows grows, and a
     // one-load-at-a-time loop left the issuer waiting on a_full.
     constexpr int kAR = XNC_A_ROWS;
-    const int grp = g.a_unit ? g.KBu : 1;
+    // per-plane ring (long K: fully connected layers): planes still built in groups of
+    // up to half the ring, all slots awaited first, so their loads are in flight together
+    // (one plane at a time waited out an L2 round trip per 4 MMAs: fc6 ran at ~1.7 us per
+    // chunk)
+    const int grp = g.a_unit ? g.KBu : max(1, min(g.NA / 2, 4));
     uint32_t it = 0;  // units of this pair so far: every unit builds its KBu planes
     for (;; ++it) {
       const int u = unit_at(g, cluster, n_clusters, (int)it);
@@ -480,87 +485,166 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
       const uint32_t* img = bits + (size_t)n * g.H * g.W * g.Cw;
       for (int kb0 = 0; kb0 < g.KBu; kb0 += grp) {
         const uint32_t use0 = it * g.KBu + kb0;
-        // barrier guarding the group's slots: per unit (group it & 1) or per plane
-        const uint32_t ab = g.a_unit ? (it & 1) : use0 % g.NA;
-        const bool wait_empty = g.a_unit ? it >= 2 : use0 >= (uint32_t)g.NA;
-        const uint32_t e_par = g.a_unit ? (((it >> 1) - 1) & 1) : (((use0 / g.NA) - 1) & 1);
-        if (wait_empty) {
-          if (lane == 0) mbar_wait_prof(&a_empty[ab], e_par, prof, w_ae, XNC_PROD_HINT);
+        const int gn = g.a_unit ? grp : min(grp, g.KBu - kb0);  // planes in this group
+        // barriers guarding the group's slots: per unit (group it & 1) or per plane
+        if (g.a_unit) {
+          if (it >= 2) {
+            if (lane == 0) mbar_wait_prof(&a_empty[it & 1], ((it >> 1) - 1) & 1, prof, w_ae, XNC_PROD_HINT);
+            __syncwarp();
+          }
+        } else {
+          for (int k = 0; k < gn; ++k) {
+            const uint32_t use = use0 + k;
+            if (use >= (uint32_t)g.NA && lane == 0)
+              mbar_wait_prof(&a_empty[use % g.NA], ((use / g.NA) - 1) & 1, prof, w_ae, XNC_PROD_HINT);
+          }
           __syncwarp();
         }
         if (!((dbg & 4) && use0 >= (uint32_t)g.NA)) {  // bit 2 (profiling): planes built once
-          for (int kp = 0; kp < grp; kp += 2) {
-            const int kbA = kbu0 + kb0 + kp;  // global K block of the first plane
-            const bool two = kp + 1 < grp;
-            uint8_t* planes[2];
-            constexpr int NQ = kKBw / 4;  // 16-byte loads per pixel and K block
-            uint32_t vmask[2][kKBw];      // valid-channel masks of each block's words
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              planes[k] = a_s + (size_t)((use0 + kp + k) % g.NA) * g.plane_bytes;
-#pragma unroll
-              for (int w = 0; w < kKBw; ++w) {
-                const int rem = g.C - ((kbA + k) * kKBc + w * 32);
-                vmask[k][w] = rem >= 32 ? 0xFFFFFFFFu : rem <= 0 ? 0u : ((1u << rem) - 1u);
+          if (g.a_unit) {
+            // a unit's planes (conv layers): two planes x kAR rows per thread in flight
+            for (int kp = 0; kp < gn; kp += 2) {
+              const int kbA = kbu0 + kb0 + kp;  // global K block of the first plane
+              const bool two = kp + 1 < gn;
+              uint8_t* planes[2];
+              constexpr int NQ = kKBw / 4;  // 16-byte loads per pixel and K block
+              uint32_t vmask[2][kKBw];      // valid-channel masks of each block's words
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                planes[k] = a_s + (size_t)((use0 + kp + k) % g.NA) * g.plane_bytes;
+  #pragma unroll
+                for (int w = 0; w < kKBw; ++w) {
+                  const int rem = g.C - ((kbA + k) * kKBc + w * 32);
+                  vmask[k][w] = rem >= 32 ? 0xFFFFFFFFu : rem <= 0 ? 0u : ((1u << rem) - 1u);
+                }
+              }
+              for (int r0 = 0; r0 < g.P; r0 += n_pt * kAR) {
+                uint4 q[2][kAR][NQ];
+                bool in_img[kAR];
+  #pragma unroll
+                for (int i = 0; i < kAR; ++i) {
+                  const int p = r0 + pt + i * n_pt;
+                  const int e = m0 + p;
+                  const int pr = e / g.IC, pc = e - pr * g.IC;
+                  const int r = pr - g.pad, c = pc - g.pad;
+                  in_img[i] = p < g.P && r >= 0 && r < g.H && c >= 0 && c < g.W;
+                  const uint32_t* src = img + ((size_t)(in_img[i] ? r : 0) * g.W + (in_img[i] ? c : 0)) * g.Cw;
+  #pragma unroll
+                  for (int k = 0; k < 2; ++k)
+  #pragma unroll
+                    for (int u = 0; u < NQ; ++u) {
+                      q[k][i][u] = make_uint4(0u, 0u, 0u, 0u);
+                      const int wl = g.Cw - (kbA + k) * kKBw - 4 * u;  // words present from this load on
+                      if (in_img[i] && (k == 0 || two) && wl > 0) {
+                        const uint32_t* sk = src + (kbA + k) * kKBw + 4 * u;
+                        if (vec4 && wl >= 4) {
+                          q[k][i][u] = __ldg(reinterpret_cast<const uint4*>(sk));
+                        } else {
+                          q[k][i][u].x = __ldg(sk);
+                          if (wl > 1) q[k][i][u].y = __ldg(sk + 1);
+                          if (wl > 2) q[k][i][u].z = __ldg(sk + 2);
+                          if (wl > 3) q[k][i][u].w = __ldg(sk + 3);
+                        }
+                      }
+                    }
+                }
+  #pragma unroll
+                for (int i = 0; i < kAR; ++i) {
+                  const int p = r0 + pt + i * n_pt;
+                  if (p >= g.P) continue;
+  #pragma unroll
+                  for (int k = 0; k < 2; ++k) {
+                    if (k == 1 && !two) continue;
+                    uint32_t wd[kKBw];
+  #pragma unroll
+                    for (int u = 0; u < NQ; ++u) {
+                      wd[4 * u] = q[k][i][u].x; wd[4 * u + 1] = q[k][i][u].y;
+                      wd[4 * u + 2] = q[k][i][u].z; wd[4 * u + 3] = q[k][i][u].w;
+                    }
+                    uint8_t* row = planes[k] + (size_t)p * 128;
+  #pragma unroll
+                    for (int h = 0; h < 8; ++h) {
+  #if XNC_UMMA_FP4
+                      // 16-byte chunk h = word h: 32 channels as nibbles (padding pixel: all d = 0)
+                      const uint4 chunk = d_nibbles32(wd[h], in_img[i] ? vmask[k][h] : 0u);
+  #else
+                      // 16-byte chunk h = half word h: 16 channels as bytes
+                      const uint32_t b16 = (wd[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
+                      const uint32_t v16 = in_img[i] ? (vmask[k][h >> 1] >> ((h & 1) * 16)) & 0xFFFFu : 0u;
+                      const uint4 chunk = d_bytes16(b16, v16);
+  #endif
+                      *reinterpret_cast<uint4*>(row + ((h ^ (p & 7)) << 4)) = chunk;
+                    }
+                  }
+                }
               }
             }
-            for (int r0 = 0; r0 < g.P; r0 += n_pt * kAR) {
-              uint4 q[2][kAR][NQ];
-              bool in_img[kAR];
-#pragma unroll
-              for (int i = 0; i < kAR; ++i) {
-                const int p = r0 + pt + i * n_pt;
+          } else {
+            // the group's (plane, pixel row) items, flattened over the producer threads:
+            // every thread issues the loads of all its items (up to kIT) before expanding any
+            constexpr int kIT = 2 * kAR;
+            constexpr int NQ = kKBw / 4;  // 16-byte loads per pixel and K block
+            const int items = gn * g.P;
+            for (int r0 = 0; r0 < items; r0 += n_pt * kIT) {
+              uint4 q[kIT][NQ];
+              int ik[kIT], ip[kIT];
+              bool in_img[kIT];
+  #pragma unroll
+              for (int i = 0; i < kIT; ++i) {
+                const int j = r0 + pt + i * n_pt;
+                const int k = j / g.P, p = j - k * g.P;  // plane within the group, pixel row
+                ik[i] = k;
+                ip[i] = p;
                 const int e = m0 + p;
                 const int pr = e / g.IC, pc = e - pr * g.IC;
                 const int r = pr - g.pad, c = pc - g.pad;
-                in_img[i] = p < g.P && r >= 0 && r < g.H && c >= 0 && c < g.W;
+                in_img[i] = j < items && r >= 0 && r < g.H && c >= 0 && c < g.W;
                 const uint32_t* src = img + ((size_t)(in_img[i] ? r : 0) * g.W + (in_img[i] ? c : 0)) * g.Cw;
-#pragma unroll
-                for (int k = 0; k < 2; ++k)
-#pragma unroll
-                  for (int u = 0; u < NQ; ++u) {
-                    q[k][i][u] = make_uint4(0u, 0u, 0u, 0u);
-                    const int wl = g.Cw - (kbA + k) * kKBw - 4 * u;  // words present from this load on
-                    if (in_img[i] && (k == 0 || two) && wl > 0) {
-                      const uint32_t* sk = src + (kbA + k) * kKBw + 4 * u;
-                      if (vec4 && wl >= 4) {
-                        q[k][i][u] = __ldg(reinterpret_cast<const uint4*>(sk));
-                      } else {
-                        q[k][i][u].x = __ldg(sk);
-                        if (wl > 1) q[k][i][u].y = __ldg(sk + 1);
-                        if (wl > 2) q[k][i][u].z = __ldg(sk + 2);
-                        if (wl > 3) q[k][i][u].w = __ldg(sk + 3);
-                      }
+                const int kb = kbu0 + kb0 + k;  // global K block
+  #pragma unroll
+                for (int u = 0; u < NQ; ++u) {
+                  q[i][u] = make_uint4(0u, 0u, 0u, 0u);
+                  const int wl = g.Cw - kb * kKBw - 4 * u;  // words present from this load on
+                  if (in_img[i] && wl > 0) {
+                    const uint32_t* sk = src + kb * kKBw + 4 * u;
+                    if (vec4 && wl >= 4) {
+                      q[i][u] = __ldg(reinterpret_cast<const uint4*>(sk));
+                    } else {
+                      q[i][u].x = __ldg(sk);
+                      if (wl > 1) q[i][u].y = __ldg(sk + 1);
+                      if (wl > 2) q[i][u].z = __ldg(sk + 2);
+                      if (wl > 3) q[i][u].w = __ldg(sk + 3);
                     }
                   }
+                }
               }
-#pragma unroll
-              for (int i = 0; i < kAR; ++i) {
-                const int p = r0 + pt + i * n_pt;
-                if (p >= g.P) continue;
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                  if (k == 1 && !two) continue;
-                  uint32_t wd[kKBw];
-#pragma unroll
-                  for (int u = 0; u < NQ; ++u) {
-                    wd[4 * u] = q[k][i][u].x; wd[4 * u + 1] = q[k][i][u].y;
-                    wd[4 * u + 2] = q[k][i][u].z; wd[4 * u + 3] = q[k][i][u].w;
-                  }
-                  uint8_t* row = planes[k] + (size_t)p * 128;
-#pragma unroll
-                  for (int h = 0; h < 8; ++h) {
-#if XNC_UMMA_FP4
-                    // 16-byte chunk h = word h: 32 channels as nibbles (padding pixel: all d = 0)
-                    const uint4 chunk = d_nibbles32(wd[h], in_img[i] ? vmask[k][h] : 0u);
-#else
-                    // 16-byte chunk h = half word h: 16 channels as bytes
-                    const uint32_t b16 = (wd[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
-                    const uint32_t v16 = in_img[i] ? (vmask[k][h >> 1] >> ((h & 1) * 16)) & 0xFFFFu : 0u;
-                    const uint4 chunk = d_bytes16(b16, v16);
-#endif
-                    *reinterpret_cast<uint4*>(row + ((h ^ (p & 7)) << 4)) = chunk;
-                  }
+  #pragma unroll
+              for (int i = 0; i < kIT; ++i) {
+                if (r0 + pt + i * n_pt >= items) continue;
+                const int k = ik[i], p = ip[i], kb = kbu0 + kb0 + k;
+                uint32_t wd[kKBw];
+  #pragma unroll
+                for (int u = 0; u < NQ; ++u) {
+                  wd[4 * u] = q[i][u].x; wd[4 * u + 1] = q[i][u].y;
+                  wd[4 * u + 2] = q[i][u].z; wd[4 * u + 3] = q[i][u].w;
+                }
+                uint8_t* row = a_s + (size_t)((use0 + k) % g.NA) * g.plane_bytes + (size_t)p * 128;
+  #pragma unroll
+                for (int h = 0; h < 8; ++h) {
+  #if XNC_UMMA_FP4
+                  // 16-byte chunk h = word h: 32 channels as nibbles (padding pixel: all d = 0)
+                  const int rem = g.C - (kb * kKBc + h * 32);
+                  const uint32_t vm = rem >= 32 ? 0xFFFFFFFFu : rem <= 0 ? 0u : ((1u << rem) - 1u);
+                  const uint4 chunk = d_nibbles32(wd[h], in_img[i] ? vm : 0u);
+  #else
+                  // 16-byte chunk h = half word h: 16 channels as bytes
+                  const int rem = g.C - (kb * kKBc + (h >> 1) * 32);
+                  const uint32_t vm = rem >= 32 ? 0xFFFFFFFFu : rem <= 0 ? 0u : ((1u << rem) - 1u);
+                  const uint32_t b16 = (wd[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
+                  const uint32_t v16 = in_img[i] ? (vm >> ((h & 1) * 16)) & 0xFFFFu : 0u;
+                  const uint4 chunk = d_bytes16(b16, v16);
+  #endif
+                  *reinterpret_cast<uint4*>(row + ((h ^ (p & 7)) << 4)) = chunk;
                 }
               }
             }
@@ -569,8 +653,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
-        if (lane == 0)
-          for (int k = 0; k < grp; ++k) mbar_arrive_cluster(full0 + ab * 8);
+        if (lane == 0) {
+          if (g.a_unit)
+            for (int k = 0; k < grp; ++k) mbar_arrive_cluster(full0 + (it & 1) * 8);
+          else
+            for (int k = 0; k < gn; ++k) mbar_arrive_cluster(full0 + ((use0 + k) % g.NA) * 8);
+        }
       }
     }
     if (prof) g_umma_prof[blockIdx.x][8] = w_ae;
@@ -890,13 +978,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
         const unsigned long long tc1 = prof ? clock64() : 0ull;
         if (prof) w_ld += tc1 - tc0;
         if (PROF && (dbg & 1)) continue;
-        if (part != nullptr) {  // K split: add this unit's raw partial sums (exact, any order)
+        if (part != nullptr) {
+          // K split: this unit's raw partial sums into its own slice (plain coalesced
+          // stores; the finalize adds the S slices -- exact integers.  red.add into one
+          // buffer cost ~4 M L2 atomics per fully connected layer at batch 256)
+          int32_t* ps = part + (size_t)(u % g.S) * (size_t)g.part_slice;
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             if (!ok[h]) continue;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              if (obase + j < g.O) atomicAdd(part + pix[h] + (size_t)(obase + j) * plane_out, acc_raw(v[h][j]));
+              if (obase + j < g.O) ps[pix[h] + (size_t)(obase + j) * plane_out] = acc_raw(v[h][j]);
           }
           continue;
         }
@@ -1181,13 +1273,15 @@ bool umma_emit_supported(int N, int C, int H, int W, int O, int kh, int kw, int 
 size_t umma_split_ws_bytes(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
   PairGeom g;
   size_t smem;
-  if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem) || split_factor(g) == 1) return 0;
-  return (size_t)N * O * g.oh * g.ow * sizeof(int32_t);
+  if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return 0;
+  const int S = split_factor(g);
+  if (S == 1) return 0;
+  return (size_t)S * N * O * g.oh * g.ow * sizeof(int32_t);
 }
 
-// K-split epilogue: part (the units' summed raw d.s_w sums) -> y / acc exactly as
-// the conv epilogue would, and part back to zero for the next call.
-__global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __restrict__ sw,
+// K-split epilogue: part (S slices of the units' raw d.s_w partial sums, summed here
+// in slice order: exact integers) -> y / acc exactly as the conv epilogue would.
+__global__ void k_split_finalize(const int32_t* __restrict__ part, int S, long slice, const int32_t* __restrict__ sw,
                                  const float* __restrict__ Kmap, const float* __restrict__ alpha,
                                  const float* __restrict__ out_scale, const float* __restrict__ out_shift,
                                  long total, int O, long plane, float* __restrict__ y, int32_t* __restrict__ acc) {
@@ -1196,8 +1290,9 @@ __global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __re
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)total; i += gridDim.x * blockDim.x) {
     const int np = i / (int)plane, p = i - np * (int)plane;
     const int n = np / O, o = np - n * O;
-    const int accv = __ldg(sw + o) - 2 * part[i];
-    part[i] = 0;
+    int d = 0;
+    for (int k = 0; k < S; ++k) d += __ldcs(part + (size_t)k * slice + i);
+    const int accv = __ldg(sw + o) - 2 * d;
     if (acc) acc[i] = accv;
     if (y) {
       float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + (long)n * plane + p)), __ldg(alpha + o));
@@ -1208,9 +1303,10 @@ __global__ void k_split_finalize(int32_t* __restrict__ part, const int32_t* __re
 }
 
 // The same for a channels-last y ([N][P][O], P = H'W'): 32 x 32 (filter, pixel) tiles
-// staged in shared memory so part [N][O][P] is read (and re-zeroed) and y written with
+// staged in shared memory so the slices [S][N][O][P] are read and y written with
 // whole-sector accesses on both sides.
-__global__ void __launch_bounds__(256) k_split_finalize_pm(int32_t* __restrict__ part, const int32_t* __restrict__ sw,
+__global__ void __launch_bounds__(256) k_split_finalize_pm(const int32_t* __restrict__ part, int S, long slice,
+                                                           const int32_t* __restrict__ sw,
                                                            const float* __restrict__ Kmap, const float* __restrict__ alpha,
                                                            const float* __restrict__ out_scale,
                                                            const float* __restrict__ out_shift, int O, int P,
@@ -1218,13 +1314,14 @@ __global__ void __launch_bounds__(256) k_split_finalize_pm(int32_t* __restrict__
   __shared__ float t[32][33];
   const int o0 = blockIdx.y * 32, p0 = blockIdx.x * 32, n = blockIdx.z;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  int32_t* pn = part + (size_t)n * O * P;
+  const int32_t* pn = part + (size_t)n * O * P;
   for (int r = ty; r < 32; r += 8) {
     const int o = o0 + r, p = p0 + tx;
     if (o < O && p < P) {
       const size_t idx = (size_t)o * P + p;
-      const int accv = __ldg(sw + o) - 2 * pn[idx];
-      pn[idx] = 0;
+      int d = 0;
+      for (int k = 0; k < S; ++k) d += __ldcs(pn + (size_t)k * slice + idx);
+      const int accv = __ldg(sw + o) - 2 * d;
       float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + (size_t)n * P + p)), __ldg(alpha + o));
       if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
       t[r][tx] = val;
@@ -1307,6 +1404,7 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
   }
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
+  g.part_slice = (long)N * O * g.oh * g.ow;
   g.tile_major = next_bits != nullptr && g.n_nb > 1;
   g.y_pm = y_pm;  // (informational: the YPM instantiation is selected above)
   kern<<<2 * pairs, threads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
@@ -1316,10 +1414,10 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
     if (y_pm)
       k_split_finalize_pm<<<dim3(cdiv(g.oh * g.ow, 32), cdiv(O, 32), N), 256, 0, s>>>(
-          part, sw, K, alpha, out_scale, out_shift, O, g.oh * g.ow, y);
+          part, g.S, g.part_slice, sw, K, alpha, out_scale, out_shift, O, g.oh * g.ow, y);
     else
-      k_split_finalize<<<blocks, 256, 0, s>>>(part, sw, K, alpha, out_scale, out_shift, total, O,
-                                              (long)g.oh * g.ow, y, acc);
+      k_split_finalize<<<blocks, 256, 0, s>>>(part, g.S, g.part_slice, sw, K, alpha, out_scale, out_shift, total,
+                                              O, (long)g.oh * g.ow, y, acc);
   }
   return launch_status();
 }

@@ -359,8 +359,8 @@ def resolve_variant(variant: str, filt: PackedFilters, N: int, C: int, H: int, W
     return variant
 
 
-# Zeroed s32 partial-sum buffers of the K split, one per (device, stream): the split
-# kernels leave them zeroed, so they are allocated (and zeroed) once, not per call.
+# s32 partial-sum buffers of the K split (S slices, every entry written by the split
+# kernel), one per (device, stream), allocated once, not per call.
 _SPLIT_WS: dict[tuple, torch.Tensor] = {}
 
 
@@ -368,7 +368,7 @@ def _split_ws(nbytes: int, dev: torch.device) -> torch.Tensor:
     key = (dev, torch.cuda.current_stream(dev).cuda_stream)
     buf = _SPLIT_WS.get(key)
     if buf is None or buf.numel() * 4 < nbytes:
-        buf = torch.zeros(nbytes // 4, dtype=torch.int32, device=dev)
+        buf = torch.empty(nbytes // 4, dtype=torch.int32, device=dev)
         _SPLIT_WS[key] = buf
     return buf
 
@@ -421,7 +421,7 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
         if filt.wq is None:
             raise ValueError("umma variant needs attach_umma_weights() first")
         osc, osh = _affine(out_affine, filt.O, dev, "out_affine")
-        # a K split (fully connected shapes) needs a zeroed s32 partial-sum buffer
+        # a K split (fully connected shapes) needs an s32 partial-sum buffer (S slices)
         ws_bytes = lib().xnc_umma_split_ws_bytes(N, C, H, W, filt.O, filt.kh, filt.kw, pad)
         split_ws = _split_ws(ws_bytes, dev) if ws_bytes else None
         check(lib().xnc_xnor_conv_umma_ws(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), _ptr(K),
