@@ -270,7 +270,6 @@ struct PairGeom {
   int n_nb;          // filter blocks
   int tiles;         // N * n_mt
   int units;         // tiles * n_nb * S work units (pair tile, filter block, K split), strided over the pairs
-  long part_slice;   // K split: s32 partial sums per split slice (N * O * oh * ow)
   int S, KBu;        // K splits per (tile, filter block) and K blocks per unit (KBn = S * KBu); S > 1
                      // for shapes with fewer (tile, block) pairs than CTA pairs (fully connected
                      // layers): the units add raw partial sums into a zeroed s32 buffer
@@ -474,6 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
     // up to half the ring, all slots awaited first, so their loads are in flight together
     // (one plane at a time waited out an L2 round trip per 4 MMAs: fc6 ran at ~1.7 us per
     // chunk)
+    // (the YPM instantiations only: fully connected layers run channels-last)
     const int grp = g.a_unit ? g.KBu : max(1, min(g.NA / 2, 4));
     uint32_t it = 0;  // units of this pair so far: every unit builds its KBu planes
     for (;; ++it) {
@@ -501,7 +501,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           __syncwarp();
         }
         if (!((dbg & 4) && use0 >= (uint32_t)g.NA)) {  // bit 2 (profiling): planes built once
-          if (g.a_unit) {
+          // (the flattened form only in the MH = 1 kernels: the MH = 2 ones run at their
+          // 512-thread launch's 128-register cap, where any extra live state spills)
+          if (MH == 2 || g.a_unit) {
             // a unit's planes (conv layers): two planes x kAR rows per thread in flight
             for (int kp = 0; kp < gn; kp += 2) {
               const int kbA = kbu0 + kb0 + kp;  // global K block of the first plane
@@ -982,7 +984,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
           // K split: this unit's raw partial sums into its own slice (plain coalesced
           // stores; the finalize adds the S slices -- exact integers.  red.add into one
           // buffer cost ~4 M L2 atomics per fully connected layer at batch 256)
-          int32_t* ps = part + (size_t)(u % g.S) * (size_t)g.part_slice;
+          // (the slice size N*O*oh*ow is derived here: one more PairGeom field moved the
+          // MH = 2 kernel's register allocation into 80 bytes of spills, C2k3 +6 %)
+          int32_t* ps = part + (size_t)(u % g.S) * ((size_t)(g.tiles / g.n_mt) * g.O * plane_out);
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             if (!ok[h]) continue;
@@ -1404,7 +1408,6 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
   }
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
-  g.part_slice = (long)N * O * g.oh * g.ow;
   g.tile_major = next_bits != nullptr && g.n_nb > 1;
   g.y_pm = y_pm;  // (informational: the YPM instantiation is selected above)
   kern<<<2 * pairs, threads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
@@ -1414,9 +1417,9 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
     if (y_pm)
       k_split_finalize_pm<<<dim3(cdiv(g.oh * g.ow, 32), cdiv(O, 32), N), 256, 0, s>>>(
-          part, g.S, g.part_slice, sw, K, alpha, out_scale, out_shift, O, g.oh * g.ow, y);
+          part, g.S, (long)N * O * g.oh * g.ow, sw, K, alpha, out_scale, out_shift, O, g.oh * g.ow, y);
     else
-      k_split_finalize<<<blocks, 256, 0, s>>>(part, g.S, g.part_slice, sw, K, alpha, out_scale, out_shift, total,
+      k_split_finalize<<<blocks, 256, 0, s>>>(part, g.S, (long)N * O * g.oh * g.ow, sw, K, alpha, out_scale, out_shift, total,
                                               O, (long)g.oh * g.ow, y, acc);
   }
   return launch_status();
