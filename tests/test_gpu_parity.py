@@ -466,6 +466,27 @@ def test_pooled_input_k1_nhwc(shape):
         assert torch.equal(a1.view(torch.int32), a2.view(torch.int32)), (relu, b is None, a is None)
 
 
+def test_layer_forward_k1_matches_forward():
+    """XnorConv2d.forward_k1 (an input whose K1 the caller produced with the layer's
+    in_affine / in_pool applied, as the network's fused front end does) == forward(x);
+    a wrong channel count is refused; pool_bias must have one entry per channel."""
+    from paper_2007_14178_b200 import XnorConv2d, ops
+    rng = np.random.default_rng(9)
+    x = torch.from_numpy(O.f32_exact(rng, (3, 64, 27, 27))).to(_dev())
+    w = torch.from_numpy(O.f32_exact(rng, (96, 64, 3, 3))).to(_dev())
+    aff = (torch.rand(64, device=_dev()) + 0.5, torch.rand(64, device=_dev()) - 0.5)
+    layer = XnorConv2d(w, pad=1, variant="auto", in_affine=aff, in_pool=(3, 2))
+    bits, A = ops.pack_input(x, in_affine=aff, in_pool=(3, 2))
+    ya = layer.forward_k1(ops.PackedInput(bits, A, 64))
+    yb = layer.forward(x)
+    assert ya.shape == (3, 96, 13, 13)
+    assert torch.equal(ya.view(torch.int32), yb.view(torch.int32))
+    with pytest.raises(ValueError):
+        layer.forward_k1(ops.PackedInput(bits, A, 32))
+    with pytest.raises(ValueError):
+        ops.pack_input(x, in_pool=(3, 2), pool_bias=torch.zeros(63, device=_dev()))
+
+
 def test_layer_in_pool_matches_pooled_layer():
     """XnorConv2d(in_pool) on the pre-pool map == the same layer on the pooled map."""
     import torch.nn.functional as F
