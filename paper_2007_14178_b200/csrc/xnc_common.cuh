@@ -38,6 +38,30 @@ inline int smem_opt_in(F* func, size_t bytes) { return smem_opt_in(reinterpret_c
 // SM count of the current device (cached per device).
 int device_sm_count();
 
+// Programmatic dependent launch: a kernel started with launch_pdl may be scheduled
+// while the previous kernel of its stream drains; every thread that reads what an
+// earlier kernel wrote, or writes what it may still read, calls pdl_wait() first (a
+// no-op for an ordinary launch).  Since each such kernel waits before it completes,
+// the order holds transitively along the stream.  env XNC_PDL=0: ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+int pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace xnc
 
 // Kernel launchers implemented in the per-kernel translation units.

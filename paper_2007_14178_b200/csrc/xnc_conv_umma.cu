@@ -402,6 +402,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_s;
   const int tile_px = 2 * MH * 128;
+  // programmatic dependent launch: everything above and the B producer's weight stream
+  // may overlap the previous kernel's tail; every other role reads (bits, K) or writes (y,
+  // next_bits) what earlier kernels touch, so it waits for them here
+  if (warp != 0) pdl_wait();
+  pdl_launch_dependents();  // persistent (one wave): the next kernel may be scheduled as CTAs exit
 #if XNC_UMMA_FP4
   // every block scale factor = 2^0 (UE8M0 0x7F in every byte of the scale columns, all
   // 128 lanes of both CTAs): the MMAs then sum plain E2M1 products
@@ -1410,8 +1415,8 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   g.inv_O = (float)(1.0 / (double)O);  // <real_t>(1.0 / channels) of the next layer's K1
   g.tile_major = next_bits != nullptr && g.n_nb > 1;
   g.y_pm = y_pm;  // (informational: the YPM instantiation is selected above)
-  kern<<<2 * pairs, threads, smem, s>>>(bits, b_map, sw, K, alpha, g, y, acc, out_scale, out_shift, part,
-                                          next_bits, next_A);
+  launch_pdl(kern, dim3(2 * pairs), dim3(threads), smem, s, bits, b_map, sw, K, alpha, g, y, acc, out_scale,
+             out_shift, part, next_bits, next_A);
   if (part != nullptr) {
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(THREADS) k_pack_input(const float* __restrict_
                                                              const float* __restrict__ in_scale,
                                                              const float* __restrict__ in_shift) {
   extern __shared__ uint4 pack_smem[];
+  pdl_wait();  // x may be the previous kernel's output
   uint32_t* wtile = reinterpret_cast<uint32_t*>(pack_smem);
   constexpr int PIX = THREADS * VEC;          // pixels per block
   constexpr int JS = PIX + 4;                 // word-plane stride (bank skew, keeps 16 B alignment)
@@ -679,7 +680,8 @@ int launch_pack_input(const float* x, int N, int C, int H, int W, uint32_t* bits
   int opt_rc = XNC_OK;
   auto go = [&](auto kern, int t) {
     opt_rc = smem_opt_in(kern, smem);  // per device (xnc_runtime.cu)
-    if (opt_rc == XNC_OK) kern<<<blocks, t, smem, s>>>(x, C, HW, Cw, inv, gpi, total, bits, A, in_scale, in_shift);
+    if (opt_rc == XNC_OK)
+      launch_pdl(kern, dim3(blocks), dim3(t), smem, s, x, C, HW, Cw, inv, gpi, total, bits, A, in_scale, in_shift);
   };
   auto pick = [&](auto aff_tag) {
     constexpr bool AF = decltype(aff_tag)::value;

@@ -1,6 +1,7 @@
 // Per-device launch state shared by the kernel launchers: the dynamic
 // shared-memory opt-in and the SM count, cached per (device, function) under a
 // mutex so that several GPUs (and host threads) can drive one process.
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -36,6 +37,11 @@ int smem_opt_in(const void* func, size_t bytes) {
   if (e != cudaSuccess) return XNC_ECUDA_BASE + (int)e;
   have = bytes;
   return XNC_OK;
+}
+
+int pdl_enabled() {
+  static const int on = getenv("XNC_PDL") ? atoi(getenv("XNC_PDL")) : 1;
+  return on;
 }
 
 int device_sm_count() {

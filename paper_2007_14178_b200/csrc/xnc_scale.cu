@@ -61,6 +61,8 @@ __global__ void __launch_bounds__(kBandThreads) k_scale_map_band(const float* __
                                                                   int kh, int kw, int pad, int oh, int ow,
                                                                   int BY, float box, float* __restrict__ K) {
   extern __shared__ float band_s[];
+  pdl_launch_dependents();  // one short wave: the next kernel (the conv) may start its prologue
+  pdl_wait();  // A is the previous kernel's output
   const int n = blockIdx.y, y0 = blockIdx.x * BY;
   const int by = min(BY, oh - y0);
   const int rows = by + kh - 1, cols = ow + kw - 1;
@@ -115,7 +117,7 @@ int launch_scale_map(const float* A, int N, int H, int W, int kh, int kw, int pa
     while (BY > 1 && smem_of(BY) > kBandSmemMax) BY = (BY + 1) / 2;
     if (smem_of(BY) <= kBandSmemMax) {
       dim3 grid(cdiv(oh, BY), N);
-      k_scale_map_band<<<grid, kBandThreads, smem_of(BY), s>>>(A, H, W, kh, kw, pad, oh, ow, BY, box, K);
+      launch_pdl(k_scale_map_band, grid, dim3(kBandThreads), smem_of(BY), s, A, H, W, kh, kw, pad, oh, ow, BY, box, K);
       return launch_status();
     }
   }
