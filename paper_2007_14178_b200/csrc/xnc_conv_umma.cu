@@ -1176,9 +1176,11 @@ __global__ void k_weight_sign_sums(const T* __restrict__ w, int O, int C, int kk
 // kind::mxf4 leaves 32 TMEM columns for the scale factors, so a block is at most 240
 // filters there (O = 256 -> 2 x 128).
 static int pair_np(int O) {
-  for (int blocks = cdiv(O, kMaxNP);; ++blocks) {
+  static const int cap = getenv("XNC_UMMA_NP_MAX") ? atoi(getenv("XNC_UMMA_NP_MAX")) : kMaxNP;  // tuning only
+  const int mx = std::min(std::max(cap, 32), kMaxNP);
+  for (int blocks = cdiv(O, mx);; ++blocks) {
     const int np = round_up(cdiv(O, blocks), 32);
-    if (np <= kMaxNP) return np;
+    if (np <= mx) return np;
   }
 }
 
