@@ -995,9 +995,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             if (!ok[h]) continue;
+            if (YPM && obase + 16 <= g.O) {
+              // channels-last slices ([pixel][O], like y): the thread's 16 filters are 64
+              // contiguous bytes, four 16-byte stores (O % 4 == 0, host-checked)
+              int4* dst = reinterpret_cast<int4*>(ps + qix[h] * g.O + obase);
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (obase + j < g.O) ps[pix[h] + (size_t)(obase + j) * plane_out] = acc_raw(v[h][j]);
+              for (int q4 = 0; q4 < 4; ++q4)
+                dst[q4] = make_int4(acc_raw(v[h][4 * q4]), acc_raw(v[h][4 * q4 + 1]), acc_raw(v[h][4 * q4 + 2]),
+                                    acc_raw(v[h][4 * q4 + 3]));
+              continue;
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (obase + j >= g.O) continue;
+              const size_t idx = YPM ? qix[h] * g.O + obase + j : pix[h] + (size_t)(obase + j) * plane_out;
+              ps[idx] = acc_raw(v[h][j]);
+            }
           }
           continue;
         }
@@ -1313,35 +1326,32 @@ __global__ void k_split_finalize(const int32_t* __restrict__ part, int S, long s
   }
 }
 
-// The same for a channels-last y ([N][P][O], P = H'W'): 32 x 32 (filter, pixel) tiles
-// staged in shared memory so the slices [S][N][O][P] are read and y written with
-// whole-sector accesses on both sides.
+// The same for a channels-last y ([N][P][O], P = H'W'): the YPM kernels store their slices
+// channels-last too, so this is an elementwise pass, 4 consecutive filters per thread
+// (O % 4 == 0, host-checked), coalesced on both sides.
 __global__ void __launch_bounds__(256) k_split_finalize_pm(const int32_t* __restrict__ part, int S, long slice,
                                                            const int32_t* __restrict__ sw,
                                                            const float* __restrict__ Kmap, const float* __restrict__ alpha,
                                                            const float* __restrict__ out_scale,
-                                                           const float* __restrict__ out_shift, int O, int P,
+                                                           const float* __restrict__ out_shift, int O, int total4,
                                                            float* __restrict__ y) {
-  __shared__ float t[32][33];
-  const int o0 = blockIdx.y * 32, p0 = blockIdx.x * 32, n = blockIdx.z;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const int32_t* pn = part + (size_t)n * O * P;
-  for (int r = ty; r < 32; r += 8) {
-    const int o = o0 + r, p = p0 + tx;
-    if (o < O && p < P) {
-      const size_t idx = (size_t)o * P + p;
-      int d = 0;
-      for (int k = 0; k < S; ++k) d += __ldcs(pn + (size_t)k * slice + idx);
-      const int accv = __ldg(sw + o) - 2 * d;
-      float val = __fmul_rn(__fmul_rn((float)accv, __ldg(Kmap + (size_t)n * P + p)), __ldg(alpha + o));
-      if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
-      t[r][tx] = val;
+  for (int i4 = blockIdx.x * blockDim.x + threadIdx.x; i4 < total4; i4 += gridDim.x * blockDim.x) {
+    const int i = 4 * i4, q = i / O, o = i - q * O;
+    int4 d = __ldcs(reinterpret_cast<const int4*>(part + i));
+    for (int k = 1; k < S; ++k) {
+      const int4 e = __ldcs(reinterpret_cast<const int4*>(part + (size_t)k * slice + i));
+      d.x += e.x; d.y += e.y; d.z += e.z; d.w += e.w;
     }
-  }
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int p = p0 + r, o = o0 + tx;
-    if (o < O && p < P) y[((size_t)n * P + p) * O + o] = t[tx][r];
+    const float kv = __ldg(Kmap + q);
+    const int dd[4] = {d.x, d.y, d.z, d.w};
+    float r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float val = __fmul_rn(__fmul_rn((float)(__ldg(sw + o + u) - 2 * dd[u]), kv), __ldg(alpha + o + u));
+      if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o + u)), __ldg(out_shift + o + u));
+      r[u] = val;
+    }
+    reinterpret_cast<float4*>(y)[i4] = make_float4(r[0], r[1], r[2], r[3]);
   }
 }
 
@@ -1423,8 +1433,8 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
     if (y_pm)
-      k_split_finalize_pm<<<dim3(cdiv(g.oh * g.ow, 32), cdiv(O, 32), N), 256, 0, s>>>(
-          part, g.S, (long)N * O * g.oh * g.ow, sw, K, alpha, out_scale, out_shift, O, g.oh * g.ow, y);
+      k_split_finalize_pm<<<(unsigned)std::min<long>(cdivl(total / 4, 256), (long)sms * 8), 256, 0, s>>>(
+          part, g.S, total, sw, K, alpha, out_scale, out_shift, O, (int)(total / 4), y);
     else
       k_split_finalize<<<blocks, 256, 0, s>>>(part, g.S, (long)N * O * g.oh * g.ow, sw, K, alpha, out_scale, out_shift, total,
                                               O, (long)g.oh * g.ow, y, acc);
