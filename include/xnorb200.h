@@ -202,6 +202,17 @@ int xnc_xnor_conv_umma_nhwc(const uint32_t* bits, const uint8_t* wq, const int32
                             const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
                             const float* out_scale, const float* out_shift, int32_t* split_ws, float* y,
                             void* stream);
+/* xnc_xnor_conv_umma_nhwc followed by the NEXT binary layer's K1 of y: next_bits
+ * [pixels][O/32] and next_A [pixels] = xnc_pack_input of y viewed as pixels 1 x 1 maps
+ * of O channels (the fc6 -> fc7 hand-off of the XNOR-Net forward; reference: the next
+ * layer's xnor_conv input binarization, pipeline.py:176-201), bit-identical.  With a
+ * K split the finalize builds them in the same pass (one block per pixel runs the
+ * sequential |.| chain); unsplit, K1 runs on y after the conv.  y is still written.
+ * O % 32 == 0, O <= 4096, y 16-byte aligned. */
+int xnc_xnor_conv_umma_nhwc_emit(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
+                                 const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
+                                 const float* out_scale, const float* out_shift, int32_t* split_ws, float* y,
+                                 uint32_t* next_bits, float* next_A, void* stream);
 /* Profiling only: per-CTA cycle counters of the last tcgen05 conv launched with
  * XNC_UMMA_DEBUG bit 7 set (16 u64 slots per CTA, host memory; blocking copy). */
 int xnc_umma_profile(unsigned long long* host_out, int n_ctas);

@@ -74,6 +74,7 @@ def lib() -> ctypes.CDLL:
         "xnc_ref_conv2d_f64": ([P, P, I, I, I, I, I, I, I, D, P, P], I),
         "xnc_vanilla_conv": ([P, I, I, I, I, P, I, I, P, P], I),
         "xnc_xnor_conv_umma_nhwc": ([P, P, P, P, P, I, I, I, I, I, I, I, I, P, P, P, P, P], I),
+        "xnc_xnor_conv_umma_nhwc_emit": ([P, P, P, P, P, I, I, I, I, I, I, I, I, P, P, P, P, P, P, P], I),
         "xnc_conv1_weight_bytes": ([], S),
         "xnc_conv1_pack_weights": ([P, P, P], I),
         "xnc_conv1_forward": ([P, I, P, P, P], I),
@@ -98,7 +99,7 @@ def exported_symbols() -> list[str]:
             "xnc_scale_rows", "xnc_scale_join", "xnc_xnor_reconstruct", "xnc_channel_abs_mean_f64",
             "xnc_apply_scaling_f64", "xnc_ref_sign_conv2d", "xnc_ref_conv2d_f64", "xnc_vanilla_conv",
             "xnc_conv1_weight_bytes", "xnc_conv1_pack_weights", "xnc_conv1_forward",
-            "xnc_xnor_conv_umma_nhwc"]
+            "xnc_xnor_conv_umma_nhwc", "xnc_xnor_conv_umma_nhwc_emit"]
 
 DTYPE_F32, DTYPE_F64, DTYPE_I8 = 0, 1, 2
 XNC_ENOTSUP = 2  # include/xnorb200.h: shape outside what the kernels support

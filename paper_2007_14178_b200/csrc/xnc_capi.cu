@@ -220,6 +220,17 @@ int xnc_xnor_conv_umma_nhwc(const uint32_t* bits, const uint8_t* wq, const int32
                           out_scale, out_shift, split_ws, nullptr, nullptr, 1);
 }
 
+int xnc_xnor_conv_umma_nhwc_emit(const uint32_t* bits, const uint8_t* wq, const int32_t* sw, const float* K,
+                                 const float* alpha, int N, int C, int H, int W, int O, int kh, int kw, int pad,
+                                 const float* out_scale, const float* out_shift, int32_t* split_ws, float* y,
+                                 uint32_t* next_bits, float* next_A, void* stream) {
+  if (!bits || !wq || !sw || !K || !alpha || !y || !next_bits || !next_A || O < 1 || (O & 31) ||
+      !conv_shape_ok(N, C, H, W, kh, kw, pad) || (reinterpret_cast<uintptr_t>(y) & 15) || (!out_scale != !out_shift))
+    return XNC_EINVAL;
+  return launch_conv_umma(bits, wq, sw, K, alpha, N, C, H, W, O, kh, kw, pad, y, nullptr, as_stream(stream),
+                          out_scale, out_shift, split_ws, next_bits, next_A, 1);
+}
+
 int xnc_umma_profile(unsigned long long* host_out, int n_ctas) {
   if (!host_out || n_ctas < 1) return XNC_EINVAL;
   return umma_profile_read(host_out, n_ctas);

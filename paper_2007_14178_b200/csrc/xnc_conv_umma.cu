@@ -1355,6 +1355,87 @@ __global__ void __launch_bounds__(256) k_split_finalize_pm(const int32_t* __rest
   }
 }
 
+// The channels-last finalize fused with the NEXT binary layer's K1 (fc6 -> fc7): a block
+// per output pixel; warps 0-7 add the slices of its O filters 1024 at a time (4 per
+// thread), write y as k_split_finalize_pm does, build the sign words (8-thread groups of
+// 4 filters: one 32-filter word) and stage |y| in shared memory, while lane 0 of warp 8
+// runs the sequential |.| chain in filter order over each 1024-filter chunk as soon as it
+// is staged (named barrier per chunk) -- exactly K1 of y (k_pack_wide: bit = y >= 0,
+// A = (sum_o |y_o|) * f32(1/O)).  Saves K1's launch and its re-read of y; the chain (O
+// dependent adds) is the floor.
+constexpr int kEmitThreads = 288;
+__global__ void __launch_bounds__(kEmitThreads) k_split_finalize_emit(const int32_t* __restrict__ part, int S, long slice,
+                                                                     const int32_t* __restrict__ sw,
+                                                                     const float* __restrict__ Kmap,
+                                                                     const float* __restrict__ alpha,
+                                                                     const float* __restrict__ out_scale,
+                                                                     const float* __restrict__ out_shift, int O,
+                                                                     float inv_O, float* __restrict__ y,
+                                                                     uint32_t* __restrict__ next_bits,
+                                                                     float* __restrict__ next_A) {
+  extern __shared__ __align__(16) float abs_s[];  // [O]
+  const int q = blockIdx.x, t = threadIdx.x, lane = t & 31;
+  const int nchunk = (O + 1023) >> 10;  // <= 4 (O <= 4096, host-checked)
+  if (t < 256) {
+    const float kv = __ldg(Kmap + q);
+    for (int k = 0; k < nchunk; ++k) {
+      const int o4 = k * 256 + t;
+      if (4 * o4 < O) {  // O % 32 == 0: a warp's 32 threads cover whole words
+        const size_t i = (size_t)q * O + 4 * o4;
+        int4 d = __ldcs(reinterpret_cast<const int4*>(part + i));
+        for (int s2 = 1; s2 < S; ++s2) {
+          const int4 e = __ldcs(reinterpret_cast<const int4*>(part + (size_t)s2 * slice + i));
+          d.x += e.x; d.y += e.y; d.z += e.z; d.w += e.w;
+        }
+        const int dd[4] = {d.x, d.y, d.z, d.w};
+        float r[4];
+        uint32_t nib = 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int o = 4 * o4 + u;
+          float val = __fmul_rn(__fmul_rn((float)(__ldg(sw + o) - 2 * dd[u]), kv), __ldg(alpha + o));
+          if (out_scale) val = __fadd_rn(__fmul_rn(val, __ldg(out_scale + o)), __ldg(out_shift + o));
+          r[u] = val;
+          abs_s[o] = fabsf(val);
+          nib |= (val >= 0.0f ? 1u : 0u) << u;
+        }
+        reinterpret_cast<float4*>(y + i)[0] = make_float4(r[0], r[1], r[2], r[3]);
+        uint32_t wv = nib << (4 * (lane & 7));
+        wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
+        wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
+        wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
+        if ((lane & 7) == 0) next_bits[(size_t)q * (O >> 5) + (o4 >> 3)] = wv;
+      }
+      __threadfence_block();
+      asm volatile("bar.arrive %0, %1;" ::"r"(1 + k), "r"(kEmitThreads) : "memory");  // chunk k staged
+    }
+  } else {
+    float s = 0.0f;
+    for (int k = 0; k < nchunk; ++k) {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + k), "r"(kEmitThreads) : "memory");
+      if (lane == 0) {
+        const int n = min(1024, O - k * 1024);  // a multiple of 32
+        const float4* b4 = reinterpret_cast<const float4*>(abs_s + k * 1024);
+        float4 cur[8], nxt[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur[u] = b4[u];
+        for (int b = 0; b < (n >> 5); ++b) {
+          if (b + 1 < (n >> 5)) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nxt[u] = b4[(b + 1) * 8 + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, cur[u].x), cur[u].y), cur[u].z), cur[u].w);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+        }
+      }
+    }
+    if (lane == 0) next_A[q] = __fmul_rn(s, inv_O);
+  }
+}
+
 bool umma_supported(int N, int C, int H, int W, int O, int kh, int kw, int pad) {
   PairGeom g;
   size_t smem;
@@ -1374,6 +1455,16 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   PairGeom g;
   size_t smem;
   if (!pair_plan(N, C, H, W, O, kh, kw, pad, g, smem)) return XNC_ENOTSUP;
+  // channels-last y with next_bits: the next layer's K1 comes after the conv (fused into
+  // the K-split finalize, else K1 of y), not from the conv epilogue
+  const bool after_emit = y_pm && next_bits != nullptr;
+  uint32_t* const emit_bits = next_bits;
+  float* const emit_A = next_A;
+  if (after_emit) {
+    if (y == nullptr || next_A == nullptr || (O & 31) || O > 4096) return XNC_ENOTSUP;
+    next_bits = nullptr;
+    next_A = nullptr;
+  }
   // several filter blocks: a pair takes whole tiles (all blocks back to back), so the
   // emitting epilogue sees every channel of its pixels in order
   if (next_bits != nullptr && g.S != 1) return XNC_ENOTSUP;
@@ -1429,10 +1520,21 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
   g.y_pm = y_pm;  // (informational: the YPM instantiation is selected above)
   launch_pdl(kern, dim3(2 * pairs), dim3(threads), smem, s, bits, b_map, sw, K, alpha, g, y, acc, out_scale,
              out_shift, part, next_bits, next_A);
+  if (after_emit && part == nullptr) {
+    // unsplit: K1 of y ([pixels][O] = pixels 1 x 1 images of O channels), as the next
+    // layer would run it
+    if (int rc = launch_status()) return rc;
+    return launch_pack_input(y, N * g.oh * g.ow, O, 1, 1, emit_bits, emit_A, s);
+  }
   if (part != nullptr) {
     const long total = (long)N * O * g.oh * g.ow;
     const int blocks = (int)std::min<long>(cdivl(total, 256), (long)sms * 8);
-    if (y_pm)
+    if (after_emit) {
+      const size_t esm = (size_t)O * sizeof(float);
+      if (int rc = smem_opt_in(k_split_finalize_emit, esm)) return rc;
+      k_split_finalize_emit<<<(unsigned)(N * g.oh * g.ow), kEmitThreads, esm, s>>>(part, g.S, total, sw, K, alpha, out_scale,
+                                                                          out_shift, O, g.inv_O, y, emit_bits, emit_A);
+    } else if (y_pm)
       k_split_finalize_pm<<<(unsigned)std::min<long>(cdivl(total / 4, 256), (long)sms * 8), 256, 0, s>>>(
           part, g.S, total, sw, K, alpha, out_scale, out_shift, O, (int)(total / 4), y);
     else

@@ -153,7 +153,9 @@ class XnorConv2d:
         """K2 -> K3+K4 on a K1-form input."""
         if variant in ("popc-fc", "umma-fc"):
             if emit_signs:
-                raise ValueError("emit_signs is not available for fully connected layers")
+                if want_acc or out is not None:
+                    raise ValueError("emit_signs returns the next layer's input: no out / want_acc")
+                return self._fc_packed_emit(p, variant)
             return self._fc_packed(p, out, want_acc, variant)
         K = ops.scale_map(p.A, self.kh, self.kw, self.pad)
         if emit_signs:
@@ -198,7 +200,7 @@ class XnorConv2d:
         over the whole input, alpha per filter (the reference's (c, ky, kx) sum)."""
         N, C, H, W = p.shape
         bits, A = p.bits, p.A
-        K = ops.scale_map(A, self.kh, self.kw, 0)                     # [N, 1, 1]
+        K = self._fc_k(A)                                             # [N, 1, 1]
         fcf = self._fc_filters(umma=variant == "umma-fc")
         if variant == "umma-fc" and not want_acc and self.O % 4 == 0 and (
                 out is None or out.is_contiguous()):
@@ -220,6 +222,29 @@ class XnorConv2d:
         if want_acc:
             return y, acc1.view(self.O, N).t().reshape(N, self.O, 1, 1).contiguous()
         return y.contiguous()
+
+    def _fc_k(self, A: torch.Tensor) -> torch.Tensor:
+        """K of a fully connected layer: the box mean of A over the whole input; for a
+        1 x 1 kernel that is A itself (K2's 0 + A, times f32(1/1), is A bit for bit), so
+        no K2 launch."""
+        if self.kh == 1 and self.kw == 1:
+            return A
+        return ops.scale_map(A, self.kh, self.kw, 0)
+
+    def _fc_packed_emit(self, p: "ops.PackedInput", variant: str) -> "ops.PackedInput":
+        """The fully connected layer with its output handed to the next binary layer in
+        K1 form (sign words + A of y [* out_affine]): fused into the K-split finalize on
+        the tcgen05 path (xnc_xnor_conv_umma_nhwc_emit), else K1 of y."""
+        N, C, H, W = p.shape
+        if variant == "umma-fc" and self.O % 32 == 0 and self.O <= 4096:
+            K = self._fc_k(p.A)
+            fcf = self._fc_filters(umma=True)
+            y, nb, nA = ops.xnor_conv_nhwc(p.bits.view(1, 1, N, H * W * ops.words(C)), fcf, K.view(1, 1, N), 0,
+                                           out_affine=self.out_affine, emit=True)
+            return ops.PackedInput(nb.view(N, 1, 1, self.O // 32), nA.view(N, 1, 1), self.O)
+        y = self._fc_packed(p, None, False, variant)
+        bits, A = ops.pack_input(y.contiguous())
+        return ops.PackedInput(bits, A, self.O)
 
     def _fc_filters(self, umma: bool = False) -> ops.PackedFilters:
         """The filters as 1x1 filters over kh*kw*C channels in (y, x, c) order; alpha

@@ -57,7 +57,8 @@ BINARY_LAYERS = (  # name, C_in, C_out, k, pad
     ("fc7", 4096, 4096, 1, 0),
 )
 POOLED_INPUT = ("conv3", "fc6")  # layers whose input is max-pool 3/2 of the previous output
-EMITS_NEXT = ("conv3", "conv4")   # binary -> binary with no pool between: the epilogue emits signs
+EMITS_NEXT = ("conv3", "conv4", "fc6")  # binary -> binary with no pool between: the next layer's K1
+                                        # comes from the conv (epilogue, or fc6's K-split finalize)
 BINARY_MACS_PER_IMAGE = (27 * 27 * 256 * 96 * 25 + 13 * 13 * 384 * 256 * 9 + 13 * 13 * 384 * 384 * 9
                          + 13 * 13 * 256 * 384 * 9 + 4096 * 256 * 36 + 4096 * 4096)
 

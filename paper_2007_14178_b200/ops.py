@@ -440,11 +440,14 @@ def xnor_conv(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor | None, p
 
 
 def xnor_conv_nhwc(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor, pad: int,
-                   out: torch.Tensor | None = None, out_affine=None) -> torch.Tensor:
+                   out: torch.Tensor | None = None, out_affine=None, emit: bool = False):
     """tcgen05 K3+K4 with y written channels-last: bits i32 [N,H,W,Cw], K f32
     [N,H',W'] -> y f32 [N,O,H',W'] in channels-last memory (the kernel writes
     [N][H'][W'][O] directly, xnc_xnor_conv_umma_nhwc).  Fully connected layers pass
-    the batch as a 1 x P image (N = 1, H = 1, W = P) and view y as [P, O]."""
+    the batch as a 1 x P image (N = 1, H = 1, W = P) and view y as [P, O].
+    emit=True (O % 32 == 0, O <= 4096) also returns the next binary layer's K1 of y,
+    (y, bits i32 [P, O/32], A f32 [P]) for the P = N*H'*W' pixels
+    (xnc_xnor_conv_umma_nhwc_emit)."""
     _need_cuda(bits, "bits", torch.int32)
     N, H, W, Cw = bits.shape
     if words(filt.C) != Cw or filt.wq is None:
@@ -460,6 +463,18 @@ def xnor_conv_nhwc(bits: torch.Tensor, filt: PackedFilters, K: torch.Tensor, pad
     osc, osh = _affine(out_affine, filt.O, bits.device, "out_affine")
     ws_bytes = lib().xnc_umma_split_ws_bytes(N, filt.C, H, W, filt.O, filt.kh, filt.kw, pad)
     split_ws = _split_ws(ws_bytes, bits.device) if ws_bytes else None
+    if emit:
+        if filt.O % 32 or filt.O > 4096:
+            raise ValueError("emit needs O % 32 == 0 and O <= 4096")
+        P = N * oh * ow
+        nb = torch.empty((P, filt.O // 32), dtype=torch.int32, device=bits.device)
+        nA = torch.empty((P,), dtype=torch.float32, device=bits.device)
+        check(lib().xnc_xnor_conv_umma_nhwc_emit(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(),
+                                                 K.data_ptr(), filt.alpha.data_ptr(), N, filt.C, H, W, filt.O,
+                                                 filt.kh, filt.kw, pad, _ptr(osc), _ptr(osh), _ptr(split_ws),
+                                                 out.data_ptr(), nb.data_ptr(), nA.data_ptr(), _stream(bits.device)),
+              "xnc_xnor_conv_umma_nhwc_emit")
+        return out, nb, nA
     check(lib().xnc_xnor_conv_umma_nhwc(bits.data_ptr(), filt.wq.data_ptr(), filt.sw.data_ptr(), K.data_ptr(),
                                         filt.alpha.data_ptr(), N, filt.C, H, W, filt.O, filt.kh, filt.kw, pad,
                                         _ptr(osc), _ptr(osh), _ptr(split_ws), out.data_ptr(), _stream(bits.device)),

@@ -487,6 +487,30 @@ def test_layer_forward_k1_matches_forward():
         ops.pack_input(x, in_pool=(3, 2), pool_bias=torch.zeros(63, device=_dev()))
 
 
+@pytest.mark.parametrize("shape", [(256, 256, 6, 4096, 6), (96, 128, 3, 512, 3), (2560, 256, 1, 1024, 1),
+                                   (64, 64, 2, 100, 2)], ids=lambda s: "x".join(map(str, s)))
+def test_fc_emit_matches_k1_of_output(shape):
+    """A fully connected layer handing the next layer its input in K1 form (sign words
+    + A of y * out_affine) gives exactly K1 of its float output: fused into the K-split
+    finalize (the first two shapes split), K1 after the conv when unsplit (2560 images),
+    and the generic fallback for a filter count that is not a multiple of 32."""
+    from paper_2007_14178_b200 import XnorConv2d, ops
+    n_img, c_in, side, n_out, k = shape
+    rng = np.random.default_rng(list(shape))
+    x = torch.from_numpy(O.f32_exact(rng, (n_img, c_in, side, side))).to(_dev())
+    w = torch.from_numpy(O.f32_exact(rng, (n_out, c_in, k, k))).to(_dev())
+    aff = (torch.rand(n_out, device=_dev()) + 0.5, torch.rand(n_out, device=_dev()) - 0.5)
+    layer = XnorConv2d(w, pad=0, variant="auto", out_affine=aff)
+    assert layer.kernel_for(x.shape) == "umma-fc"
+    y = layer.forward(x)
+    want_bits, want_A = ops.pack_input(y.contiguous())
+    bits, A = ops.pack_input(x)
+    p = layer.forward(ops.PackedInput(bits, A, c_in), emit_signs=True)
+    assert isinstance(p, ops.PackedInput) and p.C == n_out
+    assert torch.equal(p.bits.view(-1), want_bits.view(-1))
+    assert torch.equal(p.A.view(-1).view(torch.int32), want_A.view(-1).view(torch.int32))
+
+
 def test_layer_in_pool_matches_pooled_layer():
     """XnorConv2d(in_pool) on the pre-pool map == the same layer on the pooled map."""
     import torch.nn.functional as F

@@ -106,6 +106,15 @@ def case_fc_nhwc(rng):
     want = O.conv_layer(x, w, 0)
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy().reshape(want.shape).view(np.uint32), want.view(np.uint32))
+    # the fused finalize handing fc7 its K1 input (split) and its unsplit form
+    for (n_img, n_out) in ((96, 512), (2560, 1024)):
+        xe = torch.from_numpy(O.f32_exact(rng, (n_img, 64, 1, 1))).cuda()
+        le = XnorConv2d(torch.from_numpy(O.f32_exact(rng, (n_out, 64, 1, 1))).cuda(), pad=0)
+        ye = le.forward(xe)
+        wb, wa = ops.pack_input(ye.contiguous())
+        pe = le.forward(ops.PackedInput(*ops.pack_input(xe), 64), emit_signs=True)
+        torch.cuda.synchronize()
+        assert torch.equal(pe.bits.view(-1), wb.view(-1)) and torch.equal(pe.A.view(-1), wa.view(-1))
     x2, w2 = O.f32_exact(rng, (2, 64, 9, 11)), O.f32_exact(rng, (132, 64, 3, 3))
     a = XnorConv2d(torch.from_numpy(w2).cuda(), pad=1)(torch.from_numpy(x2).cuda())
     b = XnorConv2d(torch.from_numpy(w2).cuda(), pad=1, out_channels_last=True)(torch.from_numpy(x2).cuda())
