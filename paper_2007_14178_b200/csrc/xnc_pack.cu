@@ -387,25 +387,33 @@ int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int p
 // conv1's channels-last map -> max 3 x 3 / ps -> + bias -> ReLU -> conv2's folded BN
 // -> sign / A).  Laid out like the pool kernel (a thread per 4 channels of one pooled
 // pixel, nine float4 window loads, coalesced along the channels, many warps in flight:
-// that pass runs at HBM speed); a block takes kPoolPx pooled pixels x C/4 threads.
-// The pool's rule in window order, its bias and ReLU, then the affine as K1 applies
-// it; the sign nibbles are OR-reduced over 8-thread groups (one 32-channel word each:
-// C % 32 == 0, so groups never straddle pixels or warps) and the values staged
-// [C][kPoolPx + 1] for the per-pixel sequential |.| chains.  Saves the pooled map's
-// write and re-read (72 MB at batch 256) and one launch.
-constexpr int kPoolPx = 16;
-template <bool AFF>
-__global__ void __launch_bounds__(1024) k_pool_pack_nhwc(const float4* __restrict__ x, int C, int Hin, int Win,
-                                                        int Ho, int Wo, int ps, int relu, const float* __restrict__ bias,
-                                                        long npix, float inv, uint32_t* __restrict__ bits,
-                                                        float* __restrict__ A, const float* __restrict__ in_scale,
-                                                        const float* __restrict__ in_shift) {
-  extern __shared__ float tile[];  // [C][kPoolPx + 1]
-  constexpr int ld = kPoolPx + 1;
+// that pass runs at HBM speed); a block takes npx = 384 / (C/4) pooled pixels x C/4
+// threads (16 at conv2's 96 channels), at most 42 registers so that four blocks share
+// an SM (one block of 384 threads per 46-register SM slot ran 93-108 us, four 83 us at
+// batch 256, tools/pool_probe.py).  The pool's rule in window order, its bias and ReLU,
+// then the affine as K1 applies it; the sign nibbles are OR-reduced over 8-thread groups
+// (one 32-channel word each: C % 32 == 0, so groups never straddle pixels or warps) and
+// the values staged [C][npx + 1] for the per-pixel sequential |.| chains.  Saves the
+// pooled map's write and re-read (72 MB at batch 256) and one launch.
+constexpr int kPoolThreads = 384;
+// NPX > 0: the pixel count (and C = 4 * 384 / NPX) fixed at compile time -- conv2's 96
+// channels (16 pixels; 83 vs 87 us with the runtime form)
+template <bool AFF, int NPX>
+__global__ void __launch_bounds__(kPoolThreads, 4) k_pool_pack_nhwc(const float4* __restrict__ x, int C_rt, int Hin,
+                                                                   int Win, int Ho, int Wo, int ps, int relu,
+                                                                   const float* __restrict__ bias, long npix,
+                                                                   int npx_rt, float inv, uint32_t* __restrict__ bits,
+                                                                   float* __restrict__ A,
+                                                                   const float* __restrict__ in_scale,
+                                                                   const float* __restrict__ in_shift) {
+  extern __shared__ float tile[];  // [C][npx + 1]
+  const int npx = NPX > 0 ? NPX : npx_rt;
+  const int C = NPX > 0 ? 4 * kPoolThreads / NPX : C_rt;
+  const int ld = npx + 1;
   const int C4 = C >> 2, Cw = C >> 5;
   const int t = threadIdx.x, lane = t & 31;
   const int px = t / C4, c4 = t - px * C4;
-  const long q = (long)blockIdx.x * kPoolPx + px;
+  const long q = (long)blockIdx.x * npx + px;  // blockDim = (C/4) * npx: px < npx
   const bool in = q < npix;
   uint32_t nib = 0u;
   if (in) {
@@ -440,8 +448,8 @@ __global__ void __launch_bounds__(1024) k_pool_pack_nhwc(const float4* __restric
   wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
   if (in && (c4 & 7) == 0) bits[q * Cw + (c4 >> 3)] = wv;
   __syncthreads();
-  if (t < kPoolPx && A != nullptr) {
-    const long qa = (long)blockIdx.x * kPoolPx + t;
+  if (t < npx && A != nullptr) {
+    const long qa = (long)blockIdx.x * npx + t;
     if (qa < npix) {
       float s = 0.0f;
       int c = 0;
@@ -462,16 +470,18 @@ int launch_pack_input_pool_nhwc(const float* x, int N, int C, int Hin, int Win, 
                                 const float* bias, uint32_t* bits, float* A, cudaStream_t s, const float* in_scale,
                                 const float* in_shift) {
   if (pk != 3 || ps < 1 || Hin < pk || Win < pk) return XNC_ENOTSUP;
-  if ((C & 31) != 0 || C / 4 * kPoolPx > 1024 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) return XNC_ENOTSUP;
+  if ((C & 31) != 0 || C / 4 > kPoolThreads || (reinterpret_cast<uintptr_t>(x) & 15) != 0) return XNC_ENOTSUP;
+  const int npx = kPoolThreads / (C / 4);
   const int Ho = (Hin - pk) / ps + 1, Wo = (Win - pk) / ps + 1;
   const long npix = (long)N * Ho * Wo;
   if ((long)N * Hin * Win * C >= 0x7fffffffL * 4L) return XNC_ENOTSUP;
-  const size_t sm = (size_t)C * (kPoolPx + 1) * sizeof(float);
-  auto kern = in_scale ? k_pool_pack_nhwc<true> : k_pool_pack_nhwc<false>;
+  const size_t sm = (size_t)C * (npx + 1) * sizeof(float);
+  auto kern = C == 96 ? (in_scale ? k_pool_pack_nhwc<true, 16> : k_pool_pack_nhwc<false, 16>)
+                      : (in_scale ? k_pool_pack_nhwc<true, 0> : k_pool_pack_nhwc<false, 0>);
   if (int rc = smem_opt_in(kern, sm)) return rc;
-  kern<<<(unsigned)cdivl(npix, kPoolPx), (C / 4) * kPoolPx, sm, s>>>(
-      reinterpret_cast<const float4*>(x), C, Hin, Win, Ho, Wo, ps, relu, bias, npix, (float)(1.0 / (double)C), bits, A,
-      in_scale, in_shift);
+  kern<<<(unsigned)cdivl(npix, npx), (C / 4) * npx, sm, s>>>(reinterpret_cast<const float4*>(x), C, Hin, Win, Ho, Wo,
+                                                             ps, relu, bias, npix, npx, (float)(1.0 / (double)C), bits,
+                                                             A, in_scale, in_shift);
   return launch_status();
 }
 
