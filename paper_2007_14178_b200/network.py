@@ -116,7 +116,9 @@ class XnorNetAlexNet:
             in_pool = (3, 2) if name in POOLED_INPUT else None
             # (out_channels_last for conv2 / conv5, so their pools and the next K1 run
             # channels-last, measured no faster: the NHWC epilogue's per-pixel 64-byte runs
-            # cost what the coalesced pool saves; DESIGN 4b)
+            # cost what the coalesced pool saves; DESIGN 4b.  Again with the final fused
+            # channels-last pool + K1: C4 0.700 / 0.695 / 0.701 ms for conv2 / conv5 / both
+            # vs 0.694 NCHW)
             self.binary[name] = XnorConv2d(rnd(cout, cin, k, k), pad=pad, variant=variant,
                                            in_affine=in_aff, out_affine=out_aff, in_pool=in_pool)
         self.fc8_w = rnd(num_classes, 4096, scale=4096 ** -0.5)
