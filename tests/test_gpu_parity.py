@@ -440,13 +440,16 @@ def test_pooled_input_k1(shape):
         assert torch.equal(a1.view(torch.int32), a2.view(torch.int32))
 
 
-@pytest.mark.parametrize("shape", [(3, 96, 55, 55), (2, 64, 12, 11), (2, 32, 7, 9), (2, 40, 9, 9)],
+@pytest.mark.parametrize("shape", [(3, 96, 55, 55), (2, 64, 12, 11), (2, 32, 7, 9), (3, 256, 9, 13),
+                                   (2, 160, 11, 7), (2, 40, 9, 9)],
                          ids=lambda s: "x".join(map(str, s)))
 def test_pooled_input_k1_nhwc(shape):
     """The network front end's fused pass (xnc_pack_input_pool_nhwc): K1 of
     max_pool(x, 3, 2, relu, bias) on a channels-last map, with conv2's folded BN,
-    identical to pooling first (xnc_max_pool) and packing the pooled map; C = 40 is
-    not a multiple of 32 and takes that two-pass fallback."""
+    identical to pooling first (xnc_max_pool) and packing the pooled map.  96 channels
+    take the compile-time 16-pixel blocks, 32..256 the runtime pixel count (48 .. 6 per
+    block, 160 -> 9 pixels of 40 threads); C = 40 is not a multiple of 32 and takes the
+    two-pass fallback."""
     from paper_2007_14178_b200 import ops
     N, C, H, W = shape
     rng = np.random.default_rng(list(shape))
