@@ -187,10 +187,24 @@ __device__ __forceinline__ void umma_i8_pair_elect(uint32_t tmem_d, uint64_t ade
   "add.u32 al, %1, " #AO ";\n\tadd.u32 bl, %2, " #BO ";\n\tmov.b64 a, {al, %5};\n\t"   \
   "mov.b64 b, {bl, %5};\n\t" XNC_MMA_OP(D, P)
 // sf: TMEM address of the scale-factor columns (kind::mxf4; unused for kind::i8)
-template <int MH>
+// NKS < 4 (MH = 1 only): only the first NKS K = 32 steps of the chunk -- a layer whose one
+// K block is partly channel padding (conv2: C = 96 of 128) skips its all-zero steps.
+#define XNC_MMA_HEAD                                                                             \
+  "{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"                        \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
+#define XNC_MMA_ARGS ::"r"(d0), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "r"(hi), "r"(0u), "r"(sf)
+template <int MH, int NKS = 4>
 __device__ __forceinline__ void umma_chunk_pair(uint32_t d0, int np, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
                                                 uint32_t idesc, uint32_t acc, uint32_t sf) {
-  if constexpr (MH == 1) {
+  static_assert(NKS == 4 || MH == 1, "partial chunks are for MH = 1 kernels");
+  if constexpr (MH == 1 && NKS == 1) {
+    asm volatile(XNC_MMA_HEAD XNC_MMA1("%0", 0, 0, "p") "}" XNC_MMA_ARGS);
+  } else if constexpr (MH == 1 && NKS == 2) {
+    asm volatile(XNC_MMA_HEAD XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%0", 2, 2, "t") "}" XNC_MMA_ARGS);
+  } else if constexpr (MH == 1 && NKS == 3) {
+    asm volatile(XNC_MMA_HEAD XNC_MMA1("%0", 0, 0, "p") XNC_MMA1("%0", 2, 2, "t") XNC_MMA1("%0", 4, 4, "t") "}"
+                 XNC_MMA_ARGS);
+  } else if constexpr (MH == 1) {
     asm volatile(
         "{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
@@ -210,6 +224,8 @@ __device__ __forceinline__ void umma_chunk_pair(uint32_t d0, int np, uint32_t a_
 }
 #undef XNC_MMA1
 #undef XNC_MMA_OP
+#undef XNC_MMA_HEAD
+#undef XNC_MMA_ARGS
 
 #ifndef XNC_ST_HINT
 #define XNC_ST_HINT ".cs"
@@ -355,7 +371,7 @@ __device__ __forceinline__ int units_of(const PairGeom& g, int cluster, int n_cl
 // YPM: y written channels-last ([n][pixel][O], fully connected layers / NHWC maps);
 // a separate instantiation, so the NCHW epilogue's hot loop carries no branch for it
 // (a runtime flag there cost C3 ~5 % in ncu cycles).
-template <int MH, bool PROF, int AX, bool YPM = false>
+template <int MH, bool PROF, int AX, bool YPM = false, int NKS = 4>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarps + 32 * AX, 1) k_conv_umma_pair(
     const uint32_t* __restrict__ bits, const __grid_constant__ CUtensorMap b_map,
     const int32_t* __restrict__ sw, const float* __restrict__ Kmap, const float* __restrict__ alpha,
@@ -732,7 +748,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPEpiWarp
               g_umma_prof[512 + step / 8][2 * (step % 8)] = tw0 - t_start;
               g_umma_prof[512 + step / 8][2 * (step % 8) + 1] = tw1 - tw0;
             }
-            umma_chunk_pair<MH>(d0, g.NP, a_tap, b_lo0 + (st * kPCPS + j) * b16, hi, idesc, acc, sf_addr);
+            umma_chunk_pair<MH, NKS>(d0, g.NP, a_tap, b_lo0 + (st * kPCPS + j) * b16, hi, idesc, acc, sf_addr);
             acc = 1;
             if (PROF) n_mma += 4 * MH;
             if (++kx == g.kw) { kx = 0; a_tap += row_skip; } else { a_tap += 8u; }
@@ -1509,6 +1525,12 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
                                     : (g.debug ? k_conv_umma_pair<1, true, 4> : k_conv_umma_pair<1, false, 4>))
               : g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true, kPAExtra> : k_conv_umma_pair<2, false, kPAExtra>)
                           : (g.debug ? k_conv_umma_pair<1, true, kPAExtra> : k_conv_umma_pair<1, false, kPAExtra>);
+  // one K block that is partly channel padding (C <= 96 of 128): skip the all-zero K steps
+  // (a compile-time count, so the other layers' issue loop is untouched)
+  static const int part_k = getenv("XNC_PARTIAL_K") ? atoi(getenv("XNC_PARTIAL_K")) : 1;
+  if (part_k && g.KBn == 1 && C <= 96 && g.MH == 1 && !wide_a && kPAExtra == 0 && !y_pm && !g.debug)
+    kern = C <= 32 ? k_conv_umma_pair<1, false, 0, false, 1>
+                   : C <= 64 ? k_conv_umma_pair<1, false, 0, false, 2> : k_conv_umma_pair<1, false, 0, false, 3>;
   const int threads = kPThreads + (wide_a ? 32 * 4 : 0);
   if (int rc = smem_opt_in(kern, smem)) return rc;  // per device (xnc_runtime.cu)
   int32_t* part = g.S > 1 && (long)N * O * g.oh * g.ow < 0x7fffffffL ? split_ws : nullptr;

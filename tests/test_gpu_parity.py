@@ -240,7 +240,10 @@ UMMA_CASES = RANDOM_CASES + [(2, 256, 14, 14, 64, 3, 3, 1), (1, 128, 20, 20, 300
                              (2, 128, 8, 64, 256, 3, 3, 1), (3, 16, 2, 3, 256, 2, 2, 1),
                              # fewer work units than CTA pairs: K split over the pairs (4 and 3 K
                              # blocks), partial sums added in any order, then the finalize kernel
-                             (1, 512, 8, 8, 256, 3, 3, 1), (1, 384, 5, 5, 64, 3, 3, 1)]
+                             (1, 512, 8, 8, 256, 3, 3, 1), (1, 384, 5, 5, 64, 3, 3, 1),
+                             # one K block partly channel padding: 3 / 2 / 1 of its 4 K steps
+                             # issued (conv2's C = 96; the shapes above with C <= 64 too)
+                             (2, 96, 27, 27, 256, 5, 5, 2), (2, 80, 11, 13, 192, 3, 3, 1)]
 
 
 @pytest.mark.parametrize("shape", UMMA_CASES, ids=lambda s: "x".join(map(str, s)))

@@ -27,6 +27,7 @@ SHAPES = {
     # XNOR-Net AlexNet's binary layers at batch 256 (C4)
     "conv2": (256, 96, 27, 27, 256, 5),
     "conv3": (256, 256, 13, 13, 384, 3),
+    "conv4": (256, 384, 13, 13, 384, 3),
     "conv5": (256, 384, 13, 13, 256, 3),
     # fc6 / fc7 at batch 256 as the network runs them: one 1 x 256 image, 1 x 1 taps
     "fc6": (1, 9216, 1, 256, 4096, 1),
