@@ -15,7 +15,7 @@ x = (torch.rand((N, C, H, W), generator=g) * 2 - 1).pin_memory()
 w = (torch.rand((O, C, 3, 3), generator=g) * 2 - 1).cuda()
 layer = XnorConv2d(w, pad=1, variant="auto")
 out = torch.empty((N, O, H, W), dtype=torch.float32).pin_memory()
-for chunk in (8, 12, 16, 20, 24):
+for chunk in (4, 8, 12, 16, 32):
     for _ in range(2):
         layer.forward_host(x, out=out, chunk=chunk)
     torch.cuda.synchronize()
