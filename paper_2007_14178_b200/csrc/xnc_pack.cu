@@ -290,8 +290,10 @@ __device__ __forceinline__ float pool_pick(float m, float v) { return (v > m || 
 #ifndef XNC_POOL_KU
 #define XNC_POOL_KU 6  // 2 / 4 / 6 / 8: conv3's input 81 / 73 / 64 / 73 us at batch 256 (tools/pool_probe.py)
 #endif
-template <bool AFF, int PK>
-__global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict__ x, int C, int Hin, int Win,
+// NW warps per block (4; 8 when the grid is under two blocks per SM -- fc6's input at
+// batch 256 is 288 blocks: each warp's channel loop is half as long)
+template <bool AFF, int PK, int NW>
+__global__ void __launch_bounds__(NW * 32) k_pack_small_pool(const float* __restrict__ x, int C, int Hin, int Win,
                                                          int Ho, int Wo, int ps, int Cw, long npix, float inv,
                                                          uint32_t* __restrict__ bits, float* __restrict__ A,
                                                          const float* __restrict__ in_scale,
@@ -307,11 +309,11 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
   const float* xp = x + n * C * (long)Hin * Win + (long)(oy * ps) * Win + ox * ps;
   const long plane = (long)Hin * Win;
   constexpr int kU = XNC_POOL_KU;  // channels per thread per batch: kU * PK * PK loads in flight
-  for (int c0 = warp; c0 < C; c0 += 4 * kU) {
+  for (int c0 = warp; c0 < C; c0 += NW * kU) {
     float v[kU][PK * PK], sc[kU], sh[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int c = c0 + 4 * u;
+      const int c = c0 + NW * u;
       const float* b = xp + (long)c * plane;
 #pragma unroll
       for (int dy = 0; dy < PK; ++dy)
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int c = c0 + 4 * u;
+      const int c = c0 + NW * u;
       if (c < C) {
         float m = v[u][0];
 #pragma unroll
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(128) k_pack_small_pool(const float* __restrict
     for (int c = nb << 4; c < C; ++c) s = __fadd_rn(s, fabsf(tile[c * 32 + lane]));
     if (A) A[q] = __fmul_rn(s, inv);
   } else {
-    for (int j = warp - 1; j < Cw; j += 3) {
+    for (int j = warp - 1; j < Cw; j += NW - 1) {
       const int cend = min(32, C - 32 * j);
       uint32_t word = 0u;
 #pragma unroll 8
@@ -376,9 +378,11 @@ int launch_pack_input_pool(const float* x, int N, int C, int Hin, int Win, int p
   if (Ho * Wo < 32 || C < 32 || C > kSmallMaxC) return XNC_ENOTSUP;
   const int Cw = cdiv(C, 32);
   const size_t sm = (size_t)C * 32 * sizeof(float);
-  auto kern = in_scale ? k_pack_small_pool<true, 3> : k_pack_small_pool<false, 3>;
+  const bool wide = cdivl(npix, 32) < 2L * device_sm_count();
+  auto kern = wide ? (in_scale ? k_pack_small_pool<true, 3, 8> : k_pack_small_pool<false, 3, 8>)
+                   : (in_scale ? k_pack_small_pool<true, 3, 4> : k_pack_small_pool<false, 3, 4>);
   if (int rc = smem_opt_in(kern, sm)) return rc;  // per device (xnc_runtime.cu)
-  kern<<<(unsigned)cdivl(npix, 32), 128, sm, s>>>(x, C, Hin, Win, Ho, Wo, ps, Cw, npix, (float)(1.0 / (double)C),
+  kern<<<(unsigned)cdivl(npix, 32), wide ? 256 : 128, sm, s>>>(x, C, Hin, Win, Ho, Wo, ps, Cw, npix, (float)(1.0 / (double)C),
                                                   bits, A, in_scale, in_shift);
   return launch_status();
 }
