@@ -81,7 +81,7 @@ constexpr int kPEpiWarps = XNC_EPI_WARPS;  // multiple of 4 (one group per TMEM 
 constexpr int kPAExtra = XNC_A_WARPS_EXTRA;
 constexpr int kPThreads = 128 + 32 * kPEpiWarps + 32 * kPAExtra;
 #ifndef XNC_A_ROWS
-#define XNC_A_ROWS 4  // A producer: bit rows per thread per batch (x 2 planes) loaded before expanding
+#define XNC_A_ROWS 2  // A producer: bit rows per thread per batch (x 2 planes) loaded before expanding (1 / 2 / 3 / 4: profiles/umma_a_rows_ab_r5n.log)
 #endif
 #ifndef XNC_PSTAGES
 #define XNC_PSTAGES 6
