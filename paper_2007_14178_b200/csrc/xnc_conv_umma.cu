@@ -1525,13 +1525,19 @@ int launch_conv_umma(const uint32_t* bits, const uint8_t* wq, const int32_t* sw,
                                     : (g.debug ? k_conv_umma_pair<1, true, 4> : k_conv_umma_pair<1, false, 4>))
               : g.MH == 2 ? (g.debug ? k_conv_umma_pair<2, true, kPAExtra> : k_conv_umma_pair<2, false, kPAExtra>)
                           : (g.debug ? k_conv_umma_pair<1, true, kPAExtra> : k_conv_umma_pair<1, false, kPAExtra>);
+  // 256-filter blocks over several K blocks (C3): two more A-producer warps (C3 -1.5 %,
+  // profiles/umma_mid_a_ab_r6c.log); the 13 x 13 layers and the narrow ones keep theirs
+  static const int mid_env = getenv("XNC_MID_A") ? atoi(getenv("XNC_MID_A")) : 1;
+  const bool mid_a = mid_env && !wide_a && kPAExtra == 0 && g.MH == 1 && g.NP == 256 && g.taps > 1 &&
+                     g.KBn >= 2 && !g.debug && next_bits == nullptr;
+  if (mid_a) kern = y_pm ? k_conv_umma_pair<1, false, 2, true> : k_conv_umma_pair<1, false, 2>;
   // one K block that is partly channel padding (C <= 96 of 128): skip the all-zero K steps
   // (a compile-time count, so the other layers' issue loop is untouched)
   static const int part_k = getenv("XNC_PARTIAL_K") ? atoi(getenv("XNC_PARTIAL_K")) : 1;
   if (part_k && g.KBn == 1 && C <= 96 && g.MH == 1 && !wide_a && kPAExtra == 0 && !y_pm && !g.debug)
     kern = C <= 32 ? k_conv_umma_pair<1, false, 0, false, 1>
                    : C <= 64 ? k_conv_umma_pair<1, false, 0, false, 2> : k_conv_umma_pair<1, false, 0, false, 3>;
-  const int threads = kPThreads + (wide_a ? 32 * 4 : 0);
+  const int threads = kPThreads + (wide_a ? 32 * 4 : mid_a ? 32 * 2 : 0);
   if (int rc = smem_opt_in(kern, smem)) return rc;  // per device (xnc_runtime.cu)
   int32_t* part = g.S > 1 && (long)N * O * g.oh * g.ow < 0x7fffffffL ? split_ws : nullptr;
   if (g.S > 1 && part == nullptr) {  // no buffer usable: run unsplit
